@@ -1,0 +1,281 @@
+/* veq.h — C-ABI boundary of the B200-native equivalence-checker core.
+ *
+ * Replaces the hot section of the reference pipeline,
+ *   ctaeq::check_equivalence  /root/reference/proj/src/pipeline.cpp:273-336
+ * i.e. the two round-robin runs and the per-VC decision loop:
+ *   ctaeq::run(const Program&, const SharedMem&, const SchedulePolicy&)
+ *        proj/include/ctaeq/symexec.hpp:235-236, called at pipeline.cpp:276,292
+ *   ctaeq::eq(const Expr&, const Expr&, ...) — fast path only (cf == cg plus
+ *        side conditions), proj/src/decide.cpp:749-771, called at pipeline.cpp:320
+ * Everything above (parse, elaborate, validate, signature check) and below
+ * (aggregation, JSON, CLI) stays in host code. Plain C types only.
+ *
+ * Unit of work: a BATCH of independent CTA programs (one elaborated
+ * ctaeq::Program each, proj/include/ctaeq/ir.hpp:148-156), packed SoA.
+ * Threading: one veq_ctx per GPU; a ctx is not thread-safe; distinct ctxs
+ * may be used concurrently. Ownership: input buffers are caller-owned and
+ * copied; output buffers are ctx-owned and valid until the next call that
+ * produces the same kind of output on that ctx.
+ */
+#ifndef VEQ_H
+#define VEQ_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VEQ_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+  VEQ_OK = 0,
+  VEQ_E_BUDGET = 1,            /* term-table / arena capacity exhausted      */
+  VEQ_E_RATIONAL_OVERFLOW = 2, /* a coefficient left the exact int64 range   */
+  VEQ_E_OOM = 3,               /* device allocation failed                   */
+  VEQ_E_INVALID_IR = 4,        /* malformed batch                            */
+  VEQ_E_CUDA = 5,              /* CUDA runtime error (see veq_last_error)    */
+  VEQ_E_ARG = 6,               /* bad argument / handle                      */
+  VEQ_E_UNSUPPORTED = 7,       /* input outside the supported envelope       */
+  VEQ_E_NO_DEVICE = 8,         /* no CUDA device / extension unusable        */
+  VEQ_E_SCRATCH = 9            /* per-node canonicalisation scratch overflow */
+};
+
+/* ---- packed IR ---------------------------------------------------------
+ * Statement kinds/ops follow ctaeq::StmtKind / Bin / Un (ir.hpp:81-117). */
+enum { VEQ_ST_SETCONST = 0, VEQ_ST_BINOP = 1, VEQ_ST_UNOP = 2, VEQ_ST_COPY = 3,
+       VEQ_ST_LOAD = 4, VEQ_ST_STORE = 5, VEQ_ST_SYNC = 6 };
+enum { VEQ_BIN_ADD = 0, VEQ_BIN_MUL = 1, VEQ_BIN_DIV = 2, VEQ_BIN_MAX = 3 };
+enum { VEQ_UN_NEG = 0, VEQ_UN_EXP = 1 };
+enum { VEQ_ROLE_IN = 0, VEQ_ROLE_OUT = 1, VEQ_ROLE_SCRATCH = 2 };
+
+/* 16-byte statement.
+ *  SETCONST: dst, a = const-pool index, op = 1 for NEG_INF (a ignored)
+ *  BINOP:    dst, op, a, b (registers)      UNOP: dst, op, a
+ *  COPY:     dst, a = src register
+ *  LOAD:     dst, arr, a = (int32) offset   STORE: dst = SOURCE register, arr, a = offset
+ *  SYNC:     a = sync-set pool index
+ * Registers are dense PER THREAD (0 .. thread_nregs-1). */
+typedef struct veq_stmt {
+  uint8_t kind;
+  uint8_t op;
+  uint16_t arr;
+  uint32_t dst;
+  uint32_t a;
+  uint32_t b;
+} veq_stmt;
+
+typedef struct veq_array {
+  uint64_t size;      /* elements                                            */
+  uint32_t role;      /* VEQ_ROLE_*                                          */
+  uint32_t flags;     /* VEQ_ARR_STORED: some thread stores to it            */
+  int32_t input;      /* index into the session's input table, or -1        */
+  uint32_t seeded;    /* cells [0, seeded) start with input symbols          */
+} veq_array;
+#define VEQ_ARR_STORED 1u
+
+/* Exact rational constant, canonical (den > 0, gcd 1). */
+typedef struct veq_rat { int64_t num; int64_t den; } veq_rat;
+
+/* Sync set. full = every thread of the program; otherwise the set lives in
+ * one warp window: bit k of words[word_off ..] is thread lo + k, n_bits
+ * valid bits (validate_structured, proj/src/ir.cpp:276-325). */
+typedef struct veq_syncset {
+  uint32_t full;
+  uint32_t lo;
+  uint32_t n_bits;
+  uint32_t word_off;
+} veq_syncset;
+
+typedef struct veq_program_meta {
+  uint32_t n_threads;
+  uint32_t warp_size;  /* 0: none declared */
+  uint32_t thread_off; /* first global thread index of this program */
+  uint32_t array_off;  /* first array of this program in `arrays`   */
+  uint32_t n_arrays;
+  uint32_t pad;
+} veq_program_meta;
+
+/* A batch of n_progs programs. Global thread t of program p has statements
+ * stmts[thread_stmt[t] .. thread_stmt[t+1]). All pools are batch-global. */
+typedef struct veq_batch_desc {
+  uint32_t n_progs;
+  uint32_t n_threads_total;
+  uint64_t n_stmts;
+  uint32_t n_arrays_total;
+  uint32_t n_consts;
+  uint32_t n_syncsets;
+  uint32_t n_set_words;
+  const veq_program_meta *progs;     /* [n_progs]                 */
+  const uint64_t *thread_stmt;       /* [n_threads_total + 1]     */
+  const uint32_t *thread_nregs;      /* [n_threads_total]         */
+  const veq_stmt *stmts;             /* [n_stmts]                 */
+  const veq_array *arrays;           /* [n_arrays_total]          */
+  const veq_rat *consts;             /* [n_consts]                */
+  const veq_syncset *syncsets;       /* [n_syncsets]              */
+  const uint64_t *set_words;         /* [n_set_words]             */
+} veq_batch_desc;
+
+/* ---- session inputs ----------------------------------------------------
+ * The symbolic inputs of a check (ctaeq::make_symbolic_inputs,
+ * pipeline.cpp:200-212): array `name` cell i holds Var("<name>_<i>").
+ * Declaring them fixes the byte order of every input symbol (the order
+ * Expr::compare uses for Vars, expr.cpp:120) and starts a new term table. */
+typedef struct veq_input_desc {
+  const char *name;
+  uint64_t size;
+} veq_input_desc;
+
+typedef struct veq_limits {
+  uint64_t max_nodes;      /* term-table node capacity (0: default)     */
+  uint64_t max_kid_words;  /* kid arena capacity, u32 words (0: default) */
+  uint64_t scratch_bytes;  /* canonicalisation scratch pool (0: default) */
+} veq_limits;
+
+typedef struct veq_ctx veq_ctx;
+
+int veq_open(int device, const veq_limits *lim, veq_ctx **out);
+void veq_close(veq_ctx *ctx);
+const char *veq_strerror(int status);
+const char *veq_last_error(veq_ctx *ctx);
+
+/* Starts a new session: clears the term table and declares the inputs. */
+int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n);
+
+/* Copies a batch to the device; returns a batch handle (valid for the
+ * session). Host buffers may be freed afterwards. */
+int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *desc, uint32_t *batch);
+
+/* ---- run (K0 schedule, K3 executor, K4 race/uninit, K2 canonicalise) --- */
+enum { VEQ_FAULT_RACE = 1, VEQ_FAULT_SAFETY = 2 };
+enum { VEQ_SAFE_UNINIT_REG = 0, VEQ_SAFE_UNINIT_MEM = 1, VEQ_SAFE_OOB = 2,
+       VEQ_SAFE_INVALID_ARITH = 3 }; /* ctaeq::SafetyKind order */
+enum { VEQ_DETAIL_NONE = 0, VEQ_DETAIL_NEGINF_ADD, VEQ_DETAIL_NEGINF_MUL,
+       VEQ_DETAIL_NEGINF_NEG, VEQ_DETAIL_NEGINF_DIV, VEQ_DETAIL_NEGINF_EXP,
+       VEQ_DETAIL_ZERO_DEN };
+
+/* One fault. Races: (tid,stmt,step,is_write) is the access whose check
+ * failed ("second"); (tid2,stmt2,step2,is_write2) the recorded event
+ * ("first"). Safeties use tid/stmt/step; reg_slot says which source
+ * register (0 = a / store source, 1 = b) for uninitialised registers.
+ * stmt indices are batch-global; order key is (prog, step, sub). */
+typedef struct veq_fault {
+  uint8_t type;
+  uint8_t kind;     /* safety kind                                       */
+  uint8_t sub;      /* order within one statement                        */
+  uint8_t detail;   /* VEQ_DETAIL_*                                      */
+  uint8_t is_write;
+  uint8_t is_write2;
+  uint8_t reg_slot;
+  uint8_t pad;
+  uint32_t prog;
+  uint32_t tid;
+  uint32_t stmt;
+  uint32_t step;
+  uint32_t tid2;
+  uint32_t stmt2;
+  uint32_t step2;
+  int32_t offset;   /* memory faults: cell offset within `arr`           */
+  uint32_t arr;     /* memory faults: program-local array index          */
+} veq_fault;
+
+/* Per-program run summary (ctaeq::RunResult, symexec.hpp:214-225). */
+typedef struct veq_prog_result {
+  uint64_t steps;
+  uint32_t releases;
+  uint32_t n_faults;     /* faults (before host-side dedup)          */
+  uint32_t deadlocked;   /* 1: run ended with a thread not returned  */
+  uint32_t pad;
+} veq_prog_result;
+
+typedef struct veq_run_out {
+  uint32_t n_progs;
+  const veq_prog_result *progs;   /* [n_progs]                              */
+  uint64_t n_faults;
+  const veq_fault *faults;        /* unsorted; host sorts by (prog,step,sub) */
+  /* final thread states, for deadlock reports (state: 0 runnable,
+   * 1 blocked, 2 returned; blocked threads carry the sync set index and the
+   * batch-global statement index of the blocking Sync) */
+  uint32_t n_threads_total;
+  const uint8_t *thread_state;
+  const uint32_t *thread_block_set;
+  const uint64_t *thread_block_stmt;
+  /* device statistics of this call */
+  uint64_t n_nodes;               /* term-table nodes after the run */
+  uint64_t n_kid_words;
+  uint64_t n_work;                /* canonicalised raw nodes         */
+  uint64_t n_access;              /* race-check access tuples (R)    */
+} veq_run_out;
+
+int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out);
+
+/* ---- compare (K5) ------------------------------------------------------
+ * Programs a.progs[i] and b.progs[i] are compared cell by cell over their
+ * Out arrays in array-name order given by `out_order` (per program-pair,
+ * the program-local Out array indices of A then of B, sorted by name).
+ * One VC per Out cell; verdict bit: canonical forms identical (decide.cpp:
+ * 765-768). Side conditions (decide.cpp:482-491, 306-333) are returned as
+ * term-node ids with a positivity flag, in first-occurrence DFS order. */
+typedef struct veq_vc {
+  uint32_t node_a;       /* canonical node of kernel A's cell (or ~0: unset) */
+  uint32_t node_b;
+  uint32_t equal;        /* 1: structurally identical canonical forms        */
+  uint32_t sc_off;       /* side conditions [sc_off, sc_off + sc_n)           */
+  uint32_t sc_n;
+  uint32_t pad;
+} veq_vc;
+
+typedef struct veq_vc_out {
+  uint64_t n_vcs;
+  const veq_vc *vcs;
+  uint64_t n_sc;
+  const uint32_t *sc_node;       /* denominator node ids                    */
+  const uint8_t *sc_discharged;  /* positive_definite(denominator)          */
+  uint64_t n_equal;              /* device-side count of equal VCs          */
+  uint64_t n_missing;            /* Out cells never written (either side)   */
+} veq_vc_out;
+
+/* out_arrays: for program pair i, n_out_arrays[i] entries of
+ * (array index in A's program, array index in B's program), already in
+ * ascending array-name order (pipeline.cpp:120-130). */
+int veq_compare(veq_ctx *ctx, uint32_t batch_a, uint32_t batch_b,
+                const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
+                uint32_t n_out_per_pair, veq_vc_out *out);
+
+/* ---- DAG export (host to_string / slow path / reports) -----------------
+ * Exports the sub-DAG reachable from roots in canonical kid order. Nodes are
+ * renumbered densely 0..n-1 in post-order (kids first); root_index maps each
+ * root. Two-call protocol: call with buf->cap_* = 0 to size. */
+enum { VEQ_K_CONST = 0, VEQ_K_NEGINF, VEQ_K_VAR, VEQ_K_EXP, VEQ_K_MAX,
+       VEQ_K_DIV, VEQ_K_NEG, VEQ_K_MUL, VEQ_K_ADD }; /* ctaeq::Kind order */
+typedef struct veq_dag_node {
+  uint32_t kind;
+  uint32_t nkids;
+  uint64_t kid_off;   /* into kids[]                                      */
+  int64_t num;        /* Const                                             */
+  int64_t den;
+  int64_t var_input;  /* Var: input table index, or -1 for an undefined symbol */
+  uint64_t var_index; /* Var: cell index (input) or undef ordinal           */
+} veq_dag_node;
+
+typedef struct veq_dag_buf {
+  uint64_t cap_nodes, cap_kids;
+  veq_dag_node *nodes;   /* caller-allocated */
+  uint32_t *kids;
+  uint32_t *root_index;  /* [n_roots] */
+  uint64_t n_nodes, n_kids;  /* filled */
+} veq_dag_buf;
+
+int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots,
+                   veq_dag_buf *buf);
+
+/* ---- multi-GPU ---------------------------------------------------------
+ * Verdict counters are combined across ranks by the caller's collective
+ * (torch.distributed / NCCL all-reduce); the ctx exposes them as a small
+ * device-side vector so no host round trip is needed per rank. */
+int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]); /* equal, vcs, faults, missing */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,467 @@
+// ref_harness — TEST INFRASTRUCTURE ONLY (parity oracle + CPU baseline).
+//
+// Links the reference checker compiled from /root/reference/proj (see
+// oracle/Makefile) and:
+//   pair  OUTDIR A.mk B.mk CFG      elaborate both kernels with the REFERENCE
+//                                   frontend, write them as packed IR
+//                                   (a.veqir, b.veqir) plus golden.json: the
+//                                   reference's run() results for each side and
+//                                   its full check_equivalence report.
+//   gen   OUTDIR SEED               same for the reference's property-test
+//                                   program generator (tests/prog_gen.hpp).
+//   bench A.mk B.mk CFGLIST THREADS SECONDS
+//                                   CPU baseline: times the reference's own
+//                                   run(A) + run(B) + eq() per CTA pair (the
+//                                   t_exec_a + t_exec_b + t_decide span of
+//                                   pipeline.cpp:275-336) over the configs
+//                                   listed in CFGLIST, on THREADS host threads,
+//                                   until SECONDS elapse; prints JSON.
+// Nothing in the product links or calls this.
+#include <atomic>
+#include <chrono>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <thread>
+
+#include <json.hpp>
+
+#include "ctaeq/decide.hpp"
+#include "ctaeq/expr.hpp"
+#include "ctaeq/frontend.hpp"
+#include "ctaeq/ir.hpp"
+#include "ctaeq/pipeline.hpp"
+#include "ctaeq/symexec.hpp"
+#include "/root/reference/proj/tests/prog_gen.hpp"
+#include "veq_ir.hpp"
+
+using namespace ctaeq;
+using ojson = nlohmann::ordered_json;
+
+namespace {
+
+std::string read_file(const std::string &p) {
+  std::ifstream in(p, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open " + p);
+  std::ostringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
+}
+
+// ref Program -> packed IR (one program). `seeded` maps array name -> number
+// of cells that carry input symbols (from the init SharedMem).
+veq::HostBatch to_ir(const Program &p, const std::map<std::string, uint64_t> &seeded,
+                     const std::vector<std::string> &input_order) {
+  veq::HostBatch b;
+  veq_program_meta m{};
+  m.n_threads = p.n_threads;
+  m.warp_size = p.warp_size;
+  m.thread_off = 0;
+  m.array_off = 0;
+  m.n_arrays = (uint32_t)p.arrays.size();
+  b.progs.push_back(m);
+  b.prog_names.push_back(p.name);
+  std::map<std::string, uint16_t> arr_idx;
+  std::vector<bool> stored(p.arrays.size(), false);
+  for (size_t i = 0; i < p.arrays.size(); i++) arr_idx[p.arrays[i].name] = (uint16_t)i;
+  std::map<std::string, uint32_t> const_idx;
+  std::map<std::string, uint32_t> set_idx;
+  TidSet all = TidSet::full(p.n_threads);
+  for (Tid t = 0; t < p.n_threads; t++) {
+    std::map<std::string, uint32_t> regs;
+    std::vector<std::string> names;
+    auto reg = [&](const std::string &n) {
+      auto it = regs.find(n);
+      if (it != regs.end()) return it->second;
+      uint32_t id = (uint32_t)names.size();
+      regs[n] = id;
+      names.push_back(n);
+      return id;
+    };
+    for (const Stmt &s : p.threads[t].stmts) {
+      veq_stmt o{};
+      o.kind = (uint8_t)s.kind;
+      switch (s.kind) {
+      case StmtKind::SetConst: {
+        o.dst = reg(s.set_const.dst);
+        if (s.set_const.neg_infinity) {
+          o.op = 1;
+        } else {
+          std::string key = s.set_const.value.get_str();
+          auto it = const_idx.find(key);
+          if (it == const_idx.end()) {
+            Rat q = s.set_const.value;
+            if (!mpz_fits_slong(q.get_num()) || !mpz_fits_slong(q.get_den()))
+              throw std::runtime_error("constant out of int64 range");
+            b.consts.push_back({q.get_num().get_si(), q.get_den().get_si()});
+            it = const_idx.emplace(key, (uint32_t)b.consts.size() - 1).first;
+          }
+          o.a = it->second;
+        }
+        break;
+      }
+      case StmtKind::BinOp:
+        o.op = (uint8_t)s.bin_op.op;
+        o.a = reg(s.bin_op.a);
+        o.b = reg(s.bin_op.b);
+        o.dst = reg(s.bin_op.dst);
+        break;
+      case StmtKind::UnOp:
+        o.op = (uint8_t)s.un_op.op;
+        o.a = reg(s.un_op.a);
+        o.dst = reg(s.un_op.dst);
+        break;
+      case StmtKind::Copy:
+        o.a = reg(s.copy.src);
+        o.dst = reg(s.copy.dst);
+        break;
+      case StmtKind::Load:
+        o.arr = arr_idx.at(s.load.addr.array);
+        if (s.load.addr.offset < INT32_MIN || s.load.addr.offset > INT32_MAX)
+          throw std::runtime_error("offset out of int32 range");
+        o.a = (uint32_t)(int32_t)s.load.addr.offset;
+        o.dst = reg(s.load.dst);
+        break;
+      case StmtKind::Store:
+        o.arr = arr_idx.at(s.store.addr.array);
+        if (s.store.addr.offset < INT32_MIN || s.store.addr.offset > INT32_MAX)
+          throw std::runtime_error("offset out of int32 range");
+        o.a = (uint32_t)(int32_t)s.store.addr.offset;
+        o.dst = reg(s.store.src);
+        stored[o.arr] = true;
+        break;
+      case StmtKind::Sync: {
+        std::string key = s.sync.set.str();
+        auto it = set_idx.find(key);
+        if (it == set_idx.end()) {
+          veq_syncset q{};
+          if (s.sync.set == all) {
+            q.full = 1;
+            q.lo = 0;
+            q.n_bits = p.n_threads;
+          } else {
+            q.full = 0;
+            q.lo = s.sync.set.min_tid();
+            q.n_bits = s.sync.set.max_tid() - q.lo + 1;
+            q.word_off = (uint32_t)b.set_words.size();
+            std::vector<uint64_t> w((q.n_bits + 63) / 64, 0);
+            for (Tid x : s.sync.set.to_vector()) w[(x - q.lo) / 64] |= 1ull << ((x - q.lo) % 64);
+            b.set_words.insert(b.set_words.end(), w.begin(), w.end());
+          }
+          b.syncsets.push_back(q);
+          it = set_idx.emplace(key, (uint32_t)b.syncsets.size() - 1).first;
+        }
+        o.a = it->second;
+        break;
+      }
+      }
+      b.stmts.push_back(o);
+      b.locs.push_back({s.loc.line, s.loc.col});
+    }
+    b.thread_stmt.push_back(b.stmts.size());
+    b.thread_nregs.push_back((uint32_t)names.size());
+    b.reg_names.insert(b.reg_names.end(), names.begin(), names.end());
+    b.thread_reg_off.push_back(b.reg_names.size());
+  }
+  for (size_t i = 0; i < p.arrays.size(); i++) {
+    const ArrayDecl &a = p.arrays[i];
+    veq_array o{};
+    o.size = a.size;
+    o.role = (uint32_t)a.role;
+    o.flags = stored[i] ? VEQ_ARR_STORED : 0;
+    o.input = -1;
+    o.seeded = 0;
+    for (size_t k = 0; k < input_order.size(); k++)
+      if (input_order[k] == a.name) {
+        o.input = (int32_t)k;
+        o.seeded = (uint32_t)seeded.at(a.name);
+      }
+    b.arrays.push_back(o);
+    b.array_names.push_back(a.name);
+  }
+  return b;
+}
+
+ojson loc_j(const SrcLoc &l) { return ojson{{"line", l.line}, {"col", l.col}}; }
+
+ojson access_j(const AccessRef &a) {
+  return ojson{{"tid", a.tid}, {"access", access_kind_str(a.kind)}, {"loc", loc_j(a.loc)}, {"step", a.step}};
+}
+
+ojson safety_j(const SafetyReport &s) {
+  ojson j;
+  j["kind"] = safety_kind_str(s.kind);
+  j["tid"] = s.tid;
+  j["loc"] = loc_j(s.loc);
+  if (s.addr) {
+    j["array"] = s.addr->array;
+    j["offset"] = s.addr->offset;
+  }
+  j["reg"] = s.reg;
+  j["is_store"] = s.is_store;
+  j["detail"] = s.detail;
+  j["step"] = s.step;
+  return j;
+}
+
+ojson deadlock_j(const DeadlockReport &d) {
+  ojson j;
+  j["threads"] = ojson::array();
+  for (const auto &t : d.threads) {
+    ojson tj;
+    tj["tid"] = t.tid;
+    tj["state"] = thread_state_str(t.state);
+    if (t.waiting) tj["waiting"] = t.waiting->to_vector();
+    if (t.state == ThreadState::Blocked) tj["loc"] = loc_j(t.loc);
+    j["threads"].push_back(tj);
+  }
+  if (d.conflict_tids) {
+    j["conflict_tids"] = {d.conflict_tids->first, d.conflict_tids->second};
+    j["conflict_sets"] = {d.conflict_sets->first.to_vector(), d.conflict_sets->second.to_vector()};
+  }
+  j["str"] = d.str();
+  return j;
+}
+
+ojson run_j(const RunResult &rr) {
+  ojson j;
+  j["steps"] = rr.steps;
+  j["releases"] = rr.releases;
+  const char *ok[] = {"final", "race", "deadlock", "safety"};
+  j["outcome"] = ok[(int)rr.outcome.kind];
+  j["races"] = ojson::array();
+  for (const auto &r : rr.races) {
+    ojson x;
+    x["array"] = r.addr.array;
+    x["offset"] = r.addr.offset;
+    x["first"] = access_j(r.first);
+    x["second"] = access_j(r.second);
+    x["str"] = r.str();
+    j["races"].push_back(x);
+  }
+  j["safeties"] = ojson::array();
+  for (const auto &s : rr.safeties) {
+    ojson x = safety_j(s);
+    x["str"] = s.str();
+    j["safeties"].push_back(x);
+  }
+  j["deadlock"] = rr.deadlock ? deadlock_j(*rr.deadlock) : ojson(nullptr);
+  j["shared"] = ojson::object();
+  if (rr.outcome.kind == Outcome::Kind::Final)
+    for (const auto &[addr, v] : rr.outcome.shared) j["shared"][addr.str()] = to_string(v);
+  return j;
+}
+
+void write_json(const std::string &path, const ojson &j) {
+  std::ofstream out(path);
+  out << j.dump(1) << "\n";
+}
+
+ojson inputs_j(const std::vector<std::string> &order, const std::map<std::string, uint64_t> &sizes) {
+  ojson j = ojson::array();
+  for (auto &n : order) j.push_back({{"name", n}, {"size", sizes.at(n)}});
+  return j;
+}
+
+int cmd_pair(const std::string &dir, const std::string &pa_path, const std::string &pb_path,
+             const std::string &cfg_path) {
+  LaunchConfig cfg = parse_config(read_file(cfg_path));
+  CheckRequest req;
+  req.kernel_a_src = read_file(pa_path);
+  req.kernel_b_src = read_file(pb_path);
+  req.cfg = cfg;
+  ojson g;
+  // the reference's full pipeline report (minus timings)
+  Report rep = check_equivalence(req, 1);
+  ojson rj = report_to_json(rep);
+  rj.erase("timings");
+  g["report"] = rj;
+  Program pa, pb;
+  try {
+    pa = elaborate(parse_kernel(req.kernel_a_src), cfg, cfg.for_a());
+    validate_structured(pa);
+    pb = elaborate(parse_kernel(req.kernel_b_src), cfg, cfg.for_b());
+    validate_structured(pb);
+  } catch (const std::exception &e) {
+    g["elab_error"] = e.what();
+    write_json(dir + "/golden.json", g);
+    return 0;
+  }
+  SharedMem init = make_symbolic_inputs(cfg, pa.arrays);
+  std::vector<std::string> order;
+  std::map<std::string, uint64_t> sizes;
+  for (const auto &name : cfg.inputs)
+    for (const auto &a : pa.arrays)
+      if (a.name == name && !sizes.count(name)) {
+        order.push_back(name);
+        sizes[name] = a.size;
+      }
+  g["inputs"] = inputs_j(order, sizes);
+  to_ir(pa, sizes, order).save(dir + "/a.veqir");
+  to_ir(pb, sizes, order).save(dir + "/b.veqir");
+  RunResult ra = run(pa, init, SchedulePolicy::round_robin());
+  RunResult rb = run(pb, init, SchedulePolicy::round_robin());
+  g["run_a"] = run_j(ra);
+  g["run_b"] = run_j(rb);
+  // fast-path bit per VC: canonical structures identical (decide.cpp:765)
+  ojson fp = ojson::array();
+  if (ra.outcome.kind == Outcome::Kind::Final && rb.outcome.kind == Outcome::Kind::Final) {
+    std::vector<const ArrayDecl *> outs;
+    for (const auto &a : pa.arrays)
+      if (a.role == Role::Out) outs.push_back(&a);
+    std::sort(outs.begin(), outs.end(), [](auto *x, auto *y) { return x->name < y->name; });
+    for (auto *a : outs)
+      for (uint64_t i = 0; i < a->size; i++) {
+        Addr ad{a->name, (int64_t)i};
+        auto ia = ra.outcome.shared.find(ad), ib = rb.outcome.shared.find(ad);
+        ojson v;
+        v["array"] = a->name;
+        v["index"] = i;
+        if (ia == ra.outcome.shared.end() || ib == rb.outcome.shared.end()) {
+          v["missing"] = true;
+        } else {
+          Expr cf = canonicalize(ia->second), cg = canonicalize(ib->second);
+          v["fast_equal"] = (cf == cg);
+          std::vector<SideCondition> sc;
+          std::set<Expr> seen;
+          collect_side_conditions(cf, sc, seen);
+          collect_side_conditions(cg, sc, seen);
+          ojson scj = ojson::array();
+          for (auto &c : sc) scj.push_back({{"denominator", to_string(c.denominator)}, {"discharged", c.discharged}});
+          v["side_conditions"] = scj;
+        }
+        fp.push_back(v);
+      }
+  }
+  g["fast_path"] = fp;
+  write_json(dir + "/golden.json", g);
+  return 0;
+}
+
+int cmd_gen(const std::string &dir, uint64_t seed) {
+  auto gp = testutil::gen_program(seed);
+  std::vector<std::string> order;
+  std::map<std::string, uint64_t> sizes;
+  for (const auto &a : gp.prog.arrays) {
+    order.push_back(a.name);
+    sizes[a.name] = a.size;
+  }
+  ojson g;
+  g["inputs"] = inputs_j(order, sizes);
+  to_ir(gp.prog, sizes, order).save(dir + "/a.veqir");
+  RunResult r = run(gp.prog, gp.inputs, SchedulePolicy::round_robin());
+  g["run_a"] = run_j(r);
+  write_json(dir + "/golden.json", g);
+  return 0;
+}
+
+// CPU baseline: per CTA pair, time run(A)+run(B)+eq over all Out cells.
+int cmd_bench(const std::string &pa_path, const std::string &pb_path, const std::string &list_path,
+              unsigned threads, double seconds) {
+  std::string sa = read_file(pa_path), sb = read_file(pb_path);
+  KernelAst ka = parse_kernel(sa), kb = parse_kernel(sb);
+  std::vector<std::string> cfgs;
+  {
+    std::ifstream in(list_path);
+    std::string line;
+    while (std::getline(in, line))
+      if (!line.empty()) cfgs.push_back(read_file(line));
+  }
+  struct Job {
+    Program pa, pb;
+    SharedMem init;
+    uint64_t n_out = 0;
+  };
+  // elaboration is t_parse in the reference (excluded from the metric)
+  auto tp0 = std::chrono::steady_clock::now();
+  std::vector<Job> jobs(cfgs.size());
+  std::atomic<size_t> next{0};
+  auto elab = [&]() {
+    for (size_t i; (i = next++) < jobs.size();) {
+      LaunchConfig c = parse_config(cfgs[i]);
+      jobs[i].pa = elaborate(ka, c, c.for_a());
+      jobs[i].pb = elaborate(kb, c, c.for_b());
+      jobs[i].init = make_symbolic_inputs(c, jobs[i].pa.arrays);
+      for (auto &a : jobs[i].pa.arrays)
+        if (a.role == Role::Out) jobs[i].n_out += a.size;
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < threads; t++) th.emplace_back(elab);
+    for (auto &x : th) x.join();
+  }
+  double t_parse = std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count();
+  std::atomic<size_t> cursor{0};
+  std::atomic<uint64_t> done_elems{0}, done_pairs{0}, equal{0};
+  std::mutex mu;
+  double busy = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  auto worker = [&]() {
+    double my = 0;
+    for (;;) {
+      double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > seconds) break;
+      size_t i = cursor++;
+      if (i >= jobs.size()) break;
+      Job &j = jobs[i];
+      auto s0 = std::chrono::steady_clock::now();
+      RunResult ra = run(j.pa, j.init, SchedulePolicy::round_robin());
+      RunResult rb = run(j.pb, j.init, SchedulePolicy::round_robin());
+      uint64_t eqn = 0;
+      if (ra.outcome.kind == Outcome::Kind::Final && rb.outcome.kind == Outcome::Kind::Final)
+        for (auto &a : j.pa.arrays)
+          if (a.role == Role::Out)
+            for (uint64_t k = 0; k < a.size; k++) {
+              Addr ad{a.name, (int64_t)k};
+              auto ia = ra.outcome.shared.find(ad), ib = rb.outcome.shared.find(ad);
+              if (ia == ra.outcome.shared.end() || ib == rb.outcome.shared.end()) continue;
+              Verdict v = eq(ia->second, ib->second, DecideBudget{}, 0, 64);
+              if (v.kind == VerdictKind::Equal) eqn++;
+            }
+      clear_canon_cache();
+      my += std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count();
+      done_elems += j.n_out;
+      done_pairs++;
+      equal += eqn;
+    }
+    std::lock_guard<std::mutex> g(mu);
+    busy += my;
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < threads; t++) th.emplace_back(worker);
+  for (auto &x : th) x.join();
+  double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  ojson o;
+  o["pairs"] = done_pairs.load();
+  o["pairs_total"] = jobs.size();
+  o["elements"] = done_elems.load();
+  o["equal"] = equal.load();
+  o["wall_s"] = wall;
+  o["busy_s"] = busy;
+  o["threads"] = threads;
+  o["t_parse_s"] = t_parse;
+  o["elements_per_s"] = wall > 0 ? done_elems.load() / wall : 0.0;
+  std::cout << o.dump() << std::endl;
+  return 0;
+}
+
+} // namespace
+
+int main(int argc, char **argv) {
+  try {
+    std::string cmd = argc > 1 ? argv[1] : "";
+    if (cmd == "pair" && argc == 6) return cmd_pair(argv[2], argv[3], argv[4], argv[5]);
+    if (cmd == "gen" && argc == 4) return cmd_gen(argv[2], std::stoull(argv[3]));
+    if (cmd == "bench" && argc == 7)
+      return cmd_bench(argv[2], argv[3], argv[4], (unsigned)std::stoul(argv[5]), std::stod(argv[6]));
+    std::cerr << "usage: ref_harness pair OUTDIR A.mk B.mk CFG | gen OUTDIR SEED | "
+                 "bench A.mk B.mk CFGLIST THREADS SECONDS\n";
+    return 4;
+  } catch (const std::exception &e) {
+    std::cerr << "ref_harness: " << e.what() << "\n";
+    return 4;
+  }
+}

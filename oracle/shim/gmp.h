@@ -45,6 +45,7 @@ void __gmpz_pow_ui(mpz_ptr, mpz_srcptr, unsigned long);
 size_t __gmpz_sizeinbase(mpz_srcptr, int);
 mp_limb_t __gmpz_getlimbn(mpz_srcptr, mp_size_t);
 size_t __gmpz_size(mpz_srcptr);
+int __gmpz_fits_slong_p(mpz_srcptr);
 
 void __gmpq_init(mpq_ptr);
 void __gmpq_clear(mpq_ptr);
@@ -88,6 +89,7 @@ int __gmpq_equal(mpq_srcptr, mpq_srcptr);
 #define mpz_pow_ui __gmpz_pow_ui
 #define mpz_sizeinbase __gmpz_sizeinbase
 #define mpz_getlimbn __gmpz_getlimbn
+#define mpz_fits_slong_p __gmpz_fits_slong_p
 #define mpz_size(z) ((size_t)((z)->_mp_size < 0 ? -(z)->_mp_size : (z)->_mp_size))
 #define mpz_sgn(z) ((z)->_mp_size < 0 ? -1 : (z)->_mp_size > 0)
 

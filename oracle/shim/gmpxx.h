@@ -71,6 +71,7 @@ public:
   friend mpz_class gcd(const mpz_class &a, const mpz_class &b) { mpz_class r; mpz_gcd(r.z_, a.z_, b.z_); return r; }
   friend mpz_class lcm(const mpz_class &a, const mpz_class &b) { mpz_class r; mpz_lcm(r.z_, a.z_, b.z_); return r; }
   friend std::ostream &operator<<(std::ostream &os, const mpz_class &a) { return os << a.get_str(); }
+  friend bool mpz_fits_slong(const mpz_class &a) { return mpz_fits_slong_p(a.get_mpz_t()) != 0; }
 
 private:
   mpz_t z_;
