@@ -209,6 +209,14 @@ typedef struct veq_run_out {
 
 int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out);
 
+/* Final shared-memory contents after veq_run (the Final payload of
+ * ctaeq::Outcome, symexec.hpp:155): canonical term node of each cell of
+ * program `prog`'s array `array` (program-local index), or 0xFFFFFFFF when
+ * the cell holds no value. Cells of read-only input arrays report
+ * 0xFFFFFFFF too; they hold their input symbol by definition. */
+int veq_fetch_cells(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t array,
+                    uint32_t *out_nodes, uint64_t n);
+
 /* ---- compare (K5) ------------------------------------------------------
  * Programs a.progs[i] and b.progs[i] are compared cell by cell over their
  * Out arrays in array-name order given by `out_order` (per program-pair,

@@ -1,0 +1,835 @@
+// veq_api.cu — C-ABI implementation (include/veq.h): device memory,
+// batch preparation and the launch sequence of one check.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "veq_kernels.cuh"
+
+using namespace veqd;
+
+namespace {
+
+const char *kErr[] = {"ok",
+                      "term table or arena capacity exhausted",
+                      "rational coefficient overflow (outside exact int64 range)",
+                      "device out of memory",
+                      "invalid IR",
+                      "CUDA error",
+                      "bad argument",
+                      "unsupported input",
+                      "no CUDA device",
+                      "canonicalisation scratch exhausted"};
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t n = 0;
+};
+
+struct BatchDev {
+  // host copies needed for reports / compare
+  std::vector<veq_program_meta> progs;
+  std::vector<veq_array> arrays;
+  std::vector<uint64_t> arr_cell_base;
+  std::vector<uint64_t> thread_stmt;
+  uint64_t n_stmts = 0, n_cells = 0, n_segs = 0, n_rel_cap = 0, n_regs = 0, n_access_max = 0;
+  uint32_t n_threads = 0;
+  // device arrays (owned)
+  std::vector<void *> owned;
+  Batch B{};
+  // host-visible run results
+  std::vector<veq_prog_result> res;
+  std::vector<veq_fault> faults;
+  std::vector<uint8_t> th_state;
+  std::vector<uint32_t> th_bset;
+  std::vector<uint64_t> th_bstmt;
+  bool ran = false;
+};
+
+}  // namespace
+
+struct veq_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  Table T{};
+  veq_limits lim{};
+  // term table storage
+  Node *nodes = nullptr;
+  uint32_t *kids = nullptr, *slots = nullptr;
+  unsigned long long *counters = nullptr;
+  int *error = nullptr;
+  uint32_t *session_ids = nullptr;
+  uint64_t *in_base = nullptr, *in_size = nullptr;
+  uint64_t n_slots = 0;
+  // scratch pool
+  char *pool = nullptr;
+  unsigned long long *pool_used = nullptr;
+  uint64_t pool_cap = 0;
+  // session
+  std::vector<std::string> input_names;
+  std::vector<uint64_t> input_sizes;
+  std::vector<BatchDev *> batches;
+  // compare outputs
+  std::vector<veq_vc> vcs;
+  std::vector<uint32_t> sc_node;
+  std::vector<uint8_t> sc_dis;
+  uint64_t last_equal = 0, last_missing = 0, last_vcs = 0, last_faults = 0;
+};
+
+namespace {
+
+int fail(veq_ctx *c, int code, const std::string &msg) {
+  if (c) c->last_error = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) return fail(ctx, VEQ_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class X> int dalloc(veq_ctx *ctx, BatchDev *bd, X **out, size_t n) {
+  void *p = nullptr;
+  size_t bytes = std::max<size_t>(n, 1) * sizeof(X);
+  cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+  if (e != cudaSuccess) return fail(ctx, VEQ_E_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  if (bd) bd->owned.push_back(p);
+  *out = reinterpret_cast<X *>(p);
+  return VEQ_OK;
+}
+template <class X> int dupload(veq_ctx *ctx, BatchDev *bd, X **out, const X *src, size_t n) {
+  int r = dalloc(ctx, bd, out, n);
+  if (r) return r;
+  if (n) {
+    cudaError_t e = cudaMemcpyAsync(*out, src, n * sizeof(X), cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return fail(ctx, VEQ_E_CUDA, cudaGetErrorString(e));
+  }
+  return VEQ_OK;
+}
+
+uint32_t blocks(uint64_t n, uint32_t b) { return (uint32_t)((n + b - 1) / b); }
+
+int check_error_flag(veq_ctx *ctx) {
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, ctx->error, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (h) {
+    if (h == E_BUDGET) return fail(ctx, VEQ_E_BUDGET, "term table / arena capacity exhausted");
+    if (h == E_OVERFLOW) return fail(ctx, VEQ_E_RATIONAL_OVERFLOW, "rational coefficient overflow");
+    if (h == E_SCRATCH) return fail(ctx, VEQ_E_SCRATCH, "canonicalisation scratch exhausted");
+    return fail(ctx, VEQ_E_INVALID_IR, "internal invariant violated on device (code " + std::to_string(h) + ")");
+  }
+  return VEQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *veq_strerror(int s) {
+  if (s >= 0 && s < (int)(sizeof(kErr) / sizeof(kErr[0]))) return kErr[s];
+  return "unknown status";
+}
+
+const char *veq_last_error(veq_ctx *ctx) { return ctx ? ctx->last_error.c_str() : "null ctx"; }
+
+int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
+  if (!out) return VEQ_E_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return VEQ_E_NO_DEVICE;
+  if (device < 0 || device >= ndev) return VEQ_E_ARG;
+  veq_ctx *ctx = new veq_ctx();
+  ctx->device = device;
+  if (lim) ctx->lim = *lim;
+  if (!ctx->lim.max_nodes) ctx->lim.max_nodes = 64ull << 20;
+  if (!ctx->lim.max_kid_words) ctx->lim.max_kid_words = 256ull << 20;
+  if (!ctx->lim.scratch_bytes) ctx->lim.scratch_bytes = 4ull << 30;
+  if (ctx->lim.max_nodes >= (1ull << 31)) ctx->lim.max_nodes = (1ull << 31) - 1;
+  auto bail = [&](int code, const char *what) {
+    fprintf(stderr, "veq_open: %s\n", what);
+    delete ctx;
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(VEQ_E_CUDA, "cudaSetDevice");
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(VEQ_E_CUDA, "stream");
+  uint64_t slots = 1;
+  while (slots < ctx->lim.max_nodes * 2) slots <<= 1;
+  ctx->n_slots = slots;
+  if (cudaMalloc(&ctx->nodes, ctx->lim.max_nodes * sizeof(Node)) != cudaSuccess) return bail(VEQ_E_OOM, "nodes");
+  if (cudaMalloc(&ctx->kids, ctx->lim.max_kid_words * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "kids");
+  if (cudaMalloc(&ctx->slots, slots * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "slots");
+  if (cudaMalloc(&ctx->counters, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "counters");
+  if (cudaMalloc(&ctx->error, sizeof(int)) != cudaSuccess) return bail(VEQ_E_OOM, "error");
+  if (cudaMalloc(&ctx->session_ids, 4 * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "ids");
+  ctx->pool_cap = ctx->lim.scratch_bytes;
+  if (cudaMalloc(&ctx->pool, ctx->pool_cap) != cudaSuccess) return bail(VEQ_E_OOM, "scratch pool");
+  if (cudaMalloc(&ctx->pool_used, sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "pool ctr");
+  Table &T = ctx->T;
+  T.nodes = ctx->nodes;
+  T.kids = ctx->kids;
+  T.slots = ctx->slots;
+  T.counters = ctx->counters;
+  T.max_nodes = ctx->lim.max_nodes;
+  T.max_kids = ctx->lim.max_kid_words;
+  T.slot_mask = slots - 1;
+  T.error = ctx->error;
+  *out = ctx;
+  // an empty session so the ctx is usable without declared inputs
+  return veq_declare_inputs(ctx, nullptr, 0);
+}
+
+void veq_close(veq_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (BatchDev *b : ctx->batches) {
+    for (void *p : b->owned) cudaFreeAsync(p, ctx->stream);
+    delete b;
+  }
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->nodes);
+  cudaFree(ctx->kids);
+  cudaFree(ctx->slots);
+  cudaFree(ctx->counters);
+  cudaFree(ctx->error);
+  cudaFree(ctx->session_ids);
+  cudaFree(ctx->pool);
+  cudaFree(ctx->pool_used);
+  cudaFree(ctx->in_base);
+  cudaFree(ctx->in_size);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
+  if (!ctx) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  // drop batches of the previous session
+  for (BatchDev *b : ctx->batches) {
+    for (void *p : b->owned) cudaFreeAsync(p, ctx->stream);
+    delete b;
+  }
+  ctx->batches.clear();
+  ctx->input_names.clear();
+  ctx->input_sizes.clear();
+  // Byte order of "<name>_<i>" symbols: groups "<name>_" in byte order, then
+  // the decimal-string order inside a group (lexrank on the device). Exact
+  // unless one group string is a proper prefix of another ("x_" / "x_1_").
+  std::vector<std::string> g(n);
+  for (uint32_t i = 0; i < n; i++) {
+    if (!inputs[i].name) return fail(ctx, VEQ_E_ARG, "null input name");
+    ctx->input_names.push_back(inputs[i].name);
+    ctx->input_sizes.push_back(inputs[i].size);
+    g[i] = std::string(inputs[i].name) + "_";
+  }
+  for (uint32_t i = 0; i < n; i++)
+    for (uint32_t j = 0; j < n; j++)
+      if (i != j && g[j].size() > g[i].size() && g[j].compare(0, g[i].size(), g[i]) == 0)
+        return fail(ctx, VEQ_E_UNSUPPORTED, "input array names " + g[i] + " / " + g[j] + " interleave in byte order");
+  std::vector<uint32_t> ord(n);
+  for (uint32_t i = 0; i < n; i++) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) { return g[a] < g[b]; });
+  std::vector<uint64_t> base(n ? n : 1, 0), size(n ? n : 1, 0);
+  uint64_t acc = 0;
+  for (uint32_t k = 0; k < n; k++) {
+    base[ord[k]] = acc;
+    acc += inputs[ord[k]].size;
+  }
+  for (uint32_t i = 0; i < n; i++) size[i] = inputs[i].size;
+  if (acc >= (1ull << 43)) return fail(ctx, VEQ_E_UNSUPPORTED, "too many input symbols");
+  cudaFree(ctx->in_base);
+  cudaFree(ctx->in_size);
+  CK(cudaMalloc(&ctx->in_base, base.size() * 8));
+  CK(cudaMalloc(&ctx->in_size, size.size() * 8));
+  CK(cudaMemcpyAsync(ctx->in_base, base.data(), base.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->in_size, size.data(), size.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  Table &T = ctx->T;
+  T.in_base = ctx->in_base;
+  T.in_size = ctx->in_size;
+  T.n_inputs = n;
+  // fresh term table
+  CK(cudaMemsetAsync(ctx->slots, 0xff, ctx->n_slots * sizeof(uint32_t), ctx->stream));
+  CK(cudaMemsetAsync(ctx->counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), ctx->stream));
+  k_session_init<<<1, 32, 0, ctx->stream>>>(T, ctx->session_ids);
+  CK(cudaGetLastError());
+  uint32_t ids[4];
+  CK(cudaMemcpyAsync(ids, ctx->session_ids, sizeof(ids), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  T.id_neginf = ids[0];
+  T.id_zero = ids[1];
+  T.id_one = ids[2];
+  T.id_mone = ids[3];
+  return VEQ_OK;
+}
+
+int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
+  if (!ctx || !d || !out) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  const uint32_t P = d->n_progs, Tn = d->n_threads_total;
+  const uint64_t S = d->n_stmts;
+  if (S >= (1ull << 31)) return fail(ctx, VEQ_E_UNSUPPORTED, "batch has more than 2^31 statements");
+  BatchDev *bd = new BatchDev();
+  bd->progs.assign(d->progs, d->progs + P);
+  bd->arrays.assign(d->arrays, d->arrays + d->n_arrays_total);
+  bd->thread_stmt.assign(d->thread_stmt, d->thread_stmt + Tn + 1);
+  bd->n_stmts = S;
+  bd->n_threads = Tn;
+  // ---- host preparation: thread->program, segments, canonical sync ids,
+  // release capacities, register offsets, cell bases
+  std::vector<uint32_t> thread_prog(Tn);
+  std::vector<uint64_t> seg_off(Tn + 1, 0), reg_off(Tn + 1, 0), rel_off(P + 1, 0);
+  std::vector<uint64_t> seg_start;
+  std::vector<uint32_t> seg_set, prog_full(P, UNSET);
+  uint64_t n_access = 0;
+  for (uint32_t p = 0; p < P; p++) {
+    const veq_program_meta &m = d->progs[p];
+    if (m.thread_off + m.n_threads > Tn || m.array_off + m.n_arrays > d->n_arrays_total) {
+      delete bd;
+      return fail(ctx, VEQ_E_INVALID_IR, "program " + std::to_string(p) + " out of range");
+    }
+    std::map<std::vector<uint64_t>, uint32_t> canon_sets;  // content -> canonical pool id
+    uint64_t nsync = 0;
+    for (uint32_t t = 0; t < m.n_threads; t++) {
+      uint32_t gt = m.thread_off + t;
+      thread_prog[gt] = p;
+      reg_off[gt + 1] = d->thread_nregs[gt];
+      uint64_t s0 = d->thread_stmt[gt], s1 = d->thread_stmt[gt + 1];
+      seg_start.push_back(s0);
+      for (uint64_t i = s0; i < s1; i++) {
+        const veq_stmt &st = d->stmts[i];
+        if (st.kind > VEQ_ST_SYNC) {
+          delete bd;
+          return fail(ctx, VEQ_E_INVALID_IR, "bad statement kind");
+        }
+        if ((st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE) && st.arr >= m.n_arrays) {
+          delete bd;
+          return fail(ctx, VEQ_E_INVALID_IR, "array index out of range");
+        }
+        if (st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE) n_access++;
+        if (st.kind == VEQ_ST_SYNC) {
+          if (st.a >= d->n_syncsets) {
+            delete bd;
+            return fail(ctx, VEQ_E_INVALID_IR, "sync set index out of range");
+          }
+          const veq_syncset &q = d->syncsets[st.a];
+          std::vector<uint64_t> key;
+          bool is_full = q.full != 0;
+          if (!is_full) {
+            // a window set covering every thread is the full set
+            uint64_t cnt = 0;
+            for (uint32_t k = 0; k < q.n_bits; k++)
+              if ((d->set_words[q.word_off + k / 64] >> (k % 64)) & 1ull) cnt++;
+            is_full = (cnt == m.n_threads);
+            key.push_back(q.lo);
+            key.push_back(q.n_bits);
+            for (uint32_t w = 0; w < (q.n_bits + 63) / 64; w++) key.push_back(d->set_words[q.word_off + w]);
+          }
+          uint32_t cid;
+          if (is_full) {
+            if (prog_full[p] == UNSET) prog_full[p] = st.a;
+            cid = prog_full[p];
+          } else {
+            auto it = canon_sets.find(key);
+            if (it == canon_sets.end()) it = canon_sets.emplace(key, st.a).first;
+            cid = it->second;
+          }
+          seg_set.push_back(cid);
+          seg_start.push_back(i + 1);
+          nsync++;
+        }
+      }
+      seg_set.push_back(UNSET);  // last segment has no ending sync
+      seg_off[gt + 1] = seg_start.size();
+    }
+    rel_off[p + 1] = rel_off[p] + nsync;
+  }
+  for (uint32_t t = 0; t < Tn; t++) reg_off[t + 1] += reg_off[t];
+  std::vector<uint64_t> cell_base(d->n_arrays_total, UNSET64);
+  uint64_t cells = 0;
+  for (uint32_t a = 0; a < d->n_arrays_total; a++) {
+    const veq_array &ar = d->arrays[a];
+    bool direct = !(ar.flags & VEQ_ARR_STORED) && ar.input >= 0 && ar.seeded >= ar.size;
+    if (ar.input >= (int32_t)ctx->input_names.size()) {
+      delete bd;
+      return fail(ctx, VEQ_E_INVALID_IR, "array refers to an undeclared input");
+    }
+    if (!direct) {
+      cell_base[a] = cells;
+      cells += ar.size;
+    }
+  }
+  if (cells >= (1ull << 32)) {
+    delete bd;
+    return fail(ctx, VEQ_E_UNSUPPORTED, "more than 2^32 checked memory cells in one batch");
+  }
+  bd->arr_cell_base = cell_base;
+  bd->n_cells = cells;
+  bd->n_segs = seg_start.size();
+  bd->n_rel_cap = rel_off[P];
+  bd->n_regs = reg_off[Tn];
+  bd->n_access_max = n_access;
+  // ---- upload
+  Batch &B = bd->B;
+  B.n_progs = P;
+  B.n_threads = Tn;
+  B.n_stmts = S;
+  B.n_cells = cells;
+  int r = 0;
+#define UP(field, src, n, T_)                                                            \
+  do {                                                                                   \
+    T_ *p_ = nullptr;                                                                    \
+    if ((r = dupload(ctx, bd, &p_, (const T_ *)(src), (n)))) { delete bd; return r; }   \
+    B.field = p_;                                                                        \
+  } while (0)
+  UP(progs, d->progs, P, veq_program_meta);
+  UP(thread_stmt, d->thread_stmt, Tn + 1, uint64_t);
+  UP(thread_prog, thread_prog.data(), Tn, uint32_t);
+  UP(stmts, d->stmts, S, veq_stmt);
+  UP(arrays, d->arrays, d->n_arrays_total, veq_array);
+  UP(arr_cell_base, cell_base.data(), cell_base.size(), uint64_t);
+  UP(sets, d->syncsets, d->n_syncsets, veq_syncset);
+  UP(set_words, d->set_words, d->n_set_words, uint64_t);
+  UP(seg_off, seg_off.data(), Tn + 1, uint64_t);
+  UP(seg_start, seg_start.data(), seg_start.size(), uint64_t);
+  UP(seg_set, seg_set.data(), seg_set.size(), uint32_t);
+  UP(rel_off, rel_off.data(), P + 1, uint64_t);
+  UP(reg_off, reg_off.data(), Tn + 1, uint64_t);
+  UP(prog_full_set, prog_full.data(), P, uint32_t);
+#undef UP
+  uint32_t *cn = nullptr;
+  veq_rat *dconsts = nullptr;
+  if ((r = dalloc(ctx, bd, &cn, d->n_consts)) || (r = dupload(ctx, bd, &dconsts, d->consts, d->n_consts))) {
+    delete bd;
+    return r;
+  }
+  if (d->n_consts) k_intern_consts<<<blocks(d->n_consts, 256), 256, 0, ctx->stream>>>(ctx->T, dconsts, d->n_consts, cn);
+  B.const_node = cn;
+  // run-state buffers
+#define AL(field, n, T_)                                                  \
+  do {                                                                    \
+    T_ *p_ = nullptr;                                                     \
+    if ((r = dalloc(ctx, bd, &p_, (n)))) { delete bd; return r; }        \
+    B.field = p_;                                                         \
+  } while (0)
+  AL(seg_base, bd->n_segs, uint32_t);
+  AL(rel_step, bd->n_rel_cap, uint32_t);
+  AL(rel_set, bd->n_rel_cap, uint32_t);
+  AL(prog_nrel, P, uint32_t);
+  AL(prog_steps, P, unsigned long long);
+  AL(th_state, Tn, uint8_t);
+  AL(th_seg, Tn, uint32_t);
+  AL(th_bset, Tn, uint32_t);
+  AL(regfile, bd->n_regs, uint32_t);
+  AL(ref_a, S, uint32_t);
+  AL(ref_b, S, uint32_t);
+  AL(st_step, S, uint32_t);
+  AL(canon, S, uint32_t);
+  AL(chain_head, S, uint32_t);
+  AL(chain_pos, S, uint32_t);
+  AL(chain_len, S, uint32_t);
+  AL(uses, S, uint32_t);
+  AL(continued, S, uint8_t);
+  AL(tup_key, n_access, unsigned long long);
+  AL(tup_val, n_access, unsigned long long);
+  AL(n_tup, 1, unsigned long long);
+  AL(final_val, cells, uint32_t);
+  AL(final_node, cells, uint32_t);
+  uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(3 * S, 1024), 16ull << 20);
+  AL(faults, fcap, veq_fault);
+  AL(n_faults, 1, unsigned long long);
+  B.fault_cap = fcap;
+#undef AL
+  ctx->batches.push_back(bd);
+  *out = (uint32_t)(ctx->batches.size() - 1);
+  return check_error_flag(ctx);
+}
+
+int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
+  if (!ctx || batch >= ctx->batches.size()) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  Batch &B = bd->B;
+  cudaStream_t s = ctx->stream;
+  const uint64_t S = bd->n_stmts;
+  // reset run state
+  CK(cudaMemsetAsync(B.seg_base, 0xff, bd->n_segs * 4, s));
+  CK(cudaMemsetAsync(B.regfile, 0xff, std::max<uint64_t>(bd->n_regs, 1) * 4, s));
+  CK(cudaMemsetAsync(B.st_step, 0xff, S * 4, s));
+  CK(cudaMemsetAsync(B.canon, 0xff, S * 4, s));
+  CK(cudaMemsetAsync(B.uses, 0, S * 4, s));
+  CK(cudaMemsetAsync(B.continued, 0, S, s));
+  CK(cudaMemsetAsync(B.n_tup, 0, 8, s));
+  CK(cudaMemsetAsync(B.n_faults, 0, 8, s));
+  CK(cudaMemsetAsync(B.final_val, 0xff, std::max<uint64_t>(bd->n_cells, 1) * 4, s));
+  CK(cudaMemsetAsync(ctx->pool_used, 0, 8, s));
+  // K0
+  if (B.n_progs) k_schedule<<<B.n_progs, SCHED_BLOCK, 0, s>>>(B);
+  CK(cudaGetLastError());
+  // K3
+  if (B.n_threads) k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T);
+  CK(cudaGetLastError());
+  unsigned long long n_tup = 0;
+  CK(cudaMemcpyAsync(&n_tup, B.n_tup, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // K4: sort access tuples by (cell, step) and scan per cell
+  if (n_tup) {
+    unsigned long long *k2 = nullptr, *v2 = nullptr;
+    uint32_t *starts = nullptr;
+    unsigned long long *n_starts = nullptr;
+    Reader *rs = nullptr;
+    CK(cudaMallocAsync(&k2, n_tup * 8, s));
+    CK(cudaMallocAsync(&v2, n_tup * 8, s));
+    CK(cudaMallocAsync(&starts, n_tup * 4, s));
+    CK(cudaMallocAsync(&n_starts, 8, s));
+    CK(cudaMallocAsync(&rs, n_tup * sizeof(Reader), s));
+    int end_bit = 64;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tmp_bytes, s));
+    cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
+    CK(cudaMemsetAsync(n_starts, 0, 8, s));
+    k_seg_heads<<<blocks(n_tup, 256), 256, 0, s>>>(k2, n_tup, starts, n_starts);
+    unsigned long long nseg = 0;
+    CK(cudaMemcpyAsync(&nseg, n_starts, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    k_mem_scan<<<blocks(nseg, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, (uint32_t)nseg, n_tup, rs);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, s));
+    CK(cudaFreeAsync(k2, s));
+    CK(cudaFreeAsync(v2, s));
+    CK(cudaFreeAsync(starts, s));
+    CK(cudaFreeAsync(n_starts, s));
+    CK(cudaFreeAsync(rs, s));
+  }
+  // resolve loads, then operands, then count uses (incl. final cells)
+  if (S) {
+    k_resolve_loads<<<blocks(S, 256), 256, 0, s>>>(B);
+    k_resolve<<<blocks(S, 256), 256, 0, s>>>(B);
+    k_count_uses<<<blocks(S, 256), 256, 0, s>>>(B);
+  }
+  if (bd->n_cells) k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B);
+  CK(cudaGetLastError());
+  // chain logs
+  uint32_t *sz = nullptr, *base = nullptr, *log = nullptr, *log_stmt = nullptr;
+  unsigned long long n_work = 0;
+  if (S) {
+    CK(cudaMallocAsync(&sz, S * 4, s));
+    CK(cudaMallocAsync(&base, S * 4, s));
+    k_chain_sizes<<<blocks(S, 256), 256, 0, s>>>(B, sz);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, base, (int64_t)S, s);
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tb, s));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, sz, base, (int64_t)S, s);
+    uint32_t last_sz = 0, last_base = 0;
+    CK(cudaMemcpyAsync(&last_sz, sz + S - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&last_base, base + S - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t nlog = (uint64_t)last_sz + last_base;
+    CK(cudaMallocAsync(&log, std::max<uint64_t>(nlog, 1) * 4, s));
+    CK(cudaMallocAsync(&log_stmt, std::max<uint64_t>(nlog, 1) * 4, s));
+    k_chain_scatter<<<blocks(S, 256), 256, 0, s>>>(B, base, log, log_stmt);
+    CK(cudaFreeAsync(tmp, s));
+    // work list sorted by (program, step)
+    unsigned long long *wk = nullptr, *wk2 = nullptr, *nw = nullptr;
+    uint32_t *wv = nullptr, *wv2 = nullptr;
+    CK(cudaMallocAsync(&wk, S * 8, s));
+    CK(cudaMallocAsync(&wk2, S * 8, s));
+    CK(cudaMallocAsync(&wv, S * 4, s));
+    CK(cudaMallocAsync(&wv2, S * 4, s));
+    CK(cudaMallocAsync(&nw, 8, s));
+    CK(cudaMemsetAsync(nw, 0, 8, s));
+    k_make_work<<<blocks(S, 256), 256, 0, s>>>(B, wk, wv, nw);
+    CK(cudaMemcpyAsync(&n_work, nw, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (n_work) {
+      int pb = 1;
+      while ((1ull << pb) < B.n_progs + 1) pb++;
+      size_t tb2 = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, 32 + pb, s);
+      void *tmp2 = nullptr;
+      CK(cudaMallocAsync(&tmp2, tb2, s));
+      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, 32 + pb, s);
+      unsigned long long *cursor = nullptr;
+      CK(cudaMallocAsync(&cursor, 8, s));
+      CK(cudaMemsetAsync(cursor, 0, 8, s));
+      EvalCtx E{log, log_stmt, base};
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+      uint64_t threads = std::min<uint64_t>(n_work, (uint64_t)nsm * 512);
+      k_eval<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool, ctx->pool_used,
+                                                   ctx->pool_cap);
+      CK(cudaGetLastError());
+      CK(cudaFreeAsync(tmp2, s));
+      CK(cudaFreeAsync(cursor, s));
+    }
+    CK(cudaFreeAsync(wk, s));
+    CK(cudaFreeAsync(wk2, s));
+    CK(cudaFreeAsync(wv, s));
+    CK(cudaFreeAsync(wv2, s));
+    CK(cudaFreeAsync(nw, s));
+  }
+  if (bd->n_cells) k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B);
+  CK(cudaGetLastError());
+  if (sz) {
+    CK(cudaFreeAsync(sz, s));
+    CK(cudaFreeAsync(base, s));
+    CK(cudaFreeAsync(log, s));
+    CK(cudaFreeAsync(log_stmt, s));
+  }
+  // ---- results to host
+  const uint32_t P = B.n_progs;
+  std::vector<uint32_t> nrel(P);
+  std::vector<unsigned long long> steps(P);
+  unsigned long long nf = 0;
+  CK(cudaMemcpyAsync(nrel.data(), B.prog_nrel, P * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(steps.data(), B.prog_steps, P * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&nf, B.n_faults, 8, cudaMemcpyDeviceToHost, s));
+  bd->th_state.resize(B.n_threads);
+  bd->th_bset.resize(B.n_threads);
+  std::vector<uint32_t> th_seg(B.n_threads);
+  CK(cudaMemcpyAsync(bd->th_state.data(), B.th_state, B.n_threads, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(bd->th_bset.data(), B.th_bset, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(th_seg.data(), B.th_seg, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int er = check_error_flag(ctx);
+  if (er) return er;
+  if (nf > B.fault_cap) return fail(ctx, VEQ_E_BUDGET, "fault buffer overflow");
+  bd->faults.resize(nf);
+  if (nf) CK(cudaMemcpyAsync(bd->faults.data(), B.faults, nf * sizeof(veq_fault), cudaMemcpyDeviceToHost, s));
+  // blocking statement of blocked threads: end of their current segment
+  std::vector<uint64_t> seg_off_h(B.n_threads + 1), seg_start_h(bd->n_segs);
+  CK(cudaMemcpyAsync(seg_off_h.data(), B.seg_off, (B.n_threads + 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(seg_start_h.data(), B.seg_start, bd->n_segs * 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long nn[2] = {0, 0};
+  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  bd->th_bstmt.assign(B.n_threads, ~0ull);
+  for (uint32_t t = 0; t < B.n_threads; t++)
+    if (bd->th_state[t] == TS_BLOCK) bd->th_bstmt[t] = seg_start_h[seg_off_h[t] + th_seg[t] + 1] - 1;
+  bd->res.assign(P, veq_prog_result{});
+  for (uint32_t p = 0; p < P; p++) {
+    bd->res[p].steps = steps[p];
+    bd->res[p].releases = nrel[p];
+    const veq_program_meta &m = bd->progs[p];
+    for (uint32_t t = 0; t < m.n_threads; t++)
+      if (bd->th_state[m.thread_off + t] != TS_RET) bd->res[p].deadlocked = 1;
+  }
+  for (const veq_fault &f : bd->faults) bd->res[f.prog].n_faults++;
+  bd->ran = true;
+  ctx->last_faults = nf;
+  if (out) {
+    out->n_progs = P;
+    out->progs = bd->res.data();
+    out->n_faults = nf;
+    out->faults = bd->faults.data();
+    out->n_threads_total = B.n_threads;
+    out->thread_state = bd->th_state.data();
+    out->thread_block_set = bd->th_bset.data();
+    out->thread_block_stmt = bd->th_bstmt.data();
+    out->n_nodes = nn[0];
+    out->n_kid_words = nn[1];
+    out->n_work = n_work;
+    out->n_access = n_tup;
+  }
+  return VEQ_OK;
+}
+
+int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, const uint32_t *out_b,
+                uint32_t n_out, veq_vc_out *out) {
+  if (!ctx || ba >= ctx->batches.size() || bb >= ctx->batches.size()) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *A = ctx->batches[ba], *Bd = ctx->batches[bb];
+  if (!A->ran || !Bd->ran) return fail(ctx, VEQ_E_ARG, "compare before run");
+  if (A->progs.size() != Bd->progs.size()) return fail(ctx, VEQ_E_ARG, "batches differ in program count");
+  std::vector<uint32_t> ca, cb;
+  for (size_t p = 0; p < A->progs.size(); p++)
+    for (uint32_t k = 0; k < n_out; k++) {
+      uint32_t ga = A->progs[p].array_off + out_a[k], gb = Bd->progs[p].array_off + out_b[k];
+      if (out_a[k] >= A->progs[p].n_arrays || out_b[k] >= Bd->progs[p].n_arrays)
+        return fail(ctx, VEQ_E_ARG, "out array index out of range");
+      uint64_t n = A->arrays[ga].size;
+      uint64_t cba = A->arr_cell_base[ga], cbb = Bd->arr_cell_base[gb];
+      for (uint64_t i = 0; i < n; i++) {
+        ca.push_back(cba == UNSET64 ? UNSET : (uint32_t)(cba + i));
+        cb.push_back(cbb == UNSET64 || i >= Bd->arrays[gb].size ? UNSET : (uint32_t)(cbb + i));
+      }
+    }
+  uint64_t nv = ca.size();
+  cudaStream_t s = ctx->stream;
+  uint32_t *dca = nullptr, *dcb = nullptr, *scn = nullptr;
+  uint8_t *scd = nullptr;
+  veq_vc *dv = nullptr;
+  unsigned long long *cnt = nullptr;
+  uint64_t sc_cap = std::max<uint64_t>(nv * 2, 1024);
+  CK(cudaMallocAsync(&dca, std::max<uint64_t>(nv, 1) * 4, s));
+  CK(cudaMallocAsync(&dcb, std::max<uint64_t>(nv, 1) * 4, s));
+  CK(cudaMallocAsync(&dv, std::max<uint64_t>(nv, 1) * sizeof(veq_vc), s));
+  CK(cudaMallocAsync(&scn, sc_cap * 4, s));
+  CK(cudaMallocAsync(&scd, sc_cap, s));
+  CK(cudaMallocAsync(&cnt, 3 * 8, s));
+  CK(cudaMemsetAsync(cnt, 0, 24, s));
+  CK(cudaMemsetAsync(ctx->pool_used, 0, 8, s));
+  if (nv) {
+    CK(cudaMemcpyAsync(dca, ca.data(), nv * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dcb, cb.data(), nv * 4, cudaMemcpyHostToDevice, s));
+    CmpArgs C{dca, dcb, nv, dv, scn, scd, cnt, sc_cap, cnt + 1, cnt + 2};
+    k_compare<<<blocks(nv, 128), 128, 0, s>>>(ctx->T, A->B.final_node, Bd->B.final_node, C, ctx->pool, ctx->pool_used,
+                                              ctx->pool_cap);
+    CK(cudaGetLastError());
+  }
+  unsigned long long h[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(h, cnt, 24, cudaMemcpyDeviceToHost, s));
+  ctx->vcs.resize(nv);
+  if (nv) CK(cudaMemcpyAsync(ctx->vcs.data(), dv, nv * sizeof(veq_vc), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  uint64_t nsc = std::min<uint64_t>(h[0], sc_cap);
+  ctx->sc_node.resize(nsc);
+  ctx->sc_dis.resize(nsc);
+  if (nsc) {
+    CK(cudaMemcpyAsync(ctx->sc_node.data(), scn, nsc * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->sc_dis.data(), scd, nsc, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaFreeAsync(dca, s));
+  CK(cudaFreeAsync(dcb, s));
+  CK(cudaFreeAsync(dv, s));
+  CK(cudaFreeAsync(scn, s));
+  CK(cudaFreeAsync(scd, s));
+  CK(cudaFreeAsync(cnt, s));
+  CK(cudaStreamSynchronize(s));
+  int er = check_error_flag(ctx);
+  if (er) return er;
+  if (h[0] > sc_cap) return fail(ctx, VEQ_E_BUDGET, "side-condition buffer overflow");
+  ctx->last_equal = h[1];
+  ctx->last_missing = h[2];
+  ctx->last_vcs = nv;
+  if (out) {
+    out->n_vcs = nv;
+    out->vcs = ctx->vcs.data();
+    out->n_sc = nsc;
+    out->sc_node = ctx->sc_node.data();
+    out->sc_discharged = ctx->sc_dis.data();
+    out->n_equal = h[1];
+    out->n_missing = h[2];
+  }
+  return VEQ_OK;
+}
+
+int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_buf *buf) {
+  if (!ctx || !buf || (n_roots && !roots)) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  unsigned long long nn[2];
+  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  uint64_t NN = std::min<uint64_t>(nn[0], ctx->lim.max_nodes), NK = std::min<uint64_t>(nn[1], ctx->lim.max_kid_words);
+  std::vector<Node> nodes(NN);
+  std::vector<uint32_t> kids(NK);
+  if (NN) CK(cudaMemcpyAsync(nodes.data(), ctx->nodes, NN * sizeof(Node), cudaMemcpyDeviceToHost, s));
+  if (NK) CK(cudaMemcpyAsync(kids.data(), ctx->kids, NK * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // iterative post-order DFS, dense renumbering
+  std::vector<uint32_t> remap;
+  std::map<uint32_t, uint32_t> idx;
+  std::vector<uint32_t> order;
+  for (size_t r = 0; r < n_roots; r++) {
+    if (roots[r] >= NN) return fail(ctx, VEQ_E_ARG, "root id out of range");
+    std::vector<std::pair<uint32_t, uint32_t>> st{{roots[r], 0}};
+    while (!st.empty()) {
+      auto &[x, k] = st.back();
+      if (idx.count(x)) {
+        st.pop_back();
+        continue;
+      }
+      const Node &n = nodes[x];
+      bool comp = n.kind != K_CONST && n.kind != K_VAR && n.kind != K_NEGINF;
+      if (comp && k < n.nkids) {
+        uint32_t kid = kids[n.p0 + k];
+        k++;
+        if (!idx.count(kid)) st.push_back({kid, 0});
+        continue;
+      }
+      idx[x] = (uint32_t)order.size();
+      order.push_back(x);
+      st.pop_back();
+    }
+  }
+  uint64_t total_kids = 0;
+  for (uint32_t x : order) {
+    const Node &n = nodes[x];
+    if (n.kind != K_CONST && n.kind != K_VAR && n.kind != K_NEGINF) total_kids += n.nkids;
+  }
+  uint64_t cap_n = buf->cap_nodes, cap_k = buf->cap_kids;
+  buf->n_nodes = order.size();
+  buf->n_kids = total_kids;
+  if (cap_n < order.size() || cap_k < total_kids || !buf->nodes || !buf->kids || !buf->root_index)
+    return VEQ_OK;  // sizing call
+  uint64_t ko = 0;
+  for (size_t i = 0; i < order.size(); i++) {
+    const Node &n = nodes[order[i]];
+    veq_dag_node &o = buf->nodes[i];
+    o.kind = n.kind;
+    o.nkids = 0;
+    o.kid_off = ko;
+    o.num = 0;
+    o.den = 1;
+    o.var_input = -1;
+    o.var_index = 0;
+    if (n.kind == K_CONST) {
+      o.num = (int64_t)n.p0;
+      o.den = (int64_t)n.p1;
+    } else if (n.kind == K_VAR) {
+      if (n.p0 >= INPUT_KEY) {
+        o.var_input = (int64_t)(n.p1 >> 40);
+        o.var_index = n.p1 & ((1ull << 40) - 1);
+      } else {
+        o.var_input = -1;
+        o.var_index = n.p1;
+      }
+    } else if (n.kind != K_NEGINF) {
+      o.nkids = n.nkids;
+      for (uint32_t k = 0; k < n.nkids; k++) buf->kids[ko++] = idx[kids[n.p0 + k]];
+    }
+  }
+  for (size_t r = 0; r < n_roots; r++) buf->root_index[r] = idx[roots[r]];
+  return VEQ_OK;
+}
+
+int veq_fetch_cells(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t array, uint32_t *out_nodes, uint64_t n) {
+  if (!ctx || batch >= ctx->batches.size() || (n && !out_nodes)) return VEQ_E_ARG;
+  BatchDev *bd = ctx->batches[batch];
+  if (!bd->ran || prog >= bd->progs.size() || array >= bd->progs[prog].n_arrays) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  uint32_t ga = bd->progs[prog].array_off + array;
+  uint64_t size = bd->arrays[ga].size, cb = bd->arr_cell_base[ga];
+  if (n > size) n = size;
+  if (cb == UNSET64) {
+    std::fill(out_nodes, out_nodes + n, UNSET);
+    return VEQ_OK;
+  }
+  if (n) {
+    CK(cudaMemcpyAsync(out_nodes, bd->B.final_node + cb, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  return VEQ_OK;
+}
+
+int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]) {
+  if (!ctx || !out) return VEQ_E_ARG;
+  out[0] = ctx->last_equal;
+  out[1] = ctx->last_vcs;
+  out[2] = ctx->last_faults;
+  out[3] = ctx->last_missing;
+  return VEQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,895 @@
+// veq_kernels.cuh — the per-batch pipeline kernels.
+//
+//   K0 k_schedule     round-robin control schedule (symexec.cpp:764-781,
+//                     616-671): per program, step numbers of every executed
+//                     segment and the release sequence. Control is value-
+//                     independent, so this needs only the IR.
+//   K3 k_exec         per-thread symbolic execution: registers hold value
+//                     refs (raw statement ids or term ids), loads/stores emit
+//                     access tuples, Add/Max chains are linked for fusion
+//                     (step_impl, symexec.cpp:372-604).
+//   K4 k_mem_scan     per-address scan of step-sorted access tuples: races,
+//                     uninitialised reads, and load -> store value resolution
+//                     (no_racing_rd/wr + sync_mem, symexec.cpp:22-69, 491-595).
+//   K2 k_eval         canonicalises live raw nodes in step order with
+//                     operand-ready spinning (persistent threads).
+//   K5 k_compare      per-VC canonical id compare + side conditions.
+#pragma once
+#include "veq_canon.cuh"
+#include "../../include/veq.h"
+
+namespace veqd {
+
+constexpr uint8_t TS_RUN = 0, TS_BLOCK = 1, TS_RET = 2;
+constexpr uint64_t UNSET64 = ~0ull;
+
+struct Batch {
+  uint32_t n_progs, n_threads;
+  uint64_t n_stmts;
+  const veq_program_meta *progs;
+  const uint64_t *thread_stmt;
+  const uint32_t *thread_prog;
+  const veq_stmt *stmts;
+  const veq_array *arrays;
+  const uint64_t *arr_cell_base;  // per array: first global cell id, or UNSET64
+  const uint32_t *const_node;
+  const veq_syncset *sets;
+  const uint64_t *set_words;
+  const uint64_t *seg_off;    // [T+1]
+  const uint64_t *seg_start;  // statement index of each segment start
+  const uint32_t *seg_set;    // per segment: canonical set id of its ending Sync
+  const uint64_t *rel_off;    // [P+1] release capacity per program
+  const uint64_t *reg_off;    // [T+1]
+  const uint32_t *prog_full_set;  // per program: set index of its full set, or UNSET
+  uint64_t n_cells;
+  // run state
+  uint32_t *seg_base;
+  uint32_t *rel_step, *rel_set;
+  uint32_t *prog_nrel;
+  unsigned long long *prog_steps;
+  uint8_t *th_state;
+  uint32_t *th_seg, *th_bset;
+  uint32_t *regfile;
+  uint32_t *ref_a, *ref_b, *st_step, *canon;
+  uint32_t *chain_head, *chain_pos, *chain_len, *uses;
+  uint8_t *continued;
+  unsigned long long *tup_key, *tup_val;
+  unsigned long long *n_tup;
+  uint32_t *final_val, *final_node;
+  veq_fault *faults;
+  unsigned long long *n_faults;
+  uint64_t fault_cap;
+};
+
+__device__ __forceinline__ void emit_fault(const Batch &B, const veq_fault &f) {
+  unsigned long long i = atomicAdd(B.n_faults, 1ull);
+  if (i < B.fault_cap) B.faults[i] = f;
+}
+
+// ---------------------------------------------------------------------------
+// K0: schedule. One block per program, symbolic threads in contiguous chunks
+// per CUDA thread so an ordered block scan gives round-robin step offsets.
+constexpr int SCHED_BLOCK = 256;
+
+__device__ inline bool set_contains(const Batch &B, uint32_t s, uint32_t tid) {
+  veq_syncset q = B.sets[s];
+  if (q.full) return true;
+  if (tid < q.lo || tid >= q.lo + q.n_bits) return false;
+  uint32_t k = tid - q.lo;
+  return (B.set_words[q.word_off + k / 64] >> (k % 64)) & 1ull;
+}
+__device__ inline uint32_t set_min(const Batch &B, uint32_t s) {
+  veq_syncset q = B.sets[s];
+  if (q.full) return 0;
+  for (uint32_t w = 0; w * 64 < q.n_bits; w++) {
+    uint64_t x = B.set_words[q.word_off + w];
+    if (x) return q.lo + w * 64 + __ffsll((long long)x) - 1;
+  }
+  return q.lo;
+}
+
+__global__ void k_schedule(Batch B) {
+  const uint32_t p = blockIdx.x;
+  const veq_program_meta pm = B.progs[p];
+  const uint32_t T = pm.n_threads, t0 = pm.thread_off;
+  const uint32_t chunk = (T + SCHED_BLOCK - 1) / SCHED_BLOCK;
+  const uint32_t lo = threadIdx.x * chunk, hi = min(T, lo + chunk);
+  __shared__ unsigned long long s_scan[SCHED_BLOCK];
+  __shared__ unsigned long long s_step;
+  __shared__ unsigned long long s_best;
+  __shared__ uint32_t s_ret, s_blkfull, s_nrel;
+  __shared__ int s_released;
+  const uint32_t full = B.prog_full_set[p];
+  // init
+  for (uint32_t t = lo; t < hi; t++) {
+    uint32_t g = t0 + t;
+    B.th_seg[g] = 0;
+    bool empty = B.thread_stmt[g] == B.thread_stmt[g + 1];
+    B.th_state[g] = empty ? TS_RET : TS_RUN;
+    B.th_bset[g] = UNSET;
+  }
+  if (threadIdx.x == 0) {
+    s_step = 0;
+    s_nrel = 0;
+  }
+  __syncthreads();
+  for (;;) {
+    // ---- all returned?
+    if (threadIdx.x == 0) s_ret = 0;
+    __syncthreads();
+    uint32_t my_ret = 0;
+    for (uint32_t t = lo; t < hi; t++) my_ret += B.th_state[t0 + t] == TS_RET;
+    if (my_ret) atomicAdd(&s_ret, my_ret);
+    __syncthreads();
+    if (s_ret == T) break;
+    // ---- run phase: each runnable thread runs its current segment
+    unsigned long long mylen = 0;
+    for (uint32_t t = lo; t < hi; t++) {
+      uint32_t g = t0 + t;
+      if (B.th_state[g] == TS_RUN) {
+        uint64_t sj = B.seg_off[g] + B.th_seg[g];
+        uint64_t end = (sj + 1 < B.seg_off[g + 1]) ? B.seg_start[sj + 1] : B.thread_stmt[g + 1];
+        mylen += end - B.seg_start[sj];
+      }
+    }
+    s_scan[threadIdx.x] = mylen;
+    __syncthreads();
+    for (int off = 1; off < SCHED_BLOCK; off <<= 1) {  // inclusive Hillis-Steele scan
+      unsigned long long v = threadIdx.x >= (unsigned)off ? s_scan[threadIdx.x - off] : 0;
+      __syncthreads();
+      s_scan[threadIdx.x] += v;
+      __syncthreads();
+    }
+    unsigned long long total = s_scan[SCHED_BLOCK - 1];
+    unsigned long long run = s_step + s_scan[threadIdx.x] - mylen;
+    for (uint32_t t = lo; t < hi; t++) {
+      uint32_t g = t0 + t;
+      if (B.th_state[g] != TS_RUN) continue;
+      uint64_t sj = B.seg_off[g] + B.th_seg[g];
+      bool last = sj + 1 >= B.seg_off[g + 1];
+      uint64_t end = last ? B.thread_stmt[g + 1] : B.seg_start[sj + 1];
+      B.seg_base[sj] = (uint32_t)run;
+      run += end - B.seg_start[sj];
+      if (last) {
+        B.th_state[g] = TS_RET;
+      } else {
+        B.th_state[g] = TS_BLOCK;
+        B.th_bset[g] = B.seg_set[sj];  // canonical id of the Sync ending the segment
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_step += total;
+      s_best = ~0ull;
+      s_ret = 0;
+      s_blkfull = 0;
+      s_released = 0;
+    }
+    __syncthreads();
+    // ---- release phase: the releasable set with the smallest min tid
+    uint32_t c_ret = 0, c_full = 0;
+    for (uint32_t t = lo; t < hi; t++) {
+      uint32_t g = t0 + t;
+      c_ret += B.th_state[g] == TS_RET;
+      c_full += (B.th_state[g] == TS_BLOCK && B.th_bset[g] == full);
+    }
+    if (c_ret) atomicAdd(&s_ret, c_ret);
+    if (c_full) atomicAdd(&s_blkfull, c_full);
+    __syncthreads();
+    unsigned long long best = ~0ull;
+    for (uint32_t t = lo; t < hi; t++) {
+      uint32_t g = t0 + t;
+      if (B.th_state[g] != TS_BLOCK) continue;
+      uint32_t I = B.th_bset[g];
+      bool ok;
+      uint32_t mn;
+      if (I == full) {
+        ok = (s_blkfull + s_ret == T);
+        mn = 0;
+      } else {
+        veq_syncset q = B.sets[I];
+        ok = true;
+        mn = UNSET;
+        for (uint32_t k = 0; k < q.n_bits && ok; k++) {
+          if (!((B.set_words[q.word_off + k / 64] >> (k % 64)) & 1ull)) continue;
+          uint32_t m = q.lo + k;
+          if (mn == UNSET) mn = m;
+          if (m >= T) {
+            ok = false;
+            break;
+          }
+          uint8_t st = B.th_state[t0 + m];
+          if (st == TS_RET) continue;
+          if (st == TS_BLOCK && B.th_bset[t0 + m] == I) continue;
+          ok = false;
+        }
+      }
+      if (ok) {
+        unsigned long long key = ((unsigned long long)mn << 32) | I;
+        best = key < best ? key : best;
+      }
+    }
+    if (best != ~0ull) atomicMin(&s_best, best);
+    __syncthreads();
+    unsigned long long sb = s_best;
+    if (sb != ~0ull) {
+      uint32_t I = (uint32_t)(sb & 0xffffffffu);
+      for (uint32_t t = lo; t < hi; t++) {
+        uint32_t g = t0 + t;
+        if (B.th_state[g] != TS_BLOCK || B.th_bset[g] != I) continue;
+        uint32_t ns = B.th_seg[g] + 1;
+        B.th_seg[g] = ns;
+        uint64_t sj = B.seg_off[g] + ns;
+        uint64_t start = B.seg_start[sj];
+        B.th_state[g] = (start == B.thread_stmt[g + 1]) ? TS_RET : TS_RUN;
+      }
+      if (threadIdx.x == 0) {
+        uint64_t r = B.rel_off[p] + s_nrel;
+        if (r < B.rel_off[p + 1]) {
+          B.rel_step[r] = (uint32_t)s_step;
+          B.rel_set[r] = I;
+        }
+        s_nrel++;
+        s_step += 1;
+        s_released = 1;
+      }
+    }
+    __syncthreads();
+    if (total == 0 && !s_released) break;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    B.prog_nrel[p] = s_nrel;
+    B.prog_steps[p] = s_step;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: per-thread symbolic execution over value refs.
+__device__ __forceinline__ bool is_stmt_ref(uint32_t r) { return r < REF_NODE; }
+
+__global__ void k_exec(Batch B, Table T) {
+  uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= B.n_threads) return;
+  const uint32_t p = B.thread_prog[g];
+  const veq_program_meta pm = B.progs[p];
+  const uint32_t tid = g - pm.thread_off;
+  uint32_t *regs = B.regfile + B.reg_off[g];
+  const uint64_t s0 = B.thread_stmt[g], s1 = B.thread_stmt[g + 1];
+  const uint64_t j0 = B.seg_off[g], j1 = B.seg_off[g + 1];
+  for (uint64_t j = j0; j < j1; j++) {
+    uint32_t base = B.seg_base[j];
+    if (base == UNSET) break;  // segment never ran (deadlock)
+    uint64_t start = B.seg_start[j], end = (j + 1 < j1) ? B.seg_start[j + 1] : s1;
+    for (uint64_t i = start; i < end; i++) {
+      const veq_stmt st = B.stmts[i];
+      const uint32_t step = base + (uint32_t)(i - start);
+      auto readreg = [&](uint32_t r, uint8_t slot) -> uint32_t {
+        uint32_t v = regs[r];
+        if (v == UNSET) {
+          veq_fault f{};
+          f.type = VEQ_FAULT_SAFETY;
+          f.kind = VEQ_SAFE_UNINIT_REG;
+          f.sub = slot;
+          f.reg_slot = slot;
+          f.prog = p;
+          f.tid = tid;
+          f.stmt = (uint32_t)i;
+          f.step = step;
+          emit_fault(B, f);
+          v = REF_NODE | intern_undef(T, 0, g, r);
+          regs[r] = v;
+        }
+        return v;
+      };
+      switch (st.kind) {
+      case VEQ_ST_SETCONST:
+        regs[st.dst] = REF_NODE | (st.op == 1 ? T.id_neginf : B.const_node[st.a]);
+        break;
+      case VEQ_ST_COPY: {
+        uint32_t v = readreg(st.a, 0);
+        regs[st.dst] = v;
+        break;
+      }
+      case VEQ_ST_BINOP: {
+        uint32_t va = readreg(st.a, 0);
+        uint32_t vb = readreg(st.b, 1);
+        B.st_step[i] = step;
+        uint32_t ra = va, rb = vb;
+        if (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX) {
+          // chain linking: continue a chain whose tail this thread holds
+          auto tail = [&](uint32_t v) -> bool {
+            if (!is_stmt_ref(v)) return false;
+            if (v < s0 || v >= i) return false;
+            veq_stmt sk = B.stmts[v];
+            return sk.kind == VEQ_ST_BINOP && sk.op == st.op && !B.continued[v];
+          };
+          uint32_t k = UNSET, leaf = 0;
+          if (tail(va)) {
+            k = va;
+            leaf = vb;
+          } else if (tail(vb)) {
+            k = vb;
+            leaf = va;
+          }
+          if (k != UNSET) {
+            uint32_t h = B.chain_head[k];
+            uint32_t pos = B.chain_pos[k] + 1;
+            B.continued[k] = 1;
+            B.chain_head[i] = h;
+            B.chain_pos[i] = pos;
+            B.chain_len[h] = pos + 1;
+            ra = k;
+            rb = leaf;
+          } else {
+            B.chain_head[i] = (uint32_t)i;
+            B.chain_pos[i] = 0;
+            B.chain_len[i] = 1;
+          }
+        }
+        B.ref_a[i] = ra;
+        B.ref_b[i] = rb;
+        regs[st.dst] = (uint32_t)i;
+        break;
+      }
+      case VEQ_ST_UNOP: {
+        uint32_t va = readreg(st.a, 0);
+        B.st_step[i] = step;
+        B.ref_a[i] = va;
+        regs[st.dst] = (uint32_t)i;
+        break;
+      }
+      case VEQ_ST_LOAD:
+      case VEQ_ST_STORE: {
+        const uint32_t ga = pm.array_off + st.arr;
+        const veq_array arr = B.arrays[ga];
+        const int32_t off = (int32_t)st.a;
+        const bool is_store = st.kind == VEQ_ST_STORE;
+        if (off < 0 || (uint64_t)off >= arr.size) {
+          veq_fault f{};
+          f.type = VEQ_FAULT_SAFETY;
+          f.kind = VEQ_SAFE_OOB;
+          f.sub = 2;
+          f.is_write = is_store;
+          f.prog = p;
+          f.tid = tid;
+          f.stmt = (uint32_t)i;
+          f.step = step;
+          f.arr = st.arr;
+          f.offset = off;
+          emit_fault(B, f);
+          if (!is_store) regs[st.dst] = REF_NODE | intern_undef(T, 1, ga, (uint64_t)(uint32_t)off);
+          break;
+        }
+        if (!is_store) {
+          if (!(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 && (uint32_t)off < arr.seeded) {
+            regs[st.dst] = REF_NODE | intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
+            break;
+          }
+          regs[st.dst] = (uint32_t)i;
+        } else {
+          uint32_t v = readreg(st.dst, 0);
+          B.ref_a[i] = v;
+        }
+        B.st_step[i] = step;
+        uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
+        unsigned long long slot = atomicAdd(B.n_tup, 1ull);
+        B.tup_key[slot] = (cell << 32) | step;
+        B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
+        break;
+      }
+      case VEQ_ST_SYNC:
+      default:
+        break;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 helpers: "thread i is still pending in the event (owner j, step se) at
+// step s" — no release (I, r) with se < r < s and {i, j} in I (sync_mem,
+// symexec.cpp:48-69, folded over the release sequence).
+__device__ inline uint32_t find_prog_of_thread(const Batch &B, uint32_t g) { return B.thread_prog[g]; }
+
+__device__ inline bool pending(const Batch &B, uint32_t p, uint32_t j, uint32_t se, uint32_t i, uint32_t s) {
+  const uint64_t r0 = B.rel_off[p];
+  const uint32_t n = B.prog_nrel[p];
+  // first release with step > se
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) / 2;
+    if (B.rel_step[r0 + mid] <= se) lo = mid + 1;
+    else hi = mid;
+  }
+  for (uint32_t k = lo; k < n; k++) {
+    uint32_t rs = B.rel_step[r0 + k];
+    if (rs >= s) break;
+    uint32_t I = B.rel_set[r0 + k];
+    if (set_contains(B, I, i) && set_contains(B, I, j)) return false;
+  }
+  return true;
+}
+
+struct Reader {
+  uint32_t tid, step, stmt, pad;
+};
+
+// One thread per address segment [s, e) of the (cell, step)-sorted tuples.
+__global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, const unsigned long long *vals,
+                           const uint32_t *seg_starts, uint32_t n_segs, uint64_t n_tup, Reader *rscratch) {
+  uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sidx >= n_segs) return;
+  const uint64_t s = seg_starts[sidx];
+  const uint64_t cell = keys[s] >> 32;
+  uint64_t e = s + 1;
+  while (e < n_tup && (keys[e] >> 32) == cell) e++;
+  // identify the array of this cell via the first tuple's statement
+  const uint32_t stmt0 = (uint32_t)(vals[s] >> 32);
+  const uint32_t tid0 = (uint32_t)(vals[s] & 0xffffffffu);
+  (void)tid0;
+  const veq_stmt st0 = B.stmts[stmt0];
+  // program: thread of stmt0 -> binary search on thread_stmt
+  uint32_t lo = 0, hi = B.n_threads;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) / 2;
+    if (B.thread_stmt[mid] <= stmt0) lo = mid;
+    else hi = mid;
+  }
+  const uint32_t p = B.thread_prog[lo];
+  const veq_program_meta pm = B.progs[p];
+  const uint32_t ga = pm.array_off + st0.arr;
+  const veq_array arr = B.arrays[ga];
+  const uint64_t offset = cell - B.arr_cell_base[ga];
+  bool has = arr.input >= 0 && offset < arr.seeded;
+  uint32_t value = has ? (REF_NODE | intern_input_var(T, (uint32_t)arr.input, offset)) : UNSET;
+  bool w_valid = false;
+  uint32_t w_tid = 0, w_step = 0, w_stmt = 0;
+  Reader *rd = rscratch + s;
+  uint32_t nrd = 0;
+  for (uint64_t k = s; k < e; k++) {
+    const uint32_t step = (uint32_t)(keys[k] & 0xffffffffu);
+    const uint32_t stmt = (uint32_t)(vals[k] >> 32);
+    const uint32_t tid = (uint32_t)(vals[k] & 0xffffffffu);
+    const bool is_store = B.stmts[stmt].kind == VEQ_ST_STORE;
+    if (!is_store) {
+      if (w_valid && w_tid != tid && pending(B, p, w_tid, w_step, tid, step)) {
+        veq_fault f{};
+        f.type = VEQ_FAULT_RACE;
+        f.sub = 0;
+        f.prog = p;
+        f.tid = tid;
+        f.stmt = stmt;
+        f.step = step;
+        f.is_write = 0;
+        f.tid2 = w_tid;
+        f.stmt2 = w_stmt;
+        f.step2 = w_step;
+        f.is_write2 = 1;
+        f.arr = st0.arr;
+        f.offset = (int32_t)offset;
+        emit_fault(B, f);
+      }
+      if (!has) {
+        veq_fault f{};
+        f.type = VEQ_FAULT_SAFETY;
+        f.kind = VEQ_SAFE_UNINIT_MEM;
+        f.sub = 2;
+        f.prog = p;
+        f.tid = tid;
+        f.stmt = stmt;
+        f.step = step;
+        f.arr = st0.arr;
+        f.offset = (int32_t)offset;
+        emit_fault(B, f);
+        value = REF_NODE | intern_undef(T, 2, cell >> 29, cell);
+        has = true;
+      }
+      B.ref_a[stmt] = value;
+      uint32_t q = 0;
+      for (; q < nrd; q++)
+        if (rd[q].tid == tid) break;
+      rd[q] = Reader{tid, step, stmt, 0};
+      if (q == nrd) nrd++;
+    } else {
+      uint32_t best = UNSET, bq = 0;
+      for (uint32_t q = 0; q < nrd; q++) {
+        if (rd[q].tid == tid || rd[q].tid >= best) continue;
+        if (pending(B, p, rd[q].tid, rd[q].step, tid, step)) {
+          best = rd[q].tid;
+          bq = q;
+        }
+      }
+      if (best != UNSET) {
+        veq_fault f{};
+        f.type = VEQ_FAULT_RACE;
+        f.sub = 0;
+        f.prog = p;
+        f.tid = tid;
+        f.stmt = stmt;
+        f.step = step;
+        f.is_write = 1;
+        f.tid2 = best;
+        f.stmt2 = rd[bq].stmt;
+        f.step2 = rd[bq].step;
+        f.is_write2 = 0;
+        f.arr = st0.arr;
+        f.offset = (int32_t)offset;
+        emit_fault(B, f);
+      }
+      if (w_valid && w_tid != tid && pending(B, p, w_tid, w_step, tid, step)) {
+        veq_fault f{};
+        f.type = VEQ_FAULT_RACE;
+        f.sub = 1;
+        f.prog = p;
+        f.tid = tid;
+        f.stmt = stmt;
+        f.step = step;
+        f.is_write = 1;
+        f.tid2 = w_tid;
+        f.stmt2 = w_stmt;
+        f.step2 = w_step;
+        f.is_write2 = 1;
+        f.arr = st0.arr;
+        f.offset = (int32_t)offset;
+        emit_fault(B, f);
+      }
+      w_valid = true;
+      w_tid = tid;
+      w_step = step;
+      w_stmt = stmt;
+      value = B.ref_a[stmt];
+      has = true;
+    }
+  }
+  B.final_val[cell] = has ? value : UNSET;
+}
+
+__global__ void k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t *starts, unsigned long long *n_starts) {
+  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32)) {
+    unsigned long long i = atomicAdd(n_starts, 1ull);
+    starts[i] = (uint32_t)k;
+  }
+}
+
+// Follow load refs to the value they read (a load's ref_a holds the value
+// of the store it observed, which may itself be a loaded value).
+__device__ __forceinline__ uint32_t chase(const Batch &B, uint32_t r) {
+  while (is_stmt_ref(r) && B.stmts[r].kind == VEQ_ST_LOAD) r = B.ref_a[r];
+  return r;
+}
+
+__global__ void k_resolve(Batch B) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  if (B.st_step[i] == UNSET) return;
+  veq_stmt st = B.stmts[i];
+  if (st.kind == VEQ_ST_BINOP) {
+    uint32_t a = chase(B, B.ref_a[i]), b = chase(B, B.ref_b[i]);
+    B.ref_a[i] = a;
+    B.ref_b[i] = b;
+  } else if (st.kind == VEQ_ST_UNOP || st.kind == VEQ_ST_STORE) {
+    B.ref_a[i] = chase(B, B.ref_a[i]);
+  }
+}
+__global__ void k_resolve_loads(Batch B) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  if (B.st_step[i] == UNSET) return;
+  if (B.stmts[i].kind == VEQ_ST_LOAD) B.ref_a[i] = chase(B, B.ref_a[i]);
+}
+__global__ void k_resolve_finals(Batch B) {
+  uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B.n_cells) return;
+  uint32_t v = B.final_val[c];
+  if (v == UNSET) return;
+  v = chase(B, v);
+  B.final_val[c] = v;
+  if (is_stmt_ref(v)) atomicAdd(B.uses + v, 1u);
+}
+
+__global__ void k_count_uses(Batch B) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  if (B.st_step[i] == UNSET) return;
+  veq_stmt st = B.stmts[i];
+  if (st.kind == VEQ_ST_BINOP) {
+    uint32_t a = B.ref_a[i], b = B.ref_b[i];
+    if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
+    if (is_stmt_ref(b)) atomicAdd(B.uses + b, 1u);
+  } else if (st.kind == VEQ_ST_UNOP) {
+    uint32_t a = B.ref_a[i];
+    if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
+  }
+}
+
+__device__ __forceinline__ bool is_chain_op(const veq_stmt &st) {
+  return st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX);
+}
+// chain leaf count of the head (for the log scan); 0 elsewhere
+__global__ void k_chain_sizes(Batch B, uint32_t *sz) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  uint32_t v = 0;
+  if (B.st_step[i] != UNSET && is_chain_op(B.stmts[i]) && B.chain_head[i] == (uint32_t)i) v = B.chain_len[i] + 1;
+  sz[i] = v;
+}
+__global__ void k_chain_scatter(Batch B, const uint32_t *base, uint32_t *log, uint32_t *log_stmt) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  if (B.st_step[i] == UNSET || !is_chain_op(B.stmts[i])) return;
+  uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
+  uint32_t b = base[h];
+  if (pos == 0) {
+    log[b] = B.ref_a[i];
+    log[b + 1] = B.ref_b[i];
+    log_stmt[b] = (uint32_t)i;
+    log_stmt[b + 1] = (uint32_t)i;
+  } else {
+    log[b + pos + 1] = B.ref_b[i];
+    log_stmt[b + pos + 1] = (uint32_t)i;
+  }
+}
+
+// work items: every executed BinOp/UnOp except chain links absorbed by
+// their successor (continued and used exactly once).
+__global__ void k_make_work(Batch B, unsigned long long *wkey, uint32_t *wval, unsigned long long *n_work) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  if (B.st_step[i] == UNSET) return;
+  veq_stmt st = B.stmts[i];
+  if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) return;
+  if (is_chain_op(st) && B.continued[i] && B.uses[i] == 1) return;
+  // program of statement: binary search on thread_stmt
+  uint32_t lo = 0, hi = B.n_threads;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) / 2;
+    if (B.thread_stmt[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  uint32_t p = B.thread_prog[lo];
+  unsigned long long slot = atomicAdd(n_work, 1ull);
+  wkey[slot] = ((unsigned long long)p << 32) | B.st_step[i];
+  wval[slot] = (uint32_t)i;
+}
+
+// ---------------------------------------------------------------------------
+// K2: persistent evaluation in (program, step) order.
+__device__ __forceinline__ uint32_t wait_node(const Batch &B, uint32_t r) {
+  if (!is_stmt_ref(r)) return r & ~REF_NODE;
+  volatile uint32_t *c = B.canon + r;
+  uint32_t v = *c;
+  int spins = 0;
+  while (v == UNSET) {
+    if (++spins > 16) __nanosleep(spins > 1000 ? 1000 : 64);
+    v = *c;
+  }
+  return v;
+}
+
+struct EvalCtx {
+  const uint32_t *log, *log_stmt, *log_base;
+};
+
+__device__ inline void arith_fault(const Batch &B, uint32_t stmt, uint8_t detail) {
+  uint32_t lo = 0, hi = B.n_threads;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) / 2;
+    if (B.thread_stmt[mid] <= stmt) lo = mid;
+    else hi = mid;
+  }
+  uint32_t p = B.thread_prog[lo];
+  veq_fault f{};
+  f.type = VEQ_FAULT_SAFETY;
+  f.kind = VEQ_SAFE_INVALID_ARITH;
+  f.sub = 2;
+  f.detail = detail;
+  f.prog = p;
+  f.tid = lo - B.progs[p].thread_off;
+  f.stmt = stmt;
+  f.step = B.st_step[stmt];
+  emit_fault(B, f);
+}
+
+__device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, const EvalCtx &E, uint32_t i) {
+  const veq_stmt st = B.stmts[i];
+  auto undef_of = [&](uint32_t s) { return intern_undef(T, 3, s >> 29, s); };
+  if (st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX)) {
+    uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
+    uint32_t b = E.log_base[h], n = pos + 2;
+    uint32_t *ids = A.get<uint32_t>(n);
+    if (!ids) return T.id_zero;
+    uint32_t start = 0;
+    for (uint32_t k = 0; k < n; k++) ids[k] = wait_node(B, E.log[b + k]);
+    if (st.op == VEQ_BIN_ADD) {
+      // -inf operand: InvalidArithmetic at the chain statement that consumed
+      // it (symexec.cpp:474-486); that statement's value is a fresh undefined
+      // symbol and the chain continues from it, so everything up to and
+      // including that statement's own leaves is replaced by the symbol.
+      for (uint32_t k = 0; k < n; k++) {
+        if (ids[k] == T.id_neginf) {
+          uint32_t s = E.log_stmt[b + k];
+          arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
+          uint32_t r = k < 1 ? 1 : k;  // the head statement owns leaves 0 and 1
+          ids[r] = undef_of(s);
+          start = r;
+          if (k == 0) k = 1;
+        }
+      }
+      return add_nary(T, A, ids + start, n - start);
+    }
+    return max_nary(T, A, ids, n);
+  }
+  if (st.kind == VEQ_ST_BINOP) {
+    uint32_t a = wait_node(B, B.ref_a[i]), c = wait_node(B, B.ref_b[i]);
+    if (st.op == VEQ_BIN_MUL) {
+      if (a == T.id_neginf || c == T.id_neginf) {
+        arith_fault(B, i, VEQ_DETAIL_NEGINF_MUL);
+        return undef_of(i);
+      }
+      uint32_t ops[2] = {a, c};
+      return mul_canon(T, A, ops, 2);
+    }
+    // Div: div() smart constructor checks then canon_div (expr.cpp:237-245)
+    if (a == T.id_neginf || c == T.id_neginf) {
+      arith_fault(B, i, VEQ_DETAIL_NEGINF_DIV);
+      return undef_of(i);
+    }
+    if (c == T.id_zero) {
+      arith_fault(B, i, VEQ_DETAIL_ZERO_DEN);
+      return undef_of(i);
+    }
+    Node na = ld_node(T, a), nc = ld_node(T, c);
+    if (na.kind == K_CONST && nc.kind == K_CONST) return intern_const(T, rat_div(T, const_val(na), const_val(nc)));
+    return canon_div(T, A, a, c);
+  }
+  // UnOp
+  uint32_t a = wait_node(B, B.ref_a[i]);
+  if (st.op == VEQ_UN_NEG) {
+    if (a == T.id_neginf) {
+      arith_fault(B, i, VEQ_DETAIL_NEGINF_NEG);
+      return undef_of(i);
+    }
+    Node na = ld_node(T, a);
+    if (na.kind == K_CONST) {
+      Rat v = const_val(na);
+      v.n = -v.n;
+      return intern_const(T, v);
+    }
+    uint32_t ops[2] = {T.id_mone, a};
+    return mul_canon(T, A, ops, 2);
+  }
+  if (a == T.id_neginf) {
+    arith_fault(B, i, VEQ_DETAIL_NEGINF_EXP);
+    return undef_of(i);
+  }
+  if (a == T.id_zero) return T.id_one;
+  return intern(T, K_EXP, 0, 0, &a, 1);
+}
+
+__global__ void k_eval(Batch B, Table T, EvalCtx E, const uint32_t *work, uint64_t n_work,
+                       unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap) {
+  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0};
+  for (;;) {
+    unsigned long long w = atomicAdd(cursor, 1ull);
+    if (w >= n_work) break;
+    uint32_t i = work[w];
+    uint64_t mark = A.used;
+    char *mbase = A.base;
+    uint32_t r = eval_stmt(B, T, A, E, i);
+    if (A.base == mbase) A.used = mark;  // recycle scratch of this item
+    __threadfence();
+    atomicExch(B.canon + i, r);
+  }
+}
+
+__global__ void k_final_nodes(Batch B) {
+  uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B.n_cells) return;
+  uint32_t v = B.final_val[c];
+  B.final_node[c] = (v == UNSET) ? UNSET : wait_node(B, v);
+}
+
+__global__ void k_intern_consts(Table T, const veq_rat *consts, uint32_t n, uint32_t *out) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = intern_const(T, Rat{consts[i].num, consts[i].den});
+}
+
+__global__ void k_session_init(Table T, uint32_t *ids) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  ids[0] = intern(T, K_NEGINF, 0, 0, nullptr, 0);
+  ids[1] = intern(T, K_CONST, 0, 1, nullptr, 0);
+  ids[2] = intern(T, K_CONST, 1, 1, nullptr, 0);
+  ids[3] = intern(T, K_CONST, (uint64_t)-1ll, 1, nullptr, 0);
+}
+
+// ---------------------------------------------------------------------------
+// K5: compare. One thread per VC: id equality, then side conditions by an
+// iterative pre-order DFS with a visited set (first-occurrence order of
+// collect_side_conditions, decide.cpp:482-491).
+struct CmpArgs {
+  const uint32_t *cell_a, *cell_b;  // per VC: global cell ids (UNSET64 -> missing)
+  uint64_t n_vcs;
+  veq_vc *vcs;
+  uint32_t *sc_node;
+  uint8_t *sc_dis;
+  unsigned long long *n_sc;
+  uint64_t sc_cap;
+  unsigned long long *n_equal, *n_missing;
+};
+
+__device__ inline void collect_sc(const Table &T, Arena &A, uint32_t root, uint32_t *seen_den, uint32_t &nseen,
+                                  uint32_t cap, uint32_t *visited, uint32_t &nvis, uint32_t vcap) {
+  uint32_t *stack = A.get<uint32_t>(vcap);
+  if (!stack) return;
+  uint32_t sp = 0;
+  stack[sp++] = root;
+  while (sp) {
+    uint32_t x = stack[--sp];
+    Node n = ld_node(T, x);
+    if (!(n.flags & F_HASDIV)) continue;
+    bool vis = false;
+    for (uint32_t q = 0; q < nvis; q++)
+      if (visited[q] == x) {
+        vis = true;
+        break;
+      }
+    if (vis) continue;
+    if (nvis < vcap) visited[nvis++] = x;
+    if (n.kind == K_DIV) {
+      uint32_t den = ld_kid(T, n.p0 + 1);
+      bool dup = false;
+      for (uint32_t q = 0; q < nseen; q++)
+        if (seen_den[q] == den) dup = true;
+      if (!dup && nseen < cap) seen_den[nseen++] = den;
+    }
+    for (int k = (int)n.nkids - 1; k >= 0; k--)
+      if (sp < vcap) stack[sp++] = ld_kid(T, n.p0 + k);
+  }
+}
+
+__global__ void k_compare(Table T, const uint32_t *final_node_a, const uint32_t *final_node_b, CmpArgs C,
+                          char *pool, unsigned long long *pool_used, uint64_t pool_cap) {
+  uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= C.n_vcs) return;
+  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0};
+  uint32_t ca = C.cell_a[v], cb = C.cell_b[v];
+  uint32_t na = ca == UNSET ? UNSET : final_node_a[ca];
+  uint32_t nb = cb == UNSET ? UNSET : final_node_b[cb];
+  veq_vc out{};
+  out.node_a = na;
+  out.node_b = nb;
+  out.equal = (na != UNSET && na == nb);
+  if (na == UNSET || nb == UNSET) atomicAdd(C.n_missing, 1ull);
+  if (out.equal) atomicAdd(C.n_equal, 1ull);
+  out.sc_n = 0;
+  out.sc_off = 0;
+  if (na != UNSET && nb != UNSET) {
+    bool da = ld_node(T, na).flags & F_HASDIV, db = ld_node(T, nb).flags & F_HASDIV;
+    if (da || db) {
+      const uint32_t cap = 4096, vcap = 1u << 16;
+      uint32_t *seen = A.get<uint32_t>(cap);
+      uint32_t *visited = A.get<uint32_t>(vcap);
+      if (seen && visited) {
+        uint32_t nseen = 0, nvis = 0;
+        collect_sc(T, A, na, seen, nseen, cap, visited, nvis, vcap);
+        collect_sc(T, A, nb, seen, nseen, cap, visited, nvis, vcap);
+        unsigned long long off = atomicAdd(C.n_sc, (unsigned long long)nseen);
+        if (off + nseen <= C.sc_cap) {
+          for (uint32_t q = 0; q < nseen; q++) {
+            C.sc_node[off + q] = seen[q];
+            C.sc_dis[off + q] = (ld_node(T, seen[q]).flags & F_POSDEF) ? 1 : 0;
+          }
+          out.sc_off = (uint32_t)off;
+          out.sc_n = nseen;
+        }
+      }
+    }
+  }
+  C.vcs[v] = out;
+}
+
+}  // namespace veqd

@@ -1,0 +1,35 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+
+
+def golden_dirs(prefix=""):
+    out = []
+    for d in sorted(os.listdir(GOLDEN)):
+        p = os.path.join(GOLDEN, d)
+        if os.path.isdir(p) and d.startswith(prefix) and os.path.exists(os.path.join(p, "golden.json")):
+            out.append(p)
+    return out
+
+
+def gen_dirs():
+    g = os.path.join(GOLDEN, "gen")
+    return sorted(os.path.join(g, d) for d in os.listdir(g)) if os.path.isdir(g) else []
+
+
+@pytest.fixture(scope="session")
+def session():
+    from paper_2511_12638_b200.engine import Session
+    s = Session(0, max_nodes=1 << 20, max_kid_words=1 << 22, scratch_bytes=256 << 20)
+    yield s
+    s.close()
