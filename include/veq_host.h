@@ -1,0 +1,44 @@
+/* veq_host.h — C-ABI of the host-side frontend (libveq_host.so).
+ *
+ * Replaces the reference's kernel-IR loader
+ *   ctaeq::parse_kernel / parse_config / elaborate
+ *   (proj/include/ctaeq/frontend.hpp:104-129, called at pipeline.cpp:243-262)
+ * and make_symbolic_inputs (pipeline.hpp:73-74): it turns kernel sources and
+ * a launch configuration into packed IR batches (VEQIR02 byte images, see
+ * include/veq_ir.hpp) ready for veq_load_batch. Elaboration is per CTA;
+ * a grid is elaborated block-parallel on host threads.
+ */
+#ifndef VEQ_HOST_H
+#define VEQ_HOST_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { VEQH_OK = 0, VEQH_E_KERNEL_A = 1, VEQH_E_KERNEL_B = 2, VEQH_E_CONFIG = 3, VEQH_E_ARG = 4 };
+
+/* One result: two VEQIR02 images (kernel A, kernel B) and the input symbol
+ * table as text lines "name<TAB>size". Free with veqh_free. */
+typedef struct veqh_pair {
+  uint8_t *ir_a;
+  size_t ir_a_len;
+  uint8_t *ir_b;
+  size_t ir_b_len;
+  char *inputs;
+} veqh_pair;
+
+/* Elaborates kernel_a / kernel_b under cfg for n_blocks CTAs: block k binds
+ * params.<block_param> = k (block_param NULL or n_blocks == 1: the config as
+ * given). Batch program k is block k. On error returns VEQH_E_* and writes a
+ * message in the reference's wording to err. */
+int veqh_elaborate_grid(const char *kernel_a, const char *kernel_b, const char *cfg, const char *block_param,
+                        uint32_t n_blocks, uint32_t n_workers, int want_names, veqh_pair *out, char *err,
+                        size_t errlen);
+
+void veqh_free(veqh_pair *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -108,12 +108,15 @@ struct HostBatch {
   void save(const std::string &path) const {
     FILE *f = fopen(path.c_str(), "wb");
     if (!f) throw std::runtime_error("veq ir: cannot write " + path);
+    write(f);
+    fclose(f);
+  }
+  void write(FILE *f) const {
     fwrite("VEQIR02", 1, 8, f);
     wvec(f, progs); wvec(f, thread_stmt); wvec(f, thread_nregs); wvec(f, stmts);
     wvec(f, arrays); wvec(f, consts); wvec(f, syncsets); wvec(f, set_words);
     wstrs(f, prog_names); wstrs(f, array_names); wvec(f, thread_reg_off);
     wstrs(f, reg_names); wvec(f, locs);
-    fclose(f);
   }
   static HostBatch load(const std::string &path) {
     FILE *f = fopen(path.c_str(), "rb");

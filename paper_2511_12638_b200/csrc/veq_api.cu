@@ -64,6 +64,7 @@ struct veq_ctx {
   uint32_t *kids = nullptr, *slots = nullptr;
   unsigned long long *counters = nullptr;
   int *error = nullptr;
+  unsigned long long *dbg = nullptr;
   uint32_t *session_ids = nullptr;
   uint64_t *in_base = nullptr, *in_size = nullptr;
   uint64_t n_slots = 0;
@@ -123,7 +124,13 @@ int check_error_flag(veq_ctx *ctx) {
   if (h) {
     if (h == E_BUDGET) return fail(ctx, VEQ_E_BUDGET, "term table / arena capacity exhausted");
     if (h == E_OVERFLOW) return fail(ctx, VEQ_E_RATIONAL_OVERFLOW, "rational coefficient overflow");
-    if (h == E_SCRATCH) return fail(ctx, VEQ_E_SCRATCH, "canonicalisation scratch exhausted");
+    if (h == E_SCRATCH) {
+      unsigned long long d[3] = {0, 0, 0};
+      cudaMemcpy(d, ctx->dbg, sizeof(d), cudaMemcpyDeviceToHost);
+      return fail(ctx, VEQ_E_SCRATCH, "canonicalisation scratch exhausted (request " + std::to_string(d[0]) +
+                                          " B at pool offset " + std::to_string(d[1]) + ", item " +
+                                          std::to_string(d[2]) + ", pool " + std::to_string(ctx->pool_cap) + " B)");
+    }
     return fail(ctx, VEQ_E_INVALID_IR, "internal invariant violated on device (code " + std::to_string(h) + ")");
   }
   return VEQ_OK;
@@ -168,6 +175,7 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   if (cudaMalloc(&ctx->slots, slots * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "slots");
   if (cudaMalloc(&ctx->counters, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "counters");
   if (cudaMalloc(&ctx->error, sizeof(int)) != cudaSuccess) return bail(VEQ_E_OOM, "error");
+  if (cudaMalloc(&ctx->dbg, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "dbg");
   if (cudaMalloc(&ctx->session_ids, 4 * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "ids");
   ctx->pool_cap = ctx->lim.scratch_bytes;
   if (cudaMalloc(&ctx->pool, ctx->pool_cap) != cudaSuccess) return bail(VEQ_E_OOM, "scratch pool");
@@ -181,6 +189,7 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   T.max_kids = ctx->lim.max_kid_words;
   T.slot_mask = slots - 1;
   T.error = ctx->error;
+  T.dbg = ctx->dbg;
   *out = ctx;
   // an empty session so the ctx is usable without declared inputs
   return veq_declare_inputs(ctx, nullptr, 0);
@@ -199,6 +208,7 @@ void veq_close(veq_ctx *ctx) {
   cudaFree(ctx->slots);
   cudaFree(ctx->counters);
   cudaFree(ctx->error);
+  cudaFree(ctx->dbg);
   cudaFree(ctx->session_ids);
   cudaFree(ctx->pool);
   cudaFree(ctx->pool_used);
@@ -258,6 +268,7 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
   CK(cudaMemsetAsync(ctx->slots, 0xff, ctx->n_slots * sizeof(uint32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), ctx->stream));
+  CK(cudaMemsetAsync(ctx->dbg, 0, 4 * sizeof(unsigned long long), ctx->stream));
   k_session_init<<<1, 32, 0, ctx->stream>>>(T, ctx->session_ids);
   CK(cudaGetLastError());
   uint32_t ids[4];
@@ -566,8 +577,9 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
       uint64_t threads = std::min<uint64_t>(n_work, (uint64_t)nsm * 512);
+      uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
       k_eval<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool, ctx->pool_used,
-                                                   ctx->pool_cap);
+                                                   ctx->pool_cap, chunk);
       CK(cudaGetLastError());
       CK(cudaFreeAsync(tmp2, s));
       CK(cudaFreeAsync(cursor, s));
@@ -683,8 +695,9 @@ int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, c
     CK(cudaMemcpyAsync(dca, ca.data(), nv * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dcb, cb.data(), nv * 4, cudaMemcpyHostToDevice, s));
     CmpArgs C{dca, dcb, nv, dv, scn, scd, cnt, sc_cap, cnt + 1, cnt + 2};
+    uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * nv)));
     k_compare<<<blocks(nv, 128), 128, 0, s>>>(ctx->T, A->B.final_node, Bd->B.final_node, C, ctx->pool, ctx->pool_used,
-                                              ctx->pool_cap);
+                                              ctx->pool_cap, chunk);
     CK(cudaGetLastError());
   }
   unsigned long long h[3] = {0, 0, 0};

@@ -27,13 +27,19 @@ struct Arena {
   const Table *T;
   char *base;
   uint64_t cap, used;
+  uint64_t chunk;  // bytes grabbed from the pool per refill
+  uint64_t item;   // current work item (diagnostics)
 
   __device__ void *alloc(uint64_t bytes) {
     bytes = (bytes + 15) & ~15ull;
     if (used + bytes > cap) {
-      uint64_t want = bytes > (256ull << 10) ? bytes : (256ull << 10);
+      uint64_t want = bytes > chunk ? bytes : chunk;
       unsigned long long off = atomicAdd(pool_used, (unsigned long long)want);
       if (off + want > pool_cap) {
+        if (atomicCAS(T->dbg, 0ull, (unsigned long long)want) == 0ull) {
+          T->dbg[1] = off;
+          T->dbg[2] = item;
+        }
         set_error(*T, E_SCRATCH);
         return nullptr;
       }

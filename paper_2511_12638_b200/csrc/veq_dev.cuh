@@ -45,6 +45,7 @@ struct Table {
   unsigned long long *counters;  // [0] nodes, [1] kid words, [2] scratch bytes
   uint64_t max_nodes, max_kids, slot_mask;
   int *error;
+  unsigned long long *dbg;  // [0] failing request bytes, [1] pool offset, [2] item
   uint32_t id_neginf, id_zero, id_one, id_mone;
   const uint64_t *in_base;  // per declared input: first dense rank of its group
   const uint64_t *in_size;

@@ -770,14 +770,16 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
 }
 
 __global__ void k_eval(Batch B, Table T, EvalCtx E, const uint32_t *work, uint64_t n_work,
-                       unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap) {
-  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0};
+                       unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
+                       uint64_t chunk) {
+  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, chunk, 0};
   for (;;) {
     unsigned long long w = atomicAdd(cursor, 1ull);
     if (w >= n_work) break;
     uint32_t i = work[w];
     uint64_t mark = A.used;
     char *mbase = A.base;
+    A.item = i;
     uint32_t r = eval_stmt(B, T, A, E, i);
     if (A.base == mbase) A.used = mark;  // recycle scratch of this item
     __threadfence();
@@ -838,7 +840,11 @@ __device__ inline void collect_sc(const Table &T, Arena &A, uint32_t root, uint3
         break;
       }
     if (vis) continue;
-    if (nvis < vcap) visited[nvis++] = x;
+    if (nvis >= vcap) {
+      set_error(T, E_SCRATCH);
+      return;
+    }
+    visited[nvis++] = x;
     if (n.kind == K_DIV) {
       uint32_t den = ld_kid(T, n.p0 + 1);
       bool dup = false;
@@ -846,16 +852,21 @@ __device__ inline void collect_sc(const Table &T, Arena &A, uint32_t root, uint3
         if (seen_den[q] == den) dup = true;
       if (!dup && nseen < cap) seen_den[nseen++] = den;
     }
-    for (int k = (int)n.nkids - 1; k >= 0; k--)
-      if (sp < vcap) stack[sp++] = ld_kid(T, n.p0 + k);
+    for (int k = (int)n.nkids - 1; k >= 0; k--) {
+      if (sp >= vcap) {
+        set_error(T, E_SCRATCH);
+        return;
+      }
+      stack[sp++] = ld_kid(T, n.p0 + k);
+    }
   }
 }
 
 __global__ void k_compare(Table T, const uint32_t *final_node_a, const uint32_t *final_node_b, CmpArgs C,
-                          char *pool, unsigned long long *pool_used, uint64_t pool_cap) {
+                          char *pool, unsigned long long *pool_used, uint64_t pool_cap, uint64_t chunk) {
   uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= C.n_vcs) return;
-  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0};
+  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, chunk, 0};
   uint32_t ca = C.cell_a[v], cb = C.cell_b[v];
   uint32_t na = ca == UNSET ? UNSET : final_node_a[ca];
   uint32_t nb = cb == UNSET ? UNSET : final_node_b[cb];
@@ -870,7 +881,7 @@ __global__ void k_compare(Table T, const uint32_t *final_node_a, const uint32_t 
   if (na != UNSET && nb != UNSET) {
     bool da = ld_node(T, na).flags & F_HASDIV, db = ld_node(T, nb).flags & F_HASDIV;
     if (da || db) {
-      const uint32_t cap = 4096, vcap = 1u << 16;
+      const uint32_t cap = 1024, vcap = 1u << 13;
       uint32_t *seen = A.get<uint32_t>(cap);
       uint32_t *visited = A.get<uint32_t>(vcap);
       if (seen && visited) {

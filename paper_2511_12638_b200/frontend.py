@@ -1,0 +1,72 @@
+"""Kernel-language frontend (binding of include/veq_host.h, libveq_host.so).
+
+Parses and elaborates .mk kernels under a launch configuration into packed
+IR batches, exactly as the reference frontend would (proj/src/frontend.cpp),
+for one CTA or for a grid of CTAs (block index bound to a config param).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Tuple
+
+from . import ir
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+HOST_LIB = os.path.join(_HERE, "libveq_host.so")
+
+
+class FrontendError(RuntimeError):
+    """Kernel/config rejected; `kernel` is "a", "b" or "config"."""
+
+    def __init__(self, kernel: str, msg: str):
+        super().__init__(msg)
+        self.kernel = kernel
+
+
+class _Pair(C.Structure):
+    _fields_ = [("ir_a", C.POINTER(C.c_uint8)), ("ir_a_len", C.c_size_t), ("ir_b", C.POINTER(C.c_uint8)),
+                ("ir_b_len", C.c_size_t), ("inputs", C.c_void_p)]
+
+
+_lib = None
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(HOST_LIB):
+            raise RuntimeError(f"{HOST_LIB} not built (run __graft_entry__.build())")
+        L = C.CDLL(HOST_LIB)
+        L.veqh_elaborate_grid.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint32,
+                                          C.c_int, C.POINTER(_Pair), C.c_char_p, C.c_size_t]
+        L.veqh_elaborate_grid.restype = C.c_int
+        L.veqh_free.argtypes = [C.POINTER(_Pair)]
+        L.veqh_free.restype = None
+        _lib = L
+    return _lib
+
+
+def elaborate_pair(kernel_a: str, kernel_b: str, cfg: str, block_param: Optional[str] = None, n_blocks: int = 1,
+                   workers: int = 0, want_names: bool = True) -> Tuple[ir.Batch, ir.Batch, List[Tuple[str, int]]]:
+    """Returns (batch A, batch B, input symbol table)."""
+    L = _L()
+    out = _Pair()
+    err = C.create_string_buffer(4096)
+    workers = workers or (os.cpu_count() or 1)
+    st = L.veqh_elaborate_grid(kernel_a.encode(), kernel_b.encode(), cfg.encode(),
+                               block_param.encode() if block_param else None, n_blocks, workers,
+                               1 if want_names else 0, C.byref(out), err, len(err))
+    if st != 0:
+        raise FrontendError({1: "a", 2: "b", 3: "config"}.get(st, "arg"), err.value.decode())
+    try:
+        a = ir.loads(C.string_at(out.ir_a, out.ir_a_len))
+        b = ir.loads(C.string_at(out.ir_b, out.ir_b_len))
+        text = C.string_at(out.inputs).decode()
+    finally:
+        L.veqh_free(C.byref(out))
+    inputs = []
+    for line in text.splitlines():
+        name, size = line.split("\t")
+        inputs.append((name, int(size)))
+    return a, b, inputs

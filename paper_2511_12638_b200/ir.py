@@ -112,9 +112,13 @@ def _rstrs(buf: memoryview, pos: int):
 
 
 def load(path: str) -> Batch:
-    data = open(path, "rb").read()
+    with open(path, "rb") as f:
+        return loads(f.read(), path)
+
+
+def loads(data: bytes, what: str = "<buffer>") -> Batch:
     if data[:8] != b"VEQIR02\0":
-        raise ValueError(f"{path}: not a VEQIR02 file")
+        raise ValueError(f"{what}: not a VEQIR02 image")
     buf = memoryview(data)
     pos = 8
     progs, pos = _rvec(buf, pos, PROG_DT)
