@@ -1,0 +1,343 @@
+#!/usr/bin/env python3
+"""Benchmark: output elements verified per second per kernel pair.
+
+Workload (BASELINE.json configs[1], the metric's config): warp-shuffle tree
+reduction vs sequential sum over N = 2^20 inputs, as 1024 independent CTA
+pairs of 1024 elements (each CTA pair is one reference
+check_equivalence). A step = execute kernel A's batch, kernel B's batch and
+the per-VC canonical compare on the GPU (the reference's t_exec_a + t_exec_b
++ t_decide), starting from an empty term DAG, plus the cross-rank verdict
+all-reduce when N > 1. Packed IR is resident in HBM for `value`; `e2e`
+re-uploads it from pinned host memory every step through the C-ABI and reads
+the verdicts back.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU: torchrun, one rank per GPU, weak scaling (each rank owns 1024 CTA
+pairs of a world-sized input).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import shutil
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "output elements verified/sec per kernel pair at 1/2/4/8 B200 vs CPU ref"
+HBM_FALLBACK = 6650.0
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j.get("hbm_gbs", HBM_FALLBACK)), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+def ref_bench(workload, blocks, seconds, threads):
+    """The reference checker (oracle/_ref, built from the reference sources)
+    on a bounded sample of the workload's CTA pairs, all host threads."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+    if not os.path.exists(exe):
+        return None, "oracle/_ref/ref_harness not built"
+    d = tempfile.mkdtemp(prefix="veq_ref_")
+    open(os.path.join(d, "a.mk"), "w").write(workload.kernel_a)
+    open(os.path.join(d, "b.mk"), "w").write(workload.kernel_b)
+    lst = []
+    for b in blocks:
+        p = os.path.join(d, f"cfg_{b}.cfg")
+        open(p, "w").write(re.sub(r"params\.B = \d+", f"params.B = {b}", workload.cfg))
+        lst.append(p)
+    open(os.path.join(d, "list.txt"), "w").write("\n".join(lst) + "\n")
+    out = subprocess.run([exe, "bench", os.path.join(d, "a.mk"), os.path.join(d, "b.mk"),
+                          os.path.join(d, "list.txt"), str(threads), str(seconds)],
+                         capture_output=True, text=True, timeout=seconds * 10 + 120)
+    shutil.rmtree(d, ignore_errors=True)
+    if out.returncode != 0:
+        return None, out.stderr.strip()[-300:]
+    return json.loads(out.stdout.strip().splitlines()[-1]), None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--blocks", type=int, default=1024, help="CTA pairs per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    from paper_2511_12638_b200 import workloads
+    W = workloads.c2_reduce(n_blocks=args.blocks * world, block=1024)
+    cfg_json = {"workload": "C2 warp-shuffle tree reduction vs sequential sum, N=2^20 per GPU as "
+                            f"{args.blocks} CTA pairs x 1024 elements",
+                "kernel_a": "reduce_seq (1 thread)", "kernel_b": "reduce_shfl (1024 threads, warp 32)",
+                "cta_pairs_per_gpu": args.blocks, "elements_per_step_per_gpu": args.blocks,
+                "parallelism": f"dp{world} (CTA pairs sharded, verdict all-reduce)",
+                "l2": "working set re-generated every step (term table cleared; IR > 126 MB L2)"}
+    ncpu = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        per = max(1, args.steps)
+        samples = []
+        for s in range(args.warmup + per):
+            blocks = list(range((s * 8) % args.blocks, (s * 8) % args.blocks + 8))
+            r, err = ref_bench(W, blocks, max(2.0, args.cpu_seconds / per), ncpu)
+            if r is None:
+                print(json.dumps({"impl": "reference", "unavailable": err}))
+                return
+            if s >= args.warmup:
+                samples.append(r)
+        el = sum(r["elements"] for r in samples)
+        busy = sum(r["busy_s"] for r in samples) / ncpu
+        v = el / busy if busy > 0 else 0.0
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": world,
+            "steps": per, "warmup": args.warmup, "ms_per_step": 1000.0 * busy / per if per else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "exact rational (int64/GMP)",
+            "data": "synthetic", "config": cfg_json,
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference",
+                             "sample": f"{el} CTA pairs (8 per step) of the C2 grid; exec+decide span timed"},
+            "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import numpy as np
+    import torch
+    from paper_2511_12638_b200 import frontend, native as N
+    from paper_2511_12638_b200.engine import Session
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t0 = time.time()
+    a, b, inputs = frontend.elaborate_pair(W.kernel_a, W.kernel_b, W.cfg, "B", args.blocks, want_names=False,
+                                           block_base=rank * args.blocks)
+    t_elab = time.time() - t0
+    S = len(a.stmts) + len(b.stmts)
+    sess = Session(local, max_nodes=max(1 << 22, 4 * S // 10), max_kid_words=(1 << 24) + 4 * S,
+                   scratch_bytes=8 << 30)
+    L = N.lib()
+    sess.declare_inputs(inputs)
+    ba, bb = sess.load(a), sess.load(b)
+    oa, ob = [0], [0]  # y is the only Out array (array-name order)
+    for k, name in enumerate(a.array_names[:int(a.progs[0]["n_arrays"])]):
+        if int(a.arrays[k]["role"]) == N.ROLE_OUT:
+            oa = [k]
+    for k, name in enumerate(b.array_names[:int(b.progs[0]["n_arrays"])]):
+        if int(b.arrays[k]["role"]) == N.ROLE_OUT:
+            ob = [k]
+    stream = torch.cuda.ExternalStream(L.veq_stream(sess.ctx))
+    counters = torch.zeros(4, dtype=torch.float64, device="cuda")
+
+    def step():
+        st = L.veq_clear_terms(sess.ctx)
+        assert st == 0
+        ra = sess.run_raw(ba)
+        rb = sess.run_raw(bb)
+        vc = sess.compare_raw(ba, bb, oa, ob)
+        launches = ra.n_launches + rb.n_launches + 2
+        if dist is not None:
+            counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)
+            dist.all_reduce(counters)
+        return ra, rb, vc, launches
+
+    # correctness gate: every VC equal, no faults
+    ra, rb, vc, _ = step()
+    ok = vc.n_equal == vc.n_vcs == args.blocks and ra.n_faults == 0 and rb.n_faults == 0
+    if not ok:
+        print(f"[bench] rank {rank}: verification failed: {vc.n_equal}/{vc.n_vcs} equal, faults "
+              f"{ra.n_faults}/{rb.n_faults}", file=sys.stderr)
+        sys.exit(1)
+    # instrumented pass: per-phase device time (CUDA events on the ctx stream)
+    L.veq_set_timing(sess.ctx, 1)
+    ra_t, rb_t, _, _ = step()
+    L.veq_set_timing(sess.ctx, 0)
+    phases = {}
+    for i, name in enumerate(N.PHASES):
+        phases[name] = float(ra_t.phase_ms[i]) + float(rb_t.phase_ms[i])
+
+    for _ in range(args.warmup):
+        step()
+
+    def timed(fn, k):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches = 0
+        for _ in range(k):
+            launches += fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches
+
+    with ClockSampler(local) as clk:
+        ms, launches = timed(lambda: step()[3], args.steps)
+    ms_step = ms / args.steps
+    elements_step = args.blocks * world
+    value = elements_step / (ms_step / 1000.0)
+
+    # e2e: public API from pinned host buffers each step (H2D IR, D2H verdicts)
+    def pin(batch):
+        import ctypes
+        keep = []
+        for f in ("progs", "thread_stmt", "thread_nregs", "stmts", "arrays", "consts", "syncsets", "set_words"):
+            arr = getattr(batch, f)
+            t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8)).pin_memory()
+            keep.append(t)
+            setattr(batch, f, t.numpy().view(arr.dtype))
+        return keep
+
+    keep = pin(a) + pin(b)
+    h2d = a.nbytes() + b.nbytes()
+    d2h = elements_step // world * 24
+
+    def e2e_step():
+        sess.declare_inputs(inputs)
+        xa, xb = sess.load(a), sess.load(b)
+        ra = sess.run_raw(xa)
+        rb = sess.run_raw(xb)
+        vc = sess.compare_raw(xa, xb, oa, ob)
+        assert vc.n_equal == vc.n_vcs
+        if dist is not None:
+            counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)
+            dist.all_reduce(counters)
+        return ra.n_launches + rb.n_launches + 2
+
+    e2e_step()
+    e2e_k = max(1, min(args.steps, 5))
+    ms_e2e, _ = timed(e2e_step, e2e_k)
+    e2e_value = elements_step / (ms_e2e / e2e_k / 1000.0)
+
+    # roofline: dominant phase, algorithmic bytes:
+    #   exec 16 B per executed statement; sort+memscan 32 B per access tuple;
+    #   eval 2 x (16 + 4k) per created node (written once, read once)
+    peak, peak_kind = peaks()
+    S_exec = ra.n_stmts_executed + rb.n_stmts_executed
+    R = ra.n_access + rb.n_access
+    U_bytes = 16 * (ra.n_new_nodes + rb.n_new_nodes) + 4 * (ra.n_new_kid_words + rb.n_new_kid_words)
+    alg = {"exec": 16 * S_exec, "sort": 16 * R, "memscan": 16 * R, "eval": 2 * U_bytes}
+    dom = max(phases, key=lambda k: phases[k])
+    dom_bytes = alg.get(dom, 0)
+    achieved = dom_bytes / (phases[dom] / 1000.0) / 1e9 if phases[dom] > 0 else 0.0
+    b_min = 16 * S_exec + 2 * U_bytes + 32 * R + 16 * elements_step // world
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "exact rational (int64 num/den), u32 term ids", "data": "synthetic",
+        "config": cfg_json,
+        "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "peak_kind": peak_kind, "alg_bytes_per_launch": dom_bytes},
+        "step_roofline": {"b_min_bytes": b_min, "achieved_gbs": b_min / (ms_step / 1000.0) / 1e9,
+                          "frac": b_min / (ms_step / 1000.0) / 1e9 / peak},
+        "phases_ms": phases,
+        "counts": {"S": S_exec, "R": R, "new_nodes": ra.n_new_nodes + rb.n_new_nodes,
+                   "work_items": ra.n_work + rb.n_work, "t_elab_s": t_elab},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ncb = max(8, min(args.blocks, 64))
+        r, err = ref_bench(W, list(range(ncb)), args.cpu_seconds, ncpu)
+        if r is not None:
+            busy = r["busy_s"] / ncpu
+            line["cpu_baseline"] = {"value": r["elements"] / busy if busy else 0.0, "unit": "elements/s",
+                                    "cores": ncpu, "kind": "reference",
+                                    "sample": f"{r['pairs']} of the first {ncb} CTA pairs, "
+                                              f"{args.cpu_seconds:.0f}s bound, exec+decide span"}
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "elements/s", "cores": ncpu, "kind": "reference",
+                                    "sample": f"unavailable: {err}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    del keep
+    sess.close()
+
+
+if __name__ == "__main__":
+    main()

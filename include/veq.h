@@ -179,6 +179,17 @@ typedef struct veq_fault {
   uint32_t arr;     /* memory faults: program-local array index          */
 } veq_fault;
 
+/* Phases of veq_run, timed with CUDA events on the ctx stream when enabled. */
+enum { VEQ_PH_SCHEDULE = 0, VEQ_PH_EXEC, VEQ_PH_SORT, VEQ_PH_MEMSCAN, VEQ_PH_RESOLVE, VEQ_PH_CHAINS,
+       VEQ_PH_WORKLIST, VEQ_PH_EVAL, VEQ_PH_FINALS, VEQ_MAX_PHASES };
+int veq_set_timing(veq_ctx *ctx, int on);
+/* The CUDA stream (cudaStream_t) every kernel of this ctx is launched on,
+ * for callers that time or order work around it. */
+void *veq_stream(veq_ctx *ctx);
+/* Resets the term table of the current session (declared inputs and loaded
+ * batches stay valid): every run after it starts from an empty DAG. */
+int veq_clear_terms(veq_ctx *ctx);
+
 /* Per-program run summary (ctaeq::RunResult, symexec.hpp:214-225). */
 typedef struct veq_prog_result {
   uint64_t steps;
@@ -205,6 +216,12 @@ typedef struct veq_run_out {
   uint64_t n_kid_words;
   uint64_t n_work;                /* canonicalised raw nodes         */
   uint64_t n_access;              /* race-check access tuples (R)    */
+  uint64_t n_stmts_executed;      /* S: statements executed          */
+  uint64_t n_new_nodes;           /* term nodes created by this run  */
+  uint64_t n_new_kid_words;       /* kid words created by this run   */
+  uint32_t n_launches;            /* device kernel launches (incl. library sort/scan) */
+  uint32_t n_phases;
+  float phase_ms[VEQ_MAX_PHASES]; /* per-phase device time when timing is on (veq_set_timing) */
 } veq_run_out;
 
 int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out);

@@ -29,12 +29,12 @@ typedef struct veqh_pair {
 } veqh_pair;
 
 /* Elaborates kernel_a / kernel_b under cfg for n_blocks CTAs: block k binds
- * params.<block_param> = k (block_param NULL or n_blocks == 1: the config as
+ * params.<block_param> = block_base + k (block_param NULL: the config as
  * given). Batch program k is block k. On error returns VEQH_E_* and writes a
  * message in the reference's wording to err. */
 int veqh_elaborate_grid(const char *kernel_a, const char *kernel_b, const char *cfg, const char *block_param,
-                        uint32_t n_blocks, uint32_t n_workers, int want_names, veqh_pair *out, char *err,
-                        size_t errlen);
+                        uint32_t block_base, uint32_t n_blocks, uint32_t n_workers, int want_names, veqh_pair *out,
+                        char *err, size_t errlen);
 
 void veqh_free(veqh_pair *p);
 

@@ -31,8 +31,8 @@ uint8_t *to_image(const veq::HostBatch &b, size_t *len) {
 }  // namespace
 
 extern "C" int veqh_elaborate_grid(const char *kernel_a, const char *kernel_b, const char *cfg_src,
-                                   const char *block_param, uint32_t n_blocks, uint32_t n_workers, int want_names,
-                                   veqh_pair *out, char *err, size_t errlen) {
+                                   const char *block_param, uint32_t block_base, uint32_t n_blocks,
+                                   uint32_t n_workers, int want_names, veqh_pair *out, char *err, size_t errlen) {
   if (!kernel_a || !kernel_b || !cfg_src || !out || n_blocks == 0) return VEQH_E_ARG;
   std::memset(out, 0, sizeof(*out));
   veqh::LaunchConfig cfg;
@@ -55,10 +55,10 @@ extern "C" int veqh_elaborate_grid(const char *kernel_a, const char *kernel_b, c
     put_err(err, errlen, e.what());
     return VEQH_E_KERNEL_B;
   }
-  const bool grid = block_param && *block_param && n_blocks > 1;
+  const bool grid = block_param && *block_param;
   auto cfg_for = [&](uint32_t blk) {
     veqh::LaunchConfig c = cfg;
-    if (grid) c.params[block_param] = blk;
+    if (grid) c.params[block_param] = (int64_t)block_base + blk;
     return c;
   };
   std::vector<veqh::InputDecl> inputs;

@@ -41,6 +41,8 @@ struct BatchDev {
   uint32_t n_threads = 0;
   // device arrays (owned)
   std::vector<void *> owned;
+  veq_rat *dconsts = nullptr;
+  uint32_t n_consts = 0;
   Batch B{};
   // host-visible run results
   std::vector<veq_prog_result> res;
@@ -81,6 +83,10 @@ struct veq_ctx {
   std::vector<uint32_t> sc_node;
   std::vector<uint8_t> sc_dis;
   uint64_t last_equal = 0, last_missing = 0, last_vcs = 0, last_faults = 0;
+  // instrumentation
+  bool timing = false;
+  cudaEvent_t ev0[VEQ_MAX_PHASES] = {}, ev1[VEQ_MAX_PHASES] = {};
+  uint32_t launches = 0;
 };
 
 namespace {
@@ -264,20 +270,43 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
   T.in_base = ctx->in_base;
   T.in_size = ctx->in_size;
   T.n_inputs = n;
-  // fresh term table
+  int r = veq_clear_terms(ctx);
+  if (r) return r;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return VEQ_OK;
+}
+
+int veq_clear_terms(veq_ctx *ctx) {
+  if (!ctx) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  Table &T = ctx->T;
   CK(cudaMemsetAsync(ctx->slots, 0xff, ctx->n_slots * sizeof(uint32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dbg, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  // a single thread interns -inf, 0, 1, -1 first into an empty table, so
+  // their ids are 0..3 without a host round trip
   k_session_init<<<1, 32, 0, ctx->stream>>>(T, ctx->session_ids);
+  ctx->launches++;
   CK(cudaGetLastError());
-  uint32_t ids[4];
-  CK(cudaMemcpyAsync(ids, ctx->session_ids, sizeof(ids), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  T.id_neginf = ids[0];
-  T.id_zero = ids[1];
-  T.id_one = ids[2];
-  T.id_mone = ids[3];
+  T.id_neginf = 0;
+  T.id_zero = 1;
+  T.id_one = 2;
+  T.id_mone = 3;
+  return VEQ_OK;
+}
+
+void *veq_stream(veq_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int veq_set_timing(veq_ctx *ctx, int on) {
+  if (!ctx) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (on && !ctx->ev0[0])
+    for (int i = 0; i < VEQ_MAX_PHASES; i++) {
+      CK(cudaEventCreate(&ctx->ev0[i]));
+      CK(cudaEventCreate(&ctx->ev1[i]));
+    }
+  ctx->timing = on != 0;
   return VEQ_OK;
 }
 
@@ -421,8 +450,9 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     delete bd;
     return r;
   }
-  if (d->n_consts) k_intern_consts<<<blocks(d->n_consts, 256), 256, 0, ctx->stream>>>(ctx->T, dconsts, d->n_consts, cn);
   B.const_node = cn;
+  bd->dconsts = dconsts;
+  bd->n_consts = d->n_consts;
   // run-state buffers
 #define AL(field, n, T_)                                                  \
   do {                                                                    \
@@ -471,6 +501,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   cudaStream_t s = ctx->stream;
   const uint64_t S = bd->n_stmts;
   // reset run state
+  unsigned long long cnt0[2] = {0, 0};
+  CK(cudaMemcpyAsync(cnt0, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
   CK(cudaMemsetAsync(B.seg_base, 0xff, bd->n_segs * 4, s));
   CK(cudaMemsetAsync(B.regfile, 0xff, std::max<uint64_t>(bd->n_regs, 1) * 4, s));
   CK(cudaMemsetAsync(B.st_step, 0xff, S * 4, s));
@@ -481,16 +513,29 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaMemsetAsync(B.n_faults, 0, 8, s));
   CK(cudaMemsetAsync(B.final_val, 0xff, std::max<uint64_t>(bd->n_cells, 1) * 4, s));
   CK(cudaMemsetAsync(ctx->pool_used, 0, 8, s));
+  const uint32_t launches0 = ctx->launches;
+#define PH0(p) do { if (ctx->timing) CK(cudaEventRecord(ctx->ev0[p], s)); } while (0)
+#define PH1(p) do { if (ctx->timing) CK(cudaEventRecord(ctx->ev1[p], s)); } while (0)
+#define LAUNCH(...) do { __VA_ARGS__; ctx->launches++; } while (0)
+  // constants are interned per run so a cleared term table stays consistent
+  if (bd->n_consts)
+    LAUNCH(k_intern_consts<<<blocks(bd->n_consts, 256), 256, 0, s>>>(ctx->T, bd->dconsts, bd->n_consts,
+                                                                       (uint32_t *)B.const_node));
   // K0
-  if (B.n_progs) k_schedule<<<B.n_progs, SCHED_BLOCK, 0, s>>>(B);
+  PH0(VEQ_PH_SCHEDULE);
+  if (B.n_progs) LAUNCH(k_schedule<<<B.n_progs, SCHED_BLOCK, 0, s>>>(B));
+  PH1(VEQ_PH_SCHEDULE);
   CK(cudaGetLastError());
   // K3
-  if (B.n_threads) k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T);
+  PH0(VEQ_PH_EXEC);
+  if (B.n_threads) LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
+  PH1(VEQ_PH_EXEC);
   CK(cudaGetLastError());
   unsigned long long n_tup = 0;
   CK(cudaMemcpyAsync(&n_tup, B.n_tup, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   // K4: sort access tuples by (cell, step) and scan per cell
+  PH0(VEQ_PH_SORT);
   if (n_tup) {
     unsigned long long *k2 = nullptr, *v2 = nullptr;
     uint32_t *starts = nullptr;
@@ -501,18 +546,24 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMallocAsync(&starts, n_tup * 4, s));
     CK(cudaMallocAsync(&n_starts, 8, s));
     CK(cudaMallocAsync(&rs, n_tup * sizeof(Reader), s));
-    int end_bit = 64;
+    int cb = 1;
+    while ((1ull << cb) < bd->n_cells + 1) cb++;
+    int end_bit = 32 + cb;
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
     void *tmp = nullptr;
     CK(cudaMallocAsync(&tmp, tmp_bytes, s));
     cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
+    ctx->launches += (end_bit + 7) / 8 + 1;
     CK(cudaMemsetAsync(n_starts, 0, 8, s));
-    k_seg_heads<<<blocks(n_tup, 256), 256, 0, s>>>(k2, n_tup, starts, n_starts);
+    LAUNCH(k_seg_heads<<<blocks(n_tup, 256), 256, 0, s>>>(k2, n_tup, starts, n_starts));
+    PH1(VEQ_PH_SORT);
     unsigned long long nseg = 0;
     CK(cudaMemcpyAsync(&nseg, n_starts, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    k_mem_scan<<<blocks(nseg, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, (uint32_t)nseg, n_tup, rs);
+    PH0(VEQ_PH_MEMSCAN);
+    LAUNCH(k_mem_scan<<<blocks(nseg, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, (uint32_t)nseg, n_tup, rs));
+    PH1(VEQ_PH_MEMSCAN);
     CK(cudaGetLastError());
     CK(cudaFreeAsync(tmp, s));
     CK(cudaFreeAsync(k2, s));
@@ -520,27 +571,35 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaFreeAsync(starts, s));
     CK(cudaFreeAsync(n_starts, s));
     CK(cudaFreeAsync(rs, s));
+  } else {
+    PH1(VEQ_PH_SORT);
+    PH0(VEQ_PH_MEMSCAN);
+    PH1(VEQ_PH_MEMSCAN);
   }
   // resolve loads, then operands, then count uses (incl. final cells)
+  PH0(VEQ_PH_RESOLVE);
   if (S) {
-    k_resolve_loads<<<blocks(S, 256), 256, 0, s>>>(B);
-    k_resolve<<<blocks(S, 256), 256, 0, s>>>(B);
-    k_count_uses<<<blocks(S, 256), 256, 0, s>>>(B);
+    LAUNCH(k_resolve_loads<<<blocks(S, 256), 256, 0, s>>>(B));
+    LAUNCH(k_resolve<<<blocks(S, 256), 256, 0, s>>>(B));
+    LAUNCH(k_count_uses<<<blocks(S, 256), 256, 0, s>>>(B));
   }
-  if (bd->n_cells) k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B);
+  if (bd->n_cells) LAUNCH(k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
+  PH1(VEQ_PH_RESOLVE);
   CK(cudaGetLastError());
   // chain logs
   uint32_t *sz = nullptr, *base = nullptr, *log = nullptr, *log_stmt = nullptr;
   unsigned long long n_work = 0;
   if (S) {
+    PH0(VEQ_PH_CHAINS);
     CK(cudaMallocAsync(&sz, S * 4, s));
     CK(cudaMallocAsync(&base, S * 4, s));
-    k_chain_sizes<<<blocks(S, 256), 256, 0, s>>>(B, sz);
+    LAUNCH(k_chain_sizes<<<blocks(S, 256), 256, 0, s>>>(B, sz));
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, base, (int64_t)S, s);
     void *tmp = nullptr;
     CK(cudaMallocAsync(&tmp, tb, s));
     cub::DeviceScan::ExclusiveSum(tmp, tb, sz, base, (int64_t)S, s);
+    ctx->launches += 2;
     uint32_t last_sz = 0, last_base = 0;
     CK(cudaMemcpyAsync(&last_sz, sz + S - 1, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&last_base, base + S - 1, 4, cudaMemcpyDeviceToHost, s));
@@ -548,9 +607,11 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     uint64_t nlog = (uint64_t)last_sz + last_base;
     CK(cudaMallocAsync(&log, std::max<uint64_t>(nlog, 1) * 4, s));
     CK(cudaMallocAsync(&log_stmt, std::max<uint64_t>(nlog, 1) * 4, s));
-    k_chain_scatter<<<blocks(S, 256), 256, 0, s>>>(B, base, log, log_stmt);
+    LAUNCH(k_chain_scatter<<<blocks(S, 256), 256, 0, s>>>(B, base, log, log_stmt));
     CK(cudaFreeAsync(tmp, s));
+    PH1(VEQ_PH_CHAINS);
     // work list sorted by (program, step)
+    PH0(VEQ_PH_WORKLIST);
     unsigned long long *wk = nullptr, *wk2 = nullptr, *nw = nullptr;
     uint32_t *wv = nullptr, *wv2 = nullptr;
     CK(cudaMallocAsync(&wk, S * 8, s));
@@ -559,17 +620,25 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMallocAsync(&wv2, S * 4, s));
     CK(cudaMallocAsync(&nw, 8, s));
     CK(cudaMemsetAsync(nw, 0, 8, s));
-    k_make_work<<<blocks(S, 256), 256, 0, s>>>(B, wk, wv, nw);
+    LAUNCH(k_make_work<<<blocks(S, 256), 256, 0, s>>>(B, wk, wv, nw));
     CK(cudaMemcpyAsync(&n_work, nw, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    void *tmp2 = nullptr;
     if (n_work) {
       int pb = 1;
       while ((1ull << pb) < B.n_progs + 1) pb++;
+      int sb = 1;
+      while ((1ull << sb) < S + 1 && sb < 32) sb++;
+      // key = prog << 32 | step; sort only the bits in use
       size_t tb2 = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, 32 + pb, s);
-      void *tmp2 = nullptr;
       CK(cudaMallocAsync(&tmp2, tb2, s));
       cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, 32 + pb, s);
+      ctx->launches += (32 + pb + 7) / 8 + 1;
+    }
+    PH1(VEQ_PH_WORKLIST);
+    PH0(VEQ_PH_EVAL);
+    if (n_work) {
       unsigned long long *cursor = nullptr;
       CK(cudaMallocAsync(&cursor, 8, s));
       CK(cudaMemsetAsync(cursor, 0, 8, s));
@@ -578,19 +647,22 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
       uint64_t threads = std::min<uint64_t>(n_work, (uint64_t)nsm * 512);
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
-      k_eval<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool, ctx->pool_used,
-                                                   ctx->pool_cap, chunk);
+      LAUNCH(k_eval<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool,
+                                                          ctx->pool_used, ctx->pool_cap, chunk));
       CK(cudaGetLastError());
       CK(cudaFreeAsync(tmp2, s));
       CK(cudaFreeAsync(cursor, s));
     }
+    PH1(VEQ_PH_EVAL);
     CK(cudaFreeAsync(wk, s));
     CK(cudaFreeAsync(wk2, s));
     CK(cudaFreeAsync(wv, s));
     CK(cudaFreeAsync(wv2, s));
     CK(cudaFreeAsync(nw, s));
   }
-  if (bd->n_cells) k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B);
+  PH0(VEQ_PH_FINALS);
+  if (bd->n_cells) LAUNCH(k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
+  PH1(VEQ_PH_FINALS);
   CK(cudaGetLastError());
   if (sz) {
     CK(cudaFreeAsync(sz, s));
@@ -652,6 +724,18 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     out->n_kid_words = nn[1];
     out->n_work = n_work;
     out->n_access = n_tup;
+    uint64_t executed = 0;
+    for (uint32_t p = 0; p < P; p++) executed += bd->res[p].steps - bd->res[p].releases;
+    out->n_stmts_executed = executed;
+    out->n_new_nodes = nn[0] - cnt0[0];
+    out->n_new_kid_words = nn[1] - cnt0[1];
+    out->n_launches = ctx->launches - launches0;
+    out->n_phases = VEQ_MAX_PHASES;
+    for (int i = 0; i < VEQ_MAX_PHASES; i++) {
+      float ms = 0;
+      if (ctx->timing) cudaEventElapsedTime(&ms, ctx->ev0[i], ctx->ev1[i]);
+      out->phase_ms[i] = ms;
+    }
   }
   return VEQ_OK;
 }

@@ -33,7 +33,8 @@ struct Arena {
   __device__ void *alloc(uint64_t bytes) {
     bytes = (bytes + 15) & ~15ull;
     if (used + bytes > cap) {
-      uint64_t want = bytes > chunk ? bytes : chunk;
+      uint64_t want = (bytes > chunk ? bytes : chunk);
+      want = (want + 255) & ~255ull;  // keep every refill 256-B aligned
       unsigned long long off = atomicAdd(pool_used, (unsigned long long)want);
       if (off + want > pool_cap) {
         if (atomicCAS(T->dbg, 0ull, (unsigned long long)want) == 0ull) {

@@ -39,7 +39,7 @@ def _L():
             raise RuntimeError(f"{HOST_LIB} not built (run __graft_entry__.build())")
         L = C.CDLL(HOST_LIB)
         L.veqh_elaborate_grid.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint32,
-                                          C.c_int, C.POINTER(_Pair), C.c_char_p, C.c_size_t]
+                                          C.c_uint32, C.c_int, C.POINTER(_Pair), C.c_char_p, C.c_size_t]
         L.veqh_elaborate_grid.restype = C.c_int
         L.veqh_free.argtypes = [C.POINTER(_Pair)]
         L.veqh_free.restype = None
@@ -48,14 +48,16 @@ def _L():
 
 
 def elaborate_pair(kernel_a: str, kernel_b: str, cfg: str, block_param: Optional[str] = None, n_blocks: int = 1,
-                   workers: int = 0, want_names: bool = True) -> Tuple[ir.Batch, ir.Batch, List[Tuple[str, int]]]:
-    """Returns (batch A, batch B, input symbol table)."""
+                   workers: int = 0, want_names: bool = True,
+                   block_base: int = 0) -> Tuple[ir.Batch, ir.Batch, List[Tuple[str, int]]]:
+    """Returns (batch A, batch B, input symbol table). With block_param, CTA k
+    of the batch binds params.<block_param> = block_base + k."""
     L = _L()
     out = _Pair()
     err = C.create_string_buffer(4096)
     workers = workers or (os.cpu_count() or 1)
     st = L.veqh_elaborate_grid(kernel_a.encode(), kernel_b.encode(), cfg.encode(),
-                               block_param.encode() if block_param else None, n_blocks, workers,
+                               block_param.encode() if block_param else None, block_base, n_blocks, workers,
                                1 if want_names else 0, C.byref(out), err, len(err))
     if st != 0:
         raise FrontendError({1: "a", 2: "b", 3: "config"}.get(st, "arg"), err.value.decode())

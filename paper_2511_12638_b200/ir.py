@@ -82,7 +82,10 @@ class Batch:
         return int(np.searchsorted(self.thread_stmt, s, side="right") - 1)
 
     def reg_name(self, thread: int, reg: int) -> str:
-        return self.reg_names[int(self.thread_reg_off[thread]) + int(reg)]
+        lo, hi = int(self.thread_reg_off[thread]), int(self.thread_reg_off[thread + 1])
+        if lo + int(reg) >= hi:  # elaborated without register names
+            return f"r{int(reg)}"
+        return self.reg_names[lo + int(reg)]
 
     def loc(self, s: int):
         if self.locs is None or len(self.locs) == 0:

@@ -78,7 +78,8 @@ class veq_run_out(C.Structure):
     _fields_ = [("n_progs", u32), ("progs", P(veq_prog_result)), ("n_faults", u64), ("faults", P(veq_fault)),
                 ("n_threads_total", u32), ("thread_state", P(u8)), ("thread_block_set", P(u32)),
                 ("thread_block_stmt", P(u64)), ("n_nodes", u64), ("n_kid_words", u64), ("n_work", u64),
-                ("n_access", u64)]
+                ("n_access", u64), ("n_stmts_executed", u64), ("n_new_nodes", u64), ("n_new_kid_words", u64),
+                ("n_launches", u32), ("n_phases", u32), ("phase_ms", C.c_float * 9)]
 
 
 class veq_vc(C.Structure):
@@ -132,12 +133,18 @@ def lib() -> C.CDLL:
     L.veq_compare.argtypes = [vp, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
     L.veq_export_dag.argtypes = [vp, P(u32), C.c_size_t, P(veq_dag_buf)]
     L.veq_verdict_counters.argtypes = [vp, P(u64)]
+    L.veq_set_timing.argtypes = [vp, C.c_int]
+    L.veq_stream.argtypes = [vp]
+    L.veq_stream.restype = vp
+    L.veq_clear_terms.argtypes = [vp]
     for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_fetch_cells", "veq_compare",
-              "veq_export_dag", "veq_verdict_counters"):
+              "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
 
 
 EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_declare_inputs", "veq_load_batch",
-            "veq_run", "veq_fetch_cells", "veq_compare", "veq_export_dag", "veq_verdict_counters"]
+            "veq_run", "veq_fetch_cells", "veq_compare", "veq_export_dag", "veq_verdict_counters",
+            "veq_set_timing", "veq_clear_terms", "veq_stream"]
+PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]

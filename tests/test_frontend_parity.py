@@ -65,3 +65,15 @@ def test_frontend_errors_match_reference_wording():
     with pytest.raises(frontend.FrontendError) as e:
         frontend.elaborate_pair(dd, dd, "version = 1\nthreads = 4\ninputs = x\noutputs = y\n")
     assert "data-dependent address: array element x[...] is a runtime value" in str(e.value)
+
+
+@pytest.mark.parametrize("d", golden_dirs("wl_"), ids=os.path.basename)
+def test_workload_elaboration_identical(d):
+    """Our benchmark kernels (fixture dirs hold the sources) elaborate exactly
+    as the reference elaborated them."""
+    src = lambda f: open(os.path.join(d, f)).read()
+    a, b, inputs = frontend.elaborate_pair(src("a.mk"), src("b.mk"), src("cfg.cfg"))
+    g = json.load(open(os.path.join(d, "golden.json")))
+    assert inputs == [(x["name"], x["size"]) for x in g["inputs"]]
+    _same(a, ir.load(os.path.join(d, "a.veqir")))
+    _same(b, ir.load(os.path.join(d, "b.veqir")))

@@ -80,7 +80,7 @@ def _run_dir(session, d, sides):
         check_run(res, g[f"run_{side}"], f"{os.path.basename(d)}:{side}")
 
 
-@pytest.mark.parametrize("d", golden_dirs("corpus_") + golden_dirs("extra_"), ids=os.path.basename)
+@pytest.mark.parametrize("d", golden_dirs("corpus_") + golden_dirs("extra_") + golden_dirs("wl_"), ids=os.path.basename)
 def test_corpus_run_parity(session, d):
     _run_dir(session, d, ("a", "b"))
 

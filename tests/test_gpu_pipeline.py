@@ -16,7 +16,7 @@ from test_gpu_parity import _race_j, _safety_j
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("d", golden_dirs("corpus_") + golden_dirs("extra_"), ids=os.path.basename)
+@pytest.mark.parametrize("d", golden_dirs("corpus_") + golden_dirs("extra_") + golden_dirs("wl_"), ids=os.path.basename)
 def test_check_report_parity(session, d):
     g = json.load(open(os.path.join(d, "golden.json")))
     rep_ref = g["report"]
