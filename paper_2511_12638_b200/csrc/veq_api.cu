@@ -464,6 +464,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   AL(rel_step, bd->n_rel_cap, uint32_t);
   AL(rel_set, bd->n_rel_cap, uint32_t);
   AL(prog_nrel, P, uint32_t);
+  AL(prog_dead, P, uint32_t);
   AL(prog_steps, P, unsigned long long);
   AL(th_state, Tn, uint8_t);
   AL(th_seg, Tn, uint32_t);
@@ -523,7 +524,15 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
                                                                        (uint32_t *)B.const_node));
   // K0
   PH0(VEQ_PH_SCHEDULE);
-  if (B.n_progs) LAUNCH(k_schedule<<<B.n_progs, SCHED_BLOCK, 0, s>>>(B));
+  if (B.n_progs) {
+    uint32_t maxT = 0;
+    for (const veq_program_meta &m : bd->progs) maxT = std::max(maxT, m.n_threads);
+    size_t smem = maxT <= SCHED_SMEM_T ? SCHED_SMEM_T * 9 : 0;
+    B.sched_on_chip = smem > 0;
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_schedule_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LAUNCH(k_schedule_smem<<<B.n_progs, SCHED_BLOCK, smem, s>>>(B));
+  }
   PH1(VEQ_PH_SCHEDULE);
   CK(cudaGetLastError());
   // K3
@@ -645,10 +654,15 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       EvalCtx E{log, log_stmt, base};
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
-      uint64_t threads = std::min<uint64_t>(n_work, (uint64_t)nsm * 512);
+      // one warp per work item, persistent over the sorted work list
+      // persistent grid: exactly the resident capacity (no second wave)
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_warp, 128, 0);
+      if (per_sm < 1) per_sm = 1;
+      uint64_t threads = std::min<uint64_t>(n_work * 32, (uint64_t)nsm * per_sm * 128);
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
-      LAUNCH(k_eval<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool,
-                                                          ctx->pool_used, ctx->pool_cap, chunk));
+      LAUNCH(k_eval_warp<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool,
+                                                               ctx->pool_used, ctx->pool_cap, chunk));
       CK(cudaGetLastError());
       CK(cudaFreeAsync(tmp2, s));
       CK(cudaFreeAsync(cursor, s));
@@ -678,35 +692,40 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaMemcpyAsync(nrel.data(), B.prog_nrel, P * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(steps.data(), B.prog_steps, P * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&nf, B.n_faults, 8, cudaMemcpyDeviceToHost, s));
-  bd->th_state.resize(B.n_threads);
-  bd->th_bset.resize(B.n_threads);
-  std::vector<uint32_t> th_seg(B.n_threads);
-  CK(cudaMemcpyAsync(bd->th_state.data(), B.th_state, B.n_threads, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(bd->th_bset.data(), B.th_bset, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(th_seg.data(), B.th_seg, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> dead(P);
+  CK(cudaMemcpyAsync(dead.data(), B.prog_dead, P * 4, cudaMemcpyDeviceToHost, s));
+  unsigned long long nn[2] = {0, 0};
+  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   int er = check_error_flag(ctx);
   if (er) return er;
   if (nf > B.fault_cap) return fail(ctx, VEQ_E_BUDGET, "fault buffer overflow");
   bd->faults.resize(nf);
   if (nf) CK(cudaMemcpyAsync(bd->faults.data(), B.faults, nf * sizeof(veq_fault), cudaMemcpyDeviceToHost, s));
-  // blocking statement of blocked threads: end of their current segment
-  std::vector<uint64_t> seg_off_h(B.n_threads + 1), seg_start_h(bd->n_segs);
-  CK(cudaMemcpyAsync(seg_off_h.data(), B.seg_off, (B.n_threads + 1) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(seg_start_h.data(), B.seg_start, bd->n_segs * 8, cudaMemcpyDeviceToHost, s));
-  unsigned long long nn[2] = {0, 0};
-  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  bool any_dead = false;
+  for (uint32_t p = 0; p < P; p++) any_dead |= dead[p] != 0;
+  bd->th_state.assign(B.n_threads, TS_RET);
+  bd->th_bset.assign(B.n_threads, UNSET);
   bd->th_bstmt.assign(B.n_threads, ~0ull);
-  for (uint32_t t = 0; t < B.n_threads; t++)
-    if (bd->th_state[t] == TS_BLOCK) bd->th_bstmt[t] = seg_start_h[seg_off_h[t] + th_seg[t] + 1] - 1;
+  if (any_dead) {
+    // final thread states only matter for deadlock reports (symexec.cpp:335-365)
+    std::vector<uint32_t> th_seg(B.n_threads);
+    CK(cudaMemcpyAsync(bd->th_state.data(), B.th_state, B.n_threads, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(bd->th_bset.data(), B.th_bset, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(th_seg.data(), B.th_seg, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<uint64_t> seg_off_h(B.n_threads + 1), seg_start_h(bd->n_segs);
+    CK(cudaMemcpyAsync(seg_off_h.data(), B.seg_off, (B.n_threads + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(seg_start_h.data(), B.seg_start, bd->n_segs * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t t = 0; t < B.n_threads; t++)
+      if (bd->th_state[t] == TS_BLOCK) bd->th_bstmt[t] = seg_start_h[seg_off_h[t] + th_seg[t] + 1] - 1;
+  }
+  CK(cudaStreamSynchronize(s));
   bd->res.assign(P, veq_prog_result{});
   for (uint32_t p = 0; p < P; p++) {
     bd->res[p].steps = steps[p];
     bd->res[p].releases = nrel[p];
-    const veq_program_meta &m = bd->progs[p];
-    for (uint32_t t = 0; t < m.n_threads; t++)
-      if (bd->th_state[m.thread_off + t] != TS_RET) bd->res[p].deadlocked = 1;
+    bd->res[p].deadlocked = dead[p];
   }
   for (const veq_fault &f : bd->faults) bd->res[f.prog].n_faults++;
   bd->ran = true;

@@ -212,37 +212,59 @@ __device__ __forceinline__ int cmp_pref(const Table &T, uint64_t pa, uint32_t a,
 // ---- interning (K1) ----------------------------------------------------------
 // Lock-free insert-or-find. The node record and kid words are written and
 // fenced before the slot CAS publishes the id; readers go through L2 (ldcg).
+// Merkle hash of a composite: position-salted kid hashes summed, so a warp
+// can compute it with one reduction (kid order still matters).
+__device__ __forceinline__ uint64_t kid_term(uint32_t i, uint64_t kid_hash) {
+  return mix64(kid_hash + (uint64_t)(i + 1) * 0x9e3779b97f4a7c15ULL);
+}
+__device__ __forceinline__ uint64_t composite_hash(uint8_t kind, uint32_t nk, uint64_t sum) {
+  return mix64(hcomb(0x100001b3ULL, kind) ^ ((uint64_t)nk * 0xc2b2ae3d27d4eb4fULL) ^ sum);
+}
+__device__ __forceinline__ uint64_t composite_prefix(uint8_t kind, uint32_t nk, uint64_t kid0_prefix) {
+  return ((uint64_t)kind << 60) | (nk >= 4095 ? (4095ull << 48) : (((uint64_t)nk << 48) | (kid0_prefix >> 16)));
+}
+// positive_definite (proj/src/decide.cpp:306-333) from kid flags
+__device__ __forceinline__ uint8_t composite_flags(uint8_t kind, bool any_pd, bool all_pd, bool any_div) {
+  uint8_t flags = 0;
+  if (any_div || kind == K_DIV) flags |= F_HASDIV;
+  if (kind == K_EXP) flags |= F_POSDEF;
+  else if (kind == K_MAX && any_pd) flags |= F_POSDEF;
+  else if ((kind == K_ADD || kind == K_MUL || kind == K_DIV) && all_pd) flags |= F_POSDEF;
+  return flags;
+}
+
+__device__ inline uint32_t intern_meta(const Table &T, uint8_t kind, uint64_t p0, uint64_t p1, const uint32_t *kids,
+                                       uint32_t nk, uint64_t h, uint8_t flags);
+
 __device__ inline uint32_t intern(const Table &T, uint8_t kind, uint64_t p0, uint64_t p1, const uint32_t *kids,
                                   uint32_t nk) {
   uint64_t h = hcomb(0x100001b3ULL, kind);
   uint8_t flags = 0;
-  uint64_t prefix = 0;
   if (kind == K_CONST) {
     h = hcomb(hcomb(h, p0), p1);
     if ((long long)p0 > 0) flags |= F_POSDEF;
   } else if (kind == K_VAR) {
     h = hcomb(h, p0);
   } else if (kind != K_NEGINF) {
-    bool any_pd = false, all_pd = true, any_div = (kind == K_DIV);
+    bool any_pd = false, all_pd = true, any_div = false;
+    uint64_t sum = 0;
     for (uint32_t i = 0; i < nk; i++) {
       Node kn = ld_node(T, kids[i]);
-      h = hcomb(h, kn.hash);
+      sum += kid_term(i, kn.hash);
       bool pd = kn.flags & F_POSDEF;
       any_pd |= pd;
       all_pd &= pd;
       any_div |= (kn.flags & F_HASDIV) != 0;
-      if (i == 0) {
-        uint64_t kp = prefix_of(kn);
-        prefix = ((uint64_t)kind << 60) | (nk >= 4095 ? (4095ull << 48) : (((uint64_t)nk << 48) | (kp >> 16)));
-      }
+      if (i == 0) p1 = composite_prefix(kind, nk, prefix_of(kn));
     }
-    if (any_div) flags |= F_HASDIV;
-    // positive_definite, proj/src/decide.cpp:306-333
-    if (kind == K_EXP) flags |= F_POSDEF;
-    else if (kind == K_MAX && any_pd) flags |= F_POSDEF;
-    else if ((kind == K_ADD || kind == K_MUL || kind == K_DIV) && all_pd) flags |= F_POSDEF;
-    p1 = prefix;
+    h = composite_hash(kind, nk, sum);
+    flags = composite_flags(kind, any_pd, all_pd, any_div);
   }
+  return intern_meta(T, kind, p0, p1, kids, nk, h, flags);
+}
+
+__device__ inline uint32_t intern_meta(const Table &T, uint8_t kind, uint64_t p0, uint64_t p1, const uint32_t *kids,
+                                       uint32_t nk, uint64_t h, uint8_t flags) {
   uint64_t slot = h & T.slot_mask;
   uint32_t mine = EMPTY;
   for (uint64_t probes = 0;; probes++) {

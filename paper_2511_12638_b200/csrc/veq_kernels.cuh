@@ -15,8 +15,12 @@
 //                     operand-ready spinning (persistent threads).
 //   K5 k_compare      per-VC canonical id compare + side conditions.
 #pragma once
-#include "veq_canon.cuh"
+#include <cooperative_groups.h>
+
+#include "veq_warp.cuh"
 #include "../../include/veq.h"
+
+namespace cg = cooperative_groups;
 
 namespace veqd {
 
@@ -42,10 +46,12 @@ struct Batch {
   const uint64_t *reg_off;    // [T+1]
   const uint32_t *prog_full_set;  // per program: set index of its full set, or UNSET
   uint64_t n_cells;
+  uint32_t sched_on_chip;  // K0 keeps control state in dynamic shared memory
   // run state
   uint32_t *seg_base;
   uint32_t *rel_step, *rel_set;
   uint32_t *prog_nrel;
+  uint32_t *prog_dead;
   unsigned long long *prog_steps;
   uint8_t *th_state;
   uint32_t *th_seg, *th_bset;
@@ -61,8 +67,16 @@ struct Batch {
   uint64_t fault_cap;
 };
 
+// Warp-aggregated slot allocation: one atomic per group of converged lanes.
+__device__ __forceinline__ unsigned long long agg_inc(unsigned long long *ctr) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(ctr, (unsigned long long)g.size());
+  return g.shfl(base, 0) + g.thread_rank();
+}
+
 __device__ __forceinline__ void emit_fault(const Batch &B, const veq_fault &f) {
-  unsigned long long i = atomicAdd(B.n_faults, 1ull);
+  unsigned long long i = agg_inc(B.n_faults);
   if (i < B.fault_cap) B.faults[i] = f;
 }
 
@@ -88,121 +102,144 @@ __device__ inline uint32_t set_min(const Batch &B, uint32_t s) {
   return q.lo;
 }
 
-__global__ void k_schedule(Batch B) {
+// Shared-memory variant of K0 (the one launched): per-thread control state
+// lives in shared memory when the CTA has at most SCHED_SMEM_T threads, so a
+// round costs a handful of block barriers and on-chip accesses.
+constexpr uint32_t SCHED_SMEM_T = 8192;
+
+__global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
+  extern __shared__ uint8_t sched_smem[];
   const uint32_t p = blockIdx.x;
   const veq_program_meta pm = B.progs[p];
   const uint32_t T = pm.n_threads, t0 = pm.thread_off;
+  const bool on_chip = B.sched_on_chip && T <= SCHED_SMEM_T;
+  uint32_t *bs = on_chip ? reinterpret_cast<uint32_t *>(sched_smem) : B.th_bset + t0;
+  uint32_t *sg = on_chip ? bs + SCHED_SMEM_T : B.th_seg + t0;
+  uint8_t *st = on_chip ? reinterpret_cast<uint8_t *>(sg + SCHED_SMEM_T) : B.th_state + t0;
   const uint32_t chunk = (T + SCHED_BLOCK - 1) / SCHED_BLOCK;
   const uint32_t lo = threadIdx.x * chunk, hi = min(T, lo + chunk);
   __shared__ unsigned long long s_scan[SCHED_BLOCK];
-  __shared__ unsigned long long s_step;
-  __shared__ unsigned long long s_best;
+  __shared__ unsigned long long s_step, s_best;
   __shared__ uint32_t s_ret, s_blkfull, s_nrel;
   __shared__ int s_released;
   const uint32_t full = B.prog_full_set[p];
-  // init
   for (uint32_t t = lo; t < hi; t++) {
     uint32_t g = t0 + t;
-    B.th_seg[g] = 0;
-    bool empty = B.thread_stmt[g] == B.thread_stmt[g + 1];
-    B.th_state[g] = empty ? TS_RET : TS_RUN;
-    B.th_bset[g] = UNSET;
+    sg[t] = 0;
+    st[t] = B.thread_stmt[g] == B.thread_stmt[g + 1] ? TS_RET : TS_RUN;
+    bs[t] = UNSET;
   }
   if (threadIdx.x == 0) {
     s_step = 0;
     s_nrel = 0;
+    s_ret = 0;
   }
   __syncthreads();
-  for (;;) {
-    // ---- all returned?
-    if (threadIdx.x == 0) s_ret = 0;
-    __syncthreads();
-    uint32_t my_ret = 0;
-    for (uint32_t t = lo; t < hi; t++) my_ret += B.th_state[t0 + t] == TS_RET;
-    if (my_ret) atomicAdd(&s_ret, my_ret);
-    __syncthreads();
-    if (s_ret == T) break;
-    // ---- run phase: each runnable thread runs its current segment
+  {
+    uint32_t c = 0;
+    for (uint32_t t = lo; t < hi; t++) c += st[t] == TS_RET;
+    if (c) atomicAdd(&s_ret, c);
+  }
+  __syncthreads();
+  while (s_ret != T) {
+    // ---- run phase
     unsigned long long mylen = 0;
     for (uint32_t t = lo; t < hi; t++) {
+      if (st[t] != TS_RUN) continue;
       uint32_t g = t0 + t;
-      if (B.th_state[g] == TS_RUN) {
-        uint64_t sj = B.seg_off[g] + B.th_seg[g];
-        uint64_t end = (sj + 1 < B.seg_off[g + 1]) ? B.seg_start[sj + 1] : B.thread_stmt[g + 1];
-        mylen += end - B.seg_start[sj];
-      }
+      uint64_t sj = B.seg_off[g] + sg[t];
+      uint64_t end = (sj + 1 < B.seg_off[g + 1]) ? B.seg_start[sj + 1] : B.thread_stmt[g + 1];
+      mylen += end - B.seg_start[sj];
     }
-    s_scan[threadIdx.x] = mylen;
-    __syncthreads();
-    for (int off = 1; off < SCHED_BLOCK; off <<= 1) {  // inclusive Hillis-Steele scan
-      unsigned long long v = threadIdx.x >= (unsigned)off ? s_scan[threadIdx.x - off] : 0;
-      __syncthreads();
-      s_scan[threadIdx.x] += v;
-      __syncthreads();
+    // block exclusive scan (warp shuffles + one smem pass)
+    unsigned long long x = mylen;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (unsigned)o) x += y;
     }
-    unsigned long long total = s_scan[SCHED_BLOCK - 1];
-    unsigned long long run = s_step + s_scan[threadIdx.x] - mylen;
-    for (uint32_t t = lo; t < hi; t++) {
-      uint32_t g = t0 + t;
-      if (B.th_state[g] != TS_RUN) continue;
-      uint64_t sj = B.seg_off[g] + B.th_seg[g];
-      bool last = sj + 1 >= B.seg_off[g + 1];
-      uint64_t end = last ? B.thread_stmt[g + 1] : B.seg_start[sj + 1];
-      B.seg_base[sj] = (uint32_t)run;
-      run += end - B.seg_start[sj];
-      if (last) {
-        B.th_state[g] = TS_RET;
-      } else {
-        B.th_state[g] = TS_BLOCK;
-        B.th_bset[g] = B.seg_set[sj];  // canonical id of the Sync ending the segment
-      }
-    }
+    if (lane == 31) s_scan[wid] = x;
     __syncthreads();
     if (threadIdx.x == 0) {
-      s_step += total;
+      unsigned long long acc = 0;
+      for (uint32_t w = 0; w < SCHED_BLOCK / 32; w++) {
+        unsigned long long v = s_scan[w];
+        s_scan[w] = acc;
+        acc += v;
+      }
+      s_scan[SCHED_BLOCK / 32] = acc;
       s_best = ~0ull;
-      s_ret = 0;
       s_blkfull = 0;
       s_released = 0;
     }
     __syncthreads();
-    // ---- release phase: the releasable set with the smallest min tid
+    const unsigned long long total = s_scan[SCHED_BLOCK / 32];
+    unsigned long long run = s_step + s_scan[wid] + x - mylen;
     uint32_t c_ret = 0, c_full = 0;
     for (uint32_t t = lo; t < hi; t++) {
-      uint32_t g = t0 + t;
-      c_ret += B.th_state[g] == TS_RET;
-      c_full += (B.th_state[g] == TS_BLOCK && B.th_bset[g] == full);
+      if (st[t] == TS_RUN) {
+        uint32_t g = t0 + t;
+        uint64_t sj = B.seg_off[g] + sg[t];
+        bool last = sj + 1 >= B.seg_off[g + 1];
+        uint64_t end = last ? B.thread_stmt[g + 1] : B.seg_start[sj + 1];
+        B.seg_base[sj] = (uint32_t)run;
+        run += end - B.seg_start[sj];
+        if (last) {
+          st[t] = TS_RET;
+        } else {
+          st[t] = TS_BLOCK;
+          bs[t] = B.seg_set[sj];
+        }
+      }
+      c_ret += st[t] == TS_RET;
+      c_full += st[t] == TS_BLOCK && bs[t] == full;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_step += total;
+      s_ret = 0;
+    }
+    __syncthreads();
     if (c_ret) atomicAdd(&s_ret, c_ret);
     if (c_full) atomicAdd(&s_blkfull, c_full);
     __syncthreads();
+    // ---- release phase: the releasable set with the smallest min tid; a
+    // set is checked once, by its first blocked member
     unsigned long long best = ~0ull;
     for (uint32_t t = lo; t < hi; t++) {
-      uint32_t g = t0 + t;
-      if (B.th_state[g] != TS_BLOCK) continue;
-      uint32_t I = B.th_bset[g];
+      if (st[t] != TS_BLOCK) continue;
+      const uint32_t I = bs[t];
       bool ok;
       uint32_t mn;
       if (I == full) {
         ok = (s_blkfull + s_ret == T);
         mn = 0;
       } else {
-        veq_syncset q = B.sets[I];
+        const veq_syncset q = B.sets[I];
         ok = true;
         mn = UNSET;
-        for (uint32_t k = 0; k < q.n_bits && ok; k++) {
+        bool skip = false;  // a smaller member blocked on I makes the same check
+        for (uint32_t k = 0; k < q.n_bits; k++) {
           if (!((B.set_words[q.word_off + k / 64] >> (k % 64)) & 1ull)) continue;
-          uint32_t m = q.lo + k;
+          const uint32_t m = q.lo + k;
           if (mn == UNSET) mn = m;
           if (m >= T) {
             ok = false;
             break;
           }
-          uint8_t st = B.th_state[t0 + m];
-          if (st == TS_RET) continue;
-          if (st == TS_BLOCK && B.th_bset[t0 + m] == I) continue;
+          const uint8_t sm = st[m];
+          if (sm == TS_BLOCK && bs[m] == I) {
+            if (m < t) {
+              skip = true;
+              break;
+            }
+            continue;
+          }
+          if (sm == TS_RET) continue;
           ok = false;
+          break;
         }
+        if (skip) continue;
       }
       if (ok) {
         unsigned long long key = ((unsigned long long)mn << 32) | I;
@@ -211,18 +248,21 @@ __global__ void k_schedule(Batch B) {
     }
     if (best != ~0ull) atomicMin(&s_best, best);
     __syncthreads();
-    unsigned long long sb = s_best;
+    const unsigned long long sb = s_best;
     if (sb != ~0ull) {
-      uint32_t I = (uint32_t)(sb & 0xffffffffu);
+      const uint32_t I = (uint32_t)(sb & 0xffffffffu);
+      uint32_t c = 0;
       for (uint32_t t = lo; t < hi; t++) {
+        if (st[t] != TS_BLOCK || bs[t] != I) continue;
         uint32_t g = t0 + t;
-        if (B.th_state[g] != TS_BLOCK || B.th_bset[g] != I) continue;
-        uint32_t ns = B.th_seg[g] + 1;
-        B.th_seg[g] = ns;
-        uint64_t sj = B.seg_off[g] + ns;
-        uint64_t start = B.seg_start[sj];
-        B.th_state[g] = (start == B.thread_stmt[g + 1]) ? TS_RET : TS_RUN;
+        uint32_t ns = sg[t] + 1;
+        sg[t] = ns;
+        uint64_t start = B.seg_start[B.seg_off[g] + ns];
+        bool ret = start == B.thread_stmt[g + 1];
+        st[t] = ret ? TS_RET : TS_RUN;
+        c += ret;
       }
+      if (c) atomicAdd(&s_ret, c);
       if (threadIdx.x == 0) {
         uint64_t r = B.rel_off[p] + s_nrel;
         if (r < B.rel_off[p + 1]) {
@@ -236,11 +276,18 @@ __global__ void k_schedule(Batch B) {
     }
     __syncthreads();
     if (total == 0 && !s_released) break;
-    __syncthreads();
   }
+  // write back the final control state (deadlock reports) and the summary
+  if (on_chip)
+    for (uint32_t t = lo; t < hi; t++) {
+      B.th_state[t0 + t] = st[t];
+      B.th_seg[t0 + t] = sg[t];
+      B.th_bset[t0 + t] = bs[t];
+    }
   if (threadIdx.x == 0) {
     B.prog_nrel[p] = s_nrel;
     B.prog_steps[p] = s_step;
+    B.prog_dead[p] = s_ret != T;
   }
 }
 
@@ -373,7 +420,7 @@ __global__ void k_exec(Batch B, Table T) {
         }
         B.st_step[i] = step;
         uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
-        unsigned long long slot = atomicAdd(B.n_tup, 1ull);
+        unsigned long long slot = agg_inc(B.n_tup);
         B.tup_key[slot] = (cell << 32) | step;
         B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
         break;
@@ -549,7 +596,7 @@ __global__ void k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t
   uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   if (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32)) {
-    unsigned long long i = atomicAdd(n_starts, 1ull);
+    unsigned long long i = agg_inc(n_starts);
     starts[i] = (uint32_t)k;
   }
 }
@@ -650,7 +697,7 @@ __global__ void k_make_work(Batch B, unsigned long long *wkey, uint32_t *wval, u
     else hi = mid;
   }
   uint32_t p = B.thread_prog[lo];
-  unsigned long long slot = atomicAdd(n_work, 1ull);
+  unsigned long long slot = agg_inc(n_work);
   wkey[slot] = ((unsigned long long)p << 32) | B.st_step[i];
   wval[slot] = (uint32_t)i;
 }
@@ -769,21 +816,73 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
   return intern(T, K_EXP, 0, 0, &a, 1);
 }
 
-__global__ void k_eval(Batch B, Table T, EvalCtx E, const uint32_t *work, uint64_t n_work,
-                       unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
-                       uint64_t chunk) {
+// Warp-per-item variant: fused Add chains run warp-cooperatively
+// (veq_warp.cuh); every other operation runs on lane 0.
+// 64 registers/thread: 32 resident warps per SM (the latency-bound work
+// needs the warps; the rare single-thread paths may spill)
+__global__ void __launch_bounds__(128, 8) k_eval_warp(Batch B, Table T, EvalCtx E, const uint32_t *work, uint64_t n_work,
+                            unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
+                            uint64_t chunk) {
   Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, chunk, 0};
+  const uint32_t lane = lane_id();
+  // items are claimed EVAL_GRAB at a time; a warp works through its run in
+  // order, and every dependency of an item lies earlier in the sorted list,
+  // so progress is guaranteed.
+  constexpr uint32_t EVAL_GRAB = 4;
+  unsigned long long w = 0, w_end = 0;
   for (;;) {
-    unsigned long long w = atomicAdd(cursor, 1ull);
+    if (w == w_end) {
+      if (lane == 0) w = atomicAdd(cursor, (unsigned long long)EVAL_GRAB);
+      w = __shfl_sync(kFull, w, 0);
+      w_end = w + EVAL_GRAB;
+    }
     if (w >= n_work) break;
-    uint32_t i = work[w];
-    uint64_t mark = A.used;
-    char *mbase = A.base;
+    const uint32_t i = work[w++];
+    const uint64_t mark = A.used;
+    char *const mbase = A.base;
     A.item = i;
-    uint32_t r = eval_stmt(B, T, A, E, i);
-    if (A.base == mbase) A.used = mark;  // recycle scratch of this item
-    __threadfence();
-    atomicExch(B.canon + i, r);
+    const veq_stmt st = B.stmts[i];
+    uint32_t r = 0;
+    if (st.kind == VEQ_ST_BINOP && st.op == VEQ_BIN_ADD) {
+      const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
+      const uint32_t b = E.log_base[h], n = pos + 2;
+      uint32_t *ids = warp_get<uint32_t>(A, n);
+      if (ids) {
+        bool neg = false;
+        for (uint32_t k = lane; k < n; k += 32) {
+          ids[k] = wait_node(B, E.log[b + k]);
+          neg |= ids[k] == T.id_neginf;
+        }
+        __syncwarp();
+        uint32_t start = 0;
+        if (__any_sync(kFull, neg)) {
+          // -inf operands: same restart rule as eval_stmt, sequentially
+          if (lane == 0) {
+            for (uint32_t k = 0; k < n; k++) {
+              if (ids[k] != T.id_neginf) continue;
+              uint32_t s = E.log_stmt[b + k];
+              arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
+              uint32_t rr = k < 1 ? 1 : k;
+              ids[rr] = intern_undef(T, 3, s >> 29, s);
+              start = rr;
+              if (k == 0) k = 1;
+            }
+          }
+          start = __shfl_sync(kFull, start, 0);
+          __syncwarp();
+        }
+        r = warp_add_small(T, ids + start, n - start);
+        if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
+      }
+    } else {
+      if (lane == 0) r = eval_stmt(B, T, A, E, i);
+      r = __shfl_sync(kFull, r, 0);
+    }
+    if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(B.canon + i, r);
+    }
   }
 }
 

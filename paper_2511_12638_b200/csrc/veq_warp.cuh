@@ -1,0 +1,425 @@
+// veq_warp.cuh — warp-cooperative canonicalisation of sums (K1 + K2 hot path).
+//
+// One warp evaluates one fused Add node: the 32 lanes decompose the leaves'
+// terms in parallel, group like terms with a bitonic sort on factor-vector
+// hashes, rebuild the surviving terms, sort them into canonical order (order
+// prefix, full Expr::compare on ties) and intern the result with a
+// warp-reduced Merkle hash and a lane-parallel kid compare. Semantics are
+// exactly add_nary's (canon_add_kids, proj/src/expr.cpp:415-424); the
+// single-thread routines of veq_canon.cuh remain the fallback.
+#pragma once
+#include "veq_canon.cuh"
+
+namespace veqd {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+template <class X> __device__ __forceinline__ X *warp_get(Arena &A, uint64_t n) {
+  unsigned long long p = 0;
+  if (lane_id() == 0) p = (unsigned long long)A.alloc(n * sizeof(X));
+  p = __shfl_sync(kFull, p, 0);
+  return reinterpret_cast<X *>(p);
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t &total) {
+  uint32_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane_id() >= (unsigned)o) x += y;
+  }
+  total = __shfl_sync(kFull, x, 31);
+  return x - v;
+}
+
+// Bitonic sort of n (key, val) pairs held in scratch; capacity must be the
+// next power of two >= n (padding is filled here). less(ka, va, kb, vb).
+template <class Less>
+__device__ inline void warp_bitonic(uint64_t *key, uint32_t *val, uint32_t n, Less less) {
+  uint32_t P = 1;
+  while (P < n) P <<= 1;
+  for (uint32_t i = n + lane_id(); i < P; i += 32) {
+    key[i] = ~0ull;
+    val[i] = UNSET;
+  }
+  __syncwarp();
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane_id(); i < P; i += 32) {
+        uint32_t l = i ^ j;
+        if (l > i) {
+          uint64_t ki = key[i], kl = key[l];
+          uint32_t vi = val[i], vl = val[l];
+          bool up = (i & k) == 0;
+          bool sw = up ? less(kl, vl, ki, vi) : less(ki, vi, kl, vl);
+          if (sw) {
+            key[i] = kl;
+            key[l] = ki;
+            val[i] = vl;
+            val[l] = vi;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Insert-or-find of a composite whose kids sit in scratch (all lanes call).
+__device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint32_t *kids, uint32_t nk) {
+  const uint32_t lane = lane_id();
+  uint64_t sum = 0, p1 = 0;
+  bool any_pd = false, all_pd = true, any_div = false;
+  for (uint32_t i = lane; i < nk; i += 32) {
+    Node kn = ld_node(T, kids[i]);
+    sum += kid_term(i, kn.hash);
+    bool pd = kn.flags & F_POSDEF;
+    any_pd |= pd;
+    all_pd &= pd;
+    any_div |= (kn.flags & F_HASDIV) != 0;
+    if (i == 0) p1 = composite_prefix(kind, nk, prefix_of(kn));
+  }
+  sum = warp_sum_u64(sum);
+  p1 = __shfl_sync(kFull, p1, 0);
+  any_pd = __any_sync(kFull, any_pd);
+  all_pd = __all_sync(kFull, all_pd);
+  any_div = __any_sync(kFull, any_div);
+  const uint64_t h = composite_hash(kind, nk, sum);
+  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div);
+  uint64_t slot = h & T.slot_mask;
+  uint32_t mine = EMPTY;
+  for (uint64_t probes = 0;; probes++) {
+    if (probes > T.slot_mask) {
+      if (lane == 0) set_error(T, E_BUDGET);
+      return T.id_zero;
+    }
+    uint32_t cur = 0;
+    if (lane == 0) cur = *((volatile uint32_t *)(T.slots + slot));
+    cur = __shfl_sync(kFull, cur, 0);
+    if (cur == EMPTY) {
+      if (mine == EMPTY) {
+        unsigned long long id = 0, off = 0;
+        if (lane == 0) {
+          id = atomicAdd(&T.counters[0], 1ull);
+          off = atomicAdd(&T.counters[1], (unsigned long long)nk);
+        }
+        id = __shfl_sync(kFull, id, 0);
+        off = __shfl_sync(kFull, off, 0);
+        if (id >= T.max_nodes || off + nk > T.max_kids) {
+          if (lane == 0) set_error(T, E_BUDGET);
+          return T.id_zero;
+        }
+        for (uint32_t i = lane; i < nk; i += 32) T.kids[off + i] = kids[i];
+        if (lane == 0) {
+          Node n;
+          n.kind = kind;
+          n.flags = flags;
+          n.pad = 0;
+          n.nkids = nk;
+          n.hash = h;
+          n.p0 = off;
+          n.p1 = p1;
+          T.nodes[id] = n;
+        }
+        __threadfence();
+        __syncwarp();
+        mine = (uint32_t)id;
+      }
+      uint32_t prev = 0;
+      if (lane == 0) prev = atomicCAS(T.slots + slot, EMPTY, mine);
+      prev = __shfl_sync(kFull, prev, 0);
+      if (prev == EMPTY) return mine;
+      cur = prev;
+    }
+    uint64_t ch = 0;
+    if (lane == 0) ch = ld_hash(T, cur);
+    ch = __shfl_sync(kFull, ch, 0);
+    if (ch == h) {
+      Node c = ld_node(T, cur);
+      if (c.kind == kind && c.nkids == nk) {
+        bool same = true;
+        for (uint32_t i = lane; i < nk && same; i += 32) same = (ld_kid(T, c.p0 + i) == kids[i]);
+        if (__all_sync(kFull, same)) return cur;
+      }
+    }
+    slot = (slot + 1) & T.slot_mask;
+  }
+}
+
+__device__ __forceinline__ bool canon_less(const Table &T, uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+  if (ka != kb) return ka < kb;
+  if (va == vb || va == UNSET || vb == UNSET) return false;
+  return cmp_nodes(T, va, vb) < 0;
+}
+
+// Sorts ids (scratch, n entries) into canonical order in place.
+__device__ inline void warp_sort_canonical(const Table &T, Arena &A, uint32_t *ids, uint32_t n) {
+  if (n < 2) return;
+  uint32_t P = 1;
+  while (P < n) P <<= 1;
+  uint64_t *key = warp_get<uint64_t>(A, P);
+  uint32_t *val = warp_get<uint32_t>(A, P);
+  if (!key || !val) return;
+  for (uint32_t i = lane_id(); i < n; i += 32) {
+    key[i] = prefix_id(T, ids[i]);
+    val[i] = ids[i];
+  }
+  warp_bitonic(key, val, n, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return canon_less(T, ka, va, kb, vb);
+  });
+  for (uint32_t i = lane_id(); i < n; i += 32) ids[i] = val[i];
+  __syncwarp();
+}
+
+// ---- register-only fast path: at most 32 terms, no like terms -------------
+// One term per lane; both sorts are shuffle bitonic networks and the result
+// is interned straight from registers (no scratch round trips).
+template <class Less>
+__device__ __forceinline__ void reg_bitonic(uint64_t &key, uint32_t &val, Less less) {
+  const uint32_t lane = lane_id();
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      uint64_t pk = __shfl_xor_sync(kFull, key, j);
+      uint32_t pv = __shfl_xor_sync(kFull, val, j);
+      bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      bool take = (up == lower) ? less(pk, pv, key, val) : less(key, val, pk, pv);
+      if (take) {
+        key = pk;
+        val = pv;
+      }
+    }
+  }
+}
+
+// Interns a composite whose kid i is held by lane i (m <= 32 kids).
+__device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32_t kid, uint32_t m) {
+  const uint32_t lane = lane_id();
+  uint64_t term = 0, p1 = 0;
+  bool pd = true, dv = false;
+  if (lane < m) {
+    Node kn = ld_node(T, kid);
+    term = kid_term(lane, kn.hash);
+    pd = kn.flags & F_POSDEF;
+    dv = (kn.flags & F_HASDIV) != 0;
+    if (lane == 0) p1 = composite_prefix(kind, m, prefix_of(kn));
+  }
+  const uint64_t sum = warp_sum_u64(term);
+  p1 = __shfl_sync(kFull, p1, 0);
+  const bool any_pd = __any_sync(kFull, lane < m && pd), all_pd = __all_sync(kFull, pd);
+  const bool any_div = __any_sync(kFull, dv);
+  const uint64_t h = composite_hash(kind, m, sum);
+  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div);
+  uint64_t slot = h & T.slot_mask;
+  uint32_t mine = EMPTY;
+  for (uint64_t probes = 0;; probes++) {
+    if (probes > T.slot_mask) {
+      if (lane == 0) set_error(T, E_BUDGET);
+      return T.id_zero;
+    }
+    uint32_t cur = 0;
+    if (lane == 0) cur = *((volatile uint32_t *)(T.slots + slot));
+    cur = __shfl_sync(kFull, cur, 0);
+    if (cur == EMPTY) {
+      if (mine == EMPTY) {
+        unsigned long long id = 0, off = 0;
+        if (lane == 0) {
+          id = atomicAdd(&T.counters[0], 1ull);
+          off = atomicAdd(&T.counters[1], (unsigned long long)m);
+        }
+        id = __shfl_sync(kFull, id, 0);
+        off = __shfl_sync(kFull, off, 0);
+        if (id >= T.max_nodes || off + m > T.max_kids) {
+          if (lane == 0) set_error(T, E_BUDGET);
+          return T.id_zero;
+        }
+        if (lane < m) T.kids[off + lane] = kid;
+        if (lane == 0) {
+          Node n;
+          n.kind = kind;
+          n.flags = flags;
+          n.pad = 0;
+          n.nkids = m;
+          n.hash = h;
+          n.p0 = off;
+          n.p1 = p1;
+          T.nodes[id] = n;
+        }
+        __threadfence();
+        __syncwarp();
+        mine = (uint32_t)id;
+      }
+      uint32_t prev = 0;
+      if (lane == 0) prev = atomicCAS(T.slots + slot, EMPTY, mine);
+      prev = __shfl_sync(kFull, prev, 0);
+      if (prev == EMPTY) return mine;
+      cur = prev;
+    }
+    Node c = ld_node(T, cur);
+    bool same = c.hash == h && c.kind == kind && c.nkids == m;
+    if (__all_sync(kFull, same)) {
+      bool eq = lane >= m || ld_kid(T, c.p0 + lane) == kid;
+      if (__all_sync(kFull, eq)) return cur;
+    }
+    slot = (slot + 1) & T.slot_mask;
+  }
+}
+
+// Returns the canonical sum, or UNSET when the fast path does not apply
+// (more than 32 terms, or like terms that must be merged).
+__device__ inline uint32_t warp_add_small(const Table &T, const uint32_t *leaves, uint32_t n) {
+  const uint32_t lane = lane_id();
+  if (n > 32) return UNSET;
+  uint32_t leaf = UNSET, c = 0, kind = 0;
+  uint64_t p0 = 0;
+  if (lane < n) {
+    leaf = leaves[lane];
+    Node ln = ld_node(T, leaf);
+    kind = ln.kind;
+    p0 = ln.p0;
+    c = ln.kind == K_ADD ? ln.nkids : 1;
+  }
+  uint32_t m;
+  const uint32_t ex = warp_excl_scan(c, m);
+  if (m > 32) return UNSET;
+  // the leaf holding term `lane`
+  uint32_t src_leaf = 0;
+  for (uint32_t l = 0; l < n; l++) {
+    uint32_t el = __shfl_sync(kFull, ex, l), cl = __shfl_sync(kFull, c, l);
+    if (cl && el <= lane) src_leaf = l;
+  }
+  const uint32_t lk = __shfl_sync(kFull, kind, src_leaf);
+  const uint64_t lp = __shfl_sync(kFull, p0, src_leaf);
+  const uint32_t lid = __shfl_sync(kFull, leaf, src_leaf);
+  const uint32_t lex = __shfl_sync(kFull, ex, src_leaf);
+  uint32_t term_node = UNSET;
+  uint64_t key = ~0ull;
+  bool real = false;  // a literal 0 term has coefficient 0 and is dropped
+  if (lane < m) {
+    term_node = lk == K_ADD ? ld_kid(T, lp + (lane - lex)) : lid;
+    real = term_node != T.id_zero;
+    if (real) key = decompose_one(T, term_node).fh;
+  }
+  const uint32_t m_all = m;
+  m = __popc(__ballot_sync(kFull, real));
+  (void)m_all;
+  uint32_t val = lane;
+  reg_bitonic(key, val, [](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return ka != kb ? ka < kb : va < vb;
+  });
+  const uint64_t prev = __shfl_up_sync(kFull, key, 1);
+  if (__any_sync(kFull, lane > 0 && lane < m && key == prev)) return UNSET;  // like terms
+  if (m == 0) return T.id_zero;
+  if (m == 1) return __shfl_sync(kFull, term_node, __shfl_sync(kFull, val, 0) & 31);
+  // no merges: the result's kids are the term nodes themselves
+  uint32_t id = __shfl_sync(kFull, term_node, val & 31);
+  uint64_t pk = lane < m ? prefix_id(T, id) : ~0ull;
+  if (lane >= m) id = UNSET;
+  reg_bitonic(pk, id, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) { return canon_less(T, ka, va, kb, vb); });
+  return warp_intern_regs(T, K_ADD, id, m);
+}
+
+// canon_add_kids over n canonical leaves (scratch), warp-cooperative.
+__device__ inline uint32_t warp_add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
+  const uint32_t lane = lane_id();
+  // 1. term offsets per leaf
+  uint32_t *off = warp_get<uint32_t>(A, n + 1);
+  if (!off) return T.id_zero;
+  uint32_t run = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    uint32_t i = base + lane;
+    uint32_t c = i < n ? n_terms_of(T, leaves[i]) : 0;
+    uint32_t tot;
+    uint32_t ex = warp_excl_scan(c, tot);
+    if (i < n) off[i] = run + ex;
+    run += tot;
+  }
+  if (lane == 0) off[n] = run;
+  __syncwarp();
+  const uint32_t m = run;
+  if (m == 0) return T.id_zero;
+  // 2. decompose terms in parallel
+  Term *ts = warp_get<Term>(A, m);
+  uint32_t P = 1;
+  while (P < m) P <<= 1;
+  uint64_t *key = warp_get<uint64_t>(A, P);
+  uint32_t *val = warp_get<uint32_t>(A, P);
+  if (!ts || !key || !val) return T.id_zero;
+  for (uint32_t t = lane; t < m; t += 32) {
+    uint32_t lo = 0, hi = n;  // leaf of term t: last leaf with off <= t
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) / 2;
+      if (off[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    uint32_t leaf = leaves[lo];
+    Node ln = ld_node(T, leaf);
+    uint32_t id = ln.kind == K_ADD ? ld_kid(T, ln.p0 + (t - off[lo])) : leaf;
+    ts[t] = decompose_one(T, id);
+    key[t] = ts[t].fh;
+    val[t] = t;
+  }
+  __syncwarp();
+  // 3. group like terms: sort by factor-vector hash (index breaks ties)
+  warp_bitonic(key, val, m, [](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return ka != kb ? ka < kb : va < vb;
+  });
+  // 4. run heads combine their run (exact factor compare inside a hash run)
+  uint32_t *out = warp_get<uint32_t>(A, m);
+  uint32_t *cnt = warp_get<uint32_t>(A, m);
+  if (!out || !cnt) return T.id_zero;
+  uint32_t nout = 0;
+  for (uint32_t base = 0; base < m; base += 32) {
+    uint32_t p = base + lane;
+    uint32_t made = 0;
+    uint32_t local[4];
+    bool overflow = false;
+    if (p < m && (p == 0 || key[p] != key[p - 1])) {
+      uint32_t q = p + 1;
+      while (q < m && key[q] == key[p]) q++;
+      for (uint32_t a = p; a < q; a++) {
+        const Term &ta = ts[val[a]];
+        bool dup = false;  // already merged into an earlier member of this run
+        for (uint32_t b = p; b < a && !dup; b++) dup = term_key_cmp(ts[val[b]], ta) == 0;
+        if (dup) continue;
+        Rat c = ta.c;
+        uint32_t nmerge = 1;
+        for (uint32_t b = a + 1; b < q; b++)
+          if (term_key_cmp(ts[val[b]], ta) == 0) {
+            c = rat_add(T, c, ts[val[b]].c);
+            nmerge++;
+          }
+        if (rat_is(c, 0)) continue;
+        uint32_t r;
+        if (nmerge == 1 && ta.src != UNSET) r = ta.src;
+        else r = finish_term(T, A, c, ta);
+        if (made < 4) local[made] = r;
+        else overflow = true;
+        made++;
+      }
+    }
+    uint32_t tot;
+    uint32_t ex = warp_excl_scan(made, tot);
+    if (__any_sync(kFull, overflow)) {
+      // a hash run with more than four distinct factor vectors: degenerate
+      // collision pattern, handled by the single-thread path
+      uint32_t r = 0;
+      if (lane == 0) r = add_nary(T, A, leaves, n);
+      return __shfl_sync(kFull, r, 0);
+    }
+    for (uint32_t k = 0; k < made; k++) out[nout + ex + k] = local[k];
+    nout += tot;
+  }
+  __syncwarp();
+  if (nout == 0) return T.id_zero;
+  if (nout == 1) return out[0];
+  // 5. canonical order, 6. intern
+  warp_sort_canonical(T, A, out, nout);
+  return warp_intern(T, K_ADD, out, nout);
+}
+
+}  // namespace veqd
