@@ -173,6 +173,15 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(VEQ_E_CUDA, "cudaSetDevice");
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(VEQ_E_CUDA, "stream");
+  {
+    // keep freed stream-ordered allocations in the pool across syncs: the
+    // per-run work buffers are re-allocated every run
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   uint64_t slots = 1;
   while (slots < ctx->lim.max_nodes * 2) slots <<= 1;
   ctx->n_slots = slots;
@@ -316,6 +325,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   const uint32_t P = d->n_progs, Tn = d->n_threads_total;
   const uint64_t S = d->n_stmts;
   if (S >= (1ull << 31)) return fail(ctx, VEQ_E_UNSUPPORTED, "batch has more than 2^31 statements");
+  if (P >= (1u << 20)) return fail(ctx, VEQ_E_UNSUPPORTED, "batch has more than 2^20 programs");
   BatchDev *bd = new BatchDev();
   bd->progs.assign(d->progs, d->progs + P);
   bd->arrays.assign(d->arrays, d->arrays + d->n_arrays_total);
@@ -527,8 +537,10 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   if (B.n_progs) {
     uint32_t maxT = 0;
     for (const veq_program_meta &m : bd->progs) maxT = std::max(maxT, m.n_threads);
-    size_t smem = maxT <= SCHED_SMEM_T ? SCHED_SMEM_T * 9 : 0;
-    B.sched_on_chip = smem > 0;
+    // on-chip control state sized to the largest CTA of the batch, so small
+    // CTAs keep many scheduler blocks resident per SM
+    size_t smem = maxT <= SCHED_SMEM_T ? ((size_t)maxT * 9 + 15) / 16 * 16 : 0;
+    B.sched_on_chip = smem > 0 ? maxT : 0;
     if (smem > 48 * 1024)
       CK(cudaFuncSetAttribute(k_schedule_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     LAUNCH(k_schedule_smem<<<B.n_progs, SCHED_BLOCK, smem, s>>>(B));
@@ -537,7 +549,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaGetLastError());
   // K3
   PH0(VEQ_PH_EXEC);
-  if (B.n_threads) LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
+  // one warp per symbolic thread
+  if (B.n_threads) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_threads * 32, 128), 128, 0, s>>>(B, ctx->T));
   PH1(VEQ_PH_EXEC);
   CK(cudaGetLastError());
   unsigned long long n_tup = 0;
@@ -634,16 +647,23 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaStreamSynchronize(s));
     void *tmp2 = nullptr;
     if (n_work) {
-      int pb = 1;
-      while ((1ull << pb) < B.n_progs + 1) pb++;
+      // key = step << 20 | program; sort only the bits in use (steps of a
+      // program are bounded by its statements plus releases)
+      uint64_t max_step = 0;
+      for (uint32_t p = 0; p < B.n_progs; p++) {
+        const veq_program_meta &m = bd->progs[p];
+        uint64_t st = bd->thread_stmt[m.thread_off + m.n_threads] - bd->thread_stmt[m.thread_off];
+        max_step = std::max<uint64_t>(max_step, st);
+      }
+      max_step += bd->n_rel_cap;
       int sb = 1;
-      while ((1ull << sb) < S + 1 && sb < 32) sb++;
-      // key = prog << 32 | step; sort only the bits in use
+      while ((1ull << sb) < max_step + 1 && sb < 44) sb++;
+      const int end_bit = 20 + sb;
       size_t tb2 = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, 32 + pb, s);
+      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, end_bit, s);
       CK(cudaMallocAsync(&tmp2, tb2, s));
-      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, 32 + pb, s);
-      ctx->launches += (32 + pb + 7) / 8 + 1;
+      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, end_bit, s);
+      ctx->launches += (end_bit + 7) / 8 + 1;
     }
     PH1(VEQ_PH_WORKLIST);
     PH0(VEQ_PH_EVAL);

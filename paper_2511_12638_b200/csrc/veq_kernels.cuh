@@ -46,7 +46,7 @@ struct Batch {
   const uint64_t *reg_off;    // [T+1]
   const uint32_t *prog_full_set;  // per program: set index of its full set, or UNSET
   uint64_t n_cells;
-  uint32_t sched_on_chip;  // K0 keeps control state in dynamic shared memory
+  uint32_t sched_on_chip;  // K0: capacity (threads) of its on-chip control state, 0 = global
   // run state
   uint32_t *seg_base;
   uint32_t *rel_step, *rel_set;
@@ -112,10 +112,11 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
   const uint32_t p = blockIdx.x;
   const veq_program_meta pm = B.progs[p];
   const uint32_t T = pm.n_threads, t0 = pm.thread_off;
-  const bool on_chip = B.sched_on_chip && T <= SCHED_SMEM_T;
+  const uint32_t cap = B.sched_on_chip;  // threads of on-chip state per block
+  const bool on_chip = T <= cap;
   uint32_t *bs = on_chip ? reinterpret_cast<uint32_t *>(sched_smem) : B.th_bset + t0;
-  uint32_t *sg = on_chip ? bs + SCHED_SMEM_T : B.th_seg + t0;
-  uint8_t *st = on_chip ? reinterpret_cast<uint8_t *>(sg + SCHED_SMEM_T) : B.th_state + t0;
+  uint32_t *sg = on_chip ? bs + cap : B.th_seg + t0;
+  uint8_t *st = on_chip ? reinterpret_cast<uint8_t *>(sg + cap) : B.th_state + t0;
   const uint32_t chunk = (T + SCHED_BLOCK - 1) / SCHED_BLOCK;
   const uint32_t lo = threadIdx.x * chunk, hi = min(T, lo + chunk);
   __shared__ unsigned long long s_scan[SCHED_BLOCK];
@@ -434,6 +435,258 @@ __global__ void k_exec(Batch B, Table T) {
 }
 
 // ---------------------------------------------------------------------------
+// K3, warp-parallel: one warp per symbolic thread, 32 consecutive statements
+// per step. Each lane owns one statement; a register read resolves to the
+// last lane before it (in statement order) that defines the register — found
+// with shuffles — else to the register file. Copies forward their source
+// value; the first read of an uninitialised register faults and seeds it
+// (symexec.cpp:390-408). Chain links are decided warp-uniformly in lane
+// order. Semantics are identical to k_exec.
+__device__ __forceinline__ bool defines_reg(uint8_t kind) {
+  return kind == VEQ_ST_SETCONST || kind == VEQ_ST_BINOP || kind == VEQ_ST_UNOP || kind == VEQ_ST_COPY ||
+         kind == VEQ_ST_LOAD;
+}
+
+__global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (g >= B.n_threads) return;
+  const uint32_t p = B.thread_prog[g];
+  const veq_program_meta pm = B.progs[p];
+  const uint32_t tid = g - pm.thread_off;
+  uint32_t *regs = B.regfile + B.reg_off[g];
+  const uint64_t s0 = B.thread_stmt[g], s1 = B.thread_stmt[g + 1];
+  const uint64_t j0 = B.seg_off[g], j1 = B.seg_off[g + 1];
+  for (uint64_t j = j0; j < j1; j++) {
+    const uint32_t base = B.seg_base[j];
+    if (base == UNSET) break;  // segment never ran (deadlock)
+    const uint64_t start = B.seg_start[j], end = (j + 1 < j1) ? B.seg_start[j + 1] : s1;
+    for (uint64_t bt = start; bt < end; bt += 32) {
+      const uint64_t i = bt + lane;
+      const bool act = i < end;
+      veq_stmt st;
+      if (act) st = B.stmts[i];
+      else {
+        st.kind = VEQ_ST_SYNC;
+        st.op = 0;
+        st.arr = 0;
+        st.dst = st.a = st.b = 0;
+      }
+      const uint32_t step = base + (uint32_t)(i - start);
+      // ---- memory statements: bounds and direct input loads
+      uint32_t ga = 0;
+      veq_array arr{};
+      int32_t off = 0;
+      bool oob = false, direct = false, mem = act && (st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE);
+      if (mem) {
+        ga = pm.array_off + st.arr;
+        arr = B.arrays[ga];
+        off = (int32_t)st.a;
+        oob = off < 0 || (uint64_t)off >= arr.size;
+        direct = !oob && st.kind == VEQ_ST_LOAD && !(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 &&
+                 (uint32_t)off < arr.seeded;
+      }
+      const uint32_t def = (act && defines_reg(st.kind)) ? st.dst : UNSET;
+      // operand registers (UNSET: none). An out-of-bounds store reads nothing.
+      uint32_t ra = UNSET, rb = UNSET;
+      if (act) {
+        if (st.kind == VEQ_ST_COPY || st.kind == VEQ_ST_UNOP || st.kind == VEQ_ST_BINOP) ra = st.a;
+        if (st.kind == VEQ_ST_BINOP) rb = st.b;
+        if (st.kind == VEQ_ST_STORE && !oob) ra = st.dst;
+      }
+      // ---- last defining lane before me for each operand
+      int la = -1, lb = -1;
+      for (uint32_t k = 0; k < 32; k++) {
+        uint32_t dk = __shfl_sync(kFull, def, k);
+        if (k < lane) {
+          if (dk == ra && ra != UNSET) la = (int)k;
+          if (dk == rb && rb != UNSET) lb = (int)k;
+        }
+      }
+      // ---- register-file reads (operands with no earlier def in this batch)
+      uint32_t fa = UNSET, fb = UNSET;
+      if (ra != UNSET && la < 0) fa = regs[ra];
+      if (rb != UNSET && lb < 0) fb = regs[rb];
+      // uninitialised reads: the first read of a register in this batch faults
+      const uint32_t ua = (ra != UNSET && la < 0 && fa == UNSET) ? ra : UNSET;
+      const uint32_t ub = (rb != UNSET && lb < 0 && fb == UNSET) ? rb : UNSET;
+      bool first_a = ua != UNSET, first_b = ub != UNSET && ub != ua;
+      for (uint32_t k = 0; k < 32; k++) {
+        uint32_t uak = __shfl_sync(kFull, ua, k), ubk = __shfl_sync(kFull, ub, k);
+        if (k < lane) {
+          if (ua != UNSET && (uak == ua || ubk == ua)) first_a = false;
+          if (ub != UNSET && (uak == ub || ubk == ub)) first_b = false;
+        }
+      }
+      if (ua != UNSET) fa = REF_NODE | intern_undef(T, 0, g, ua);
+      if (ub != UNSET) fb = REF_NODE | intern_undef(T, 0, g, ub);
+      if (first_a || first_b) {
+        veq_fault f{};
+        f.type = VEQ_FAULT_SAFETY;
+        f.kind = VEQ_SAFE_UNINIT_REG;
+        f.prog = p;
+        f.tid = tid;
+        f.stmt = (uint32_t)i;
+        f.step = step;
+        if (first_a) {
+          f.sub = 0;
+          f.reg_slot = 0;
+          emit_fault(B, f);
+        }
+        if (first_b) {
+          f.sub = 1;
+          f.reg_slot = 1;
+          emit_fault(B, f);
+        }
+      }
+      // ---- own value of each defining lane (copies resolved below)
+      uint32_t val = UNSET;
+      if (def != UNSET) {
+        switch (st.kind) {
+        case VEQ_ST_SETCONST: val = REF_NODE | (st.op == 1 ? T.id_neginf : B.const_node[st.a]); break;
+        case VEQ_ST_BINOP:
+        case VEQ_ST_UNOP: val = (uint32_t)i; break;
+        case VEQ_ST_LOAD:
+          if (oob) val = REF_NODE | intern_undef(T, 1, ga, (uint64_t)(uint32_t)off);
+          else if (direct) val = REF_NODE | intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
+          else val = (uint32_t)i;
+          break;
+        default: break;  // copy
+        }
+      }
+      // ---- operand values; copies take their source's value (iterate until
+      // every copy in the batch is resolved — chains are at most 31 long)
+      uint32_t va = fa, vb = fb;
+      bool pending_copy = st.kind == VEQ_ST_COPY && act;
+      if (st.kind == VEQ_ST_COPY && act && la < 0) {
+        val = va;
+        pending_copy = false;
+      }
+      while (__any_sync(kFull, pending_copy)) {
+        uint32_t src = __shfl_sync(kFull, val, la < 0 ? lane : (uint32_t)la);
+        bool src_ready = __shfl_sync(kFull, !pending_copy, la < 0 ? lane : (uint32_t)la);
+        if (pending_copy && src_ready) {
+          val = src;
+          pending_copy = false;
+        }
+      }
+      {
+        uint32_t x = __shfl_sync(kFull, val, la < 0 ? lane : (uint32_t)la);
+        uint32_t y = __shfl_sync(kFull, val, lb < 0 ? lane : (uint32_t)lb);
+        if (la >= 0) va = x;
+        if (lb >= 0) vb = y;
+      }
+      if (st.kind == VEQ_ST_COPY && act) val = va;
+      // ---- per-statement effects
+      if (act) {
+        if (mem && oob) {
+          veq_fault f{};
+          f.type = VEQ_FAULT_SAFETY;
+          f.kind = VEQ_SAFE_OOB;
+          f.sub = 2;
+          f.is_write = st.kind == VEQ_ST_STORE;
+          f.prog = p;
+          f.tid = tid;
+          f.stmt = (uint32_t)i;
+          f.step = step;
+          f.arr = st.arr;
+          f.offset = off;
+          emit_fault(B, f);
+        } else if (mem && !direct) {
+          if (st.kind == VEQ_ST_STORE) B.ref_a[i] = va;
+          B.st_step[i] = step;
+          uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
+          unsigned long long slot = agg_inc(B.n_tup);
+          B.tup_key[slot] = (cell << 32) | step;
+          B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
+        } else if (st.kind == VEQ_ST_BINOP || st.kind == VEQ_ST_UNOP) {
+          B.st_step[i] = step;
+          B.ref_a[i] = va;
+          if (st.kind == VEQ_ST_BINOP) B.ref_b[i] = vb;
+        }
+      }
+      // ---- chain links, decided warp-uniformly in statement order
+      const bool chain = act && st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX);
+      uint32_t my_head = 0, my_pos = 0;
+      uint32_t cont_mask = 0;  // in-batch chain ops already continued
+      uint32_t chain_lanes = __ballot_sync(kFull, chain);
+      while (chain_lanes) {
+        const uint32_t k = __ffs(chain_lanes) - 1;
+        chain_lanes &= chain_lanes - 1;
+        const uint32_t vak = __shfl_sync(kFull, va, k), vbk = __shfl_sync(kFull, vb, k);
+        const uint32_t opk = __shfl_sync(kFull, (uint32_t)st.op, k);
+        const uint64_t ik = bt + k;
+        // tail test for a candidate ref v (uniform across the warp)
+        auto tail = [&](uint32_t v) -> bool {
+          if (!is_stmt_ref(v) || v < s0 || v >= ik) return false;
+          if (v >= bt) {
+            uint32_t lv = (uint32_t)(v - bt);
+            bool ch = (__ballot_sync(kFull, chain && st.op == opk) >> lv) & 1u;
+            return ch && !((cont_mask >> lv) & 1u);
+          }
+          veq_stmt sv = B.stmts[v];
+          return sv.kind == VEQ_ST_BINOP && sv.op == opk && !*((volatile uint8_t *)(B.continued + v));
+        };
+        uint32_t pred = UNSET, leaf = 0;
+        bool ta = tail(vak);
+        bool tb = !ta && tail(vbk);
+        if (ta) {
+          pred = vak;
+          leaf = vbk;
+        } else if (tb) {
+          pred = vbk;
+          leaf = vak;
+        }
+        uint32_t head, pos;
+        if (pred != UNSET) {
+          uint32_t hp, pp;
+          if (pred >= bt) {
+            hp = __shfl_sync(kFull, my_head, (uint32_t)(pred - bt));
+            pp = __shfl_sync(kFull, my_pos, (uint32_t)(pred - bt));
+            cont_mask |= 1u << (uint32_t)(pred - bt);
+          } else {
+            hp = B.chain_head[pred];
+            pp = B.chain_pos[pred];
+          }
+          head = hp;
+          pos = pp + 1;
+          if (lane == 0) {
+            if (pred < bt) B.continued[pred] = 1;
+            B.chain_len[head] = pos + 1;
+          }
+        } else {
+          head = (uint32_t)ik;
+          pos = 0;
+          if (lane == 0) B.chain_len[head] = 1;
+        }
+        if (lane == k) {
+          my_head = head;
+          my_pos = pos;
+          B.chain_head[i] = head;
+          B.chain_pos[i] = pos;
+          if (pred != UNSET) {
+            B.ref_a[i] = pred;
+            B.ref_b[i] = leaf;
+          }
+        }
+      }
+      if ((cont_mask >> lane) & 1u) B.continued[i] = 1;
+      // ---- register file: seeds first, then the last def of each register
+      if (first_a) regs[ua] = fa;
+      if (first_b) regs[ub] = fb;
+      __syncwarp();
+      bool last_def = def != UNSET;
+      for (uint32_t k = 0; k < 32; k++) {
+        uint32_t dk = __shfl_sync(kFull, def, k);
+        if (k > lane && dk == def) last_def = false;
+      }
+      if (last_def) regs[def] = val;
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K4 helpers: "thread i is still pending in the event (owner j, step se) at
 // step s" — no release (I, r) with se < r < s and {i, j} in I (sync_mem,
 // symexec.cpp:48-69, folded over the release sequence).
@@ -698,7 +951,9 @@ __global__ void k_make_work(Batch B, unsigned long long *wkey, uint32_t *wval, u
   }
   uint32_t p = B.thread_prog[lo];
   unsigned long long slot = agg_inc(n_work);
-  wkey[slot] = ((unsigned long long)p << 32) | B.st_step[i];
+  // (step, program): every dependency of an item has a smaller step in the
+  // same program, hence a smaller key, and all CTAs advance together
+  wkey[slot] = ((unsigned long long)B.st_step[i] << 20) | p;
   wval[slot] = (uint32_t)i;
 }
 
