@@ -453,6 +453,13 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   UP(rel_off, rel_off.data(), P + 1, uint64_t);
   UP(reg_off, reg_off.data(), Tn + 1, uint64_t);
   UP(prog_full_set, prog_full.data(), P, uint32_t);
+  {
+    std::vector<uint32_t> longs;
+    for (uint32_t t = 0; t < Tn; t++)
+      if (d->thread_stmt[t + 1] - d->thread_stmt[t] >= EXEC_WARP_MIN) longs.push_back(t);
+    B.n_long = (uint32_t)longs.size();
+    UP(long_threads, longs.data(), longs.size(), uint32_t);
+  }
 #undef UP
   uint32_t *cn = nullptr;
   veq_rat *dconsts = nullptr;
@@ -549,8 +556,9 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaGetLastError());
   // K3
   PH0(VEQ_PH_EXEC);
-  // one warp per symbolic thread
-  if (B.n_threads) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_threads * 32, 128), 128, 0, s>>>(B, ctx->T));
+  // short threads: one CUDA thread each; long threads: one warp each
+  if (B.n_threads) LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
+  if (B.n_long) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_long * 32, 128), 128, 0, s>>>(B, ctx->T));
   PH1(VEQ_PH_EXEC);
   CK(cudaGetLastError());
   unsigned long long n_tup = 0;

@@ -47,6 +47,8 @@ struct Batch {
   const uint32_t *prog_full_set;  // per program: set index of its full set, or UNSET
   uint64_t n_cells;
   uint32_t sched_on_chip;  // K0: capacity (threads) of its on-chip control state, 0 = global
+  const uint32_t *long_threads;  // threads with >= EXEC_WARP_MIN statements (warp executor)
+  uint32_t n_long;
   // run state
   uint32_t *seg_base;
   uint32_t *rel_step, *rel_set;
@@ -296,9 +298,13 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
 // K3: per-thread symbolic execution over value refs.
 __device__ __forceinline__ bool is_stmt_ref(uint32_t r) { return r < REF_NODE; }
 
+// Threads with at least EXEC_WARP_MIN statements run on k_exec_warp.
+constexpr uint64_t EXEC_WARP_MIN = 64;
+
 __global__ void k_exec(Batch B, Table T) {
   uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= B.n_threads) return;
+  if (B.thread_stmt[g + 1] - B.thread_stmt[g] >= EXEC_WARP_MIN) return;
   const uint32_t p = B.thread_prog[g];
   const veq_program_meta pm = B.progs[p];
   const uint32_t tid = g - pm.thread_off;
@@ -449,8 +455,9 @@ __device__ __forceinline__ bool defines_reg(uint8_t kind) {
 
 __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (g >= B.n_threads) return;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= B.n_long) return;
+  const uint32_t g = B.long_threads[w];
   const uint32_t p = B.thread_prog[g];
   const veq_program_meta pm = B.progs[p];
   const uint32_t tid = g - pm.thread_off;
