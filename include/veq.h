@@ -1,12 +1,12 @@
 /* veq.h — C-ABI boundary of the B200-native equivalence-checker core.
  *
  * Replaces the hot section of the reference pipeline,
- *   ctaeq::check_equivalence  /root/reference/proj/src/pipeline.cpp:273-336
+ *   ctaeq::check_equivalence  /root/reference/proj/src/pipeline.cpp:180-243
  * i.e. the two round-robin runs and the per-VC decision loop:
  *   ctaeq::run(const Program&, const SharedMem&, const SchedulePolicy&)
- *        proj/include/ctaeq/symexec.hpp:235-236, called at pipeline.cpp:276,292
+ *        proj/include/ctaeq/symexec.hpp:235-236, called at pipeline.cpp:183,199
  *   ctaeq::eq(const Expr&, const Expr&, ...) — fast path only (cf == cg plus
- *        side conditions), proj/src/decide.cpp:749-771, called at pipeline.cpp:320
+ *        side conditions), proj/src/decide.cpp:749-771, called at pipeline.cpp:227
  * Everything above (parse, elaborate, validate, signature check) and below
  * (aggregation, JSON, CLI) stays in host code. Plain C types only.
  *
@@ -118,7 +118,7 @@ typedef struct veq_batch_desc {
 
 /* ---- session inputs ----------------------------------------------------
  * The symbolic inputs of a check (ctaeq::make_symbolic_inputs,
- * pipeline.cpp:200-212): array `name` cell i holds Var("<name>_<i>").
+ * pipeline.cpp:107-119): array `name` cell i holds Var("<name>_<i>").
  * Declaring them fixes the byte order of every input symbol (the order
  * Expr::compare uses for Vars, expr.cpp:120) and starts a new term table. */
 typedef struct veq_input_desc {
@@ -262,7 +262,7 @@ typedef struct veq_vc_out {
 
 /* out_arrays: for program pair i, n_out_arrays[i] entries of
  * (array index in A's program, array index in B's program), already in
- * ascending array-name order (pipeline.cpp:120-130). */
+ * ascending array-name order (pipeline.cpp:128-131). */
 int veq_compare(veq_ctx *ctx, uint32_t batch_a, uint32_t batch_b,
                 const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
                 uint32_t n_out_per_pair, veq_vc_out *out);

@@ -2,7 +2,7 @@
  *
  * Replaces the reference's kernel-IR loader
  *   ctaeq::parse_kernel / parse_config / elaborate
- *   (proj/include/ctaeq/frontend.hpp:104-129, called at pipeline.cpp:243-262)
+ *   (proj/include/ctaeq/frontend.hpp:104-129, called at pipeline.cpp:150-169)
  * and make_symbolic_inputs (pipeline.hpp:73-74): it turns kernel sources and
  * a launch configuration into packed IR batches (VEQIR02 byte images, see
  * include/veq_ir.hpp) ready for veq_load_batch. Elaboration is per CTA;

@@ -13,7 +13,7 @@
 //                                   CPU baseline: times the reference's own
 //                                   run(A) + run(B) + eq() per CTA pair (the
 //                                   t_exec_a + t_exec_b + t_decide span of
-//                                   pipeline.cpp:275-336) over the configs
+//                                   pipeline.cpp:182-243) over the configs
 //                                   listed in CFGLIST, on THREADS host threads,
 //                                   until SECONDS elapse; prints JSON.
 // Nothing in the product links or calls this.
@@ -375,7 +375,7 @@ int cmd_bench(const std::string &pa_path, const std::string &pb_path, const std:
     uint64_t n_out = 0;
   };
   // Parse, elaboration and make_symbolic_inputs are the reference's t_parse
-  // and setup (pipeline.cpp:240-273) and are excluded from the metric; they
+  // and setup (pipeline.cpp:147-180) and are excluded from the metric; they
   // run per job inside the worker, outside the timed span, so memory stays
   // bounded by the thread count.
   std::atomic<size_t> cursor{0};

@@ -56,7 +56,7 @@ struct ParsedKernel {
   const std::string &name() const;
 };
 
-// Input symbols of a pair (make_symbolic_inputs, pipeline.cpp:200-212):
+// Input symbols of a pair (make_symbolic_inputs, pipeline.cpp:107-119):
 // for each config input that names one of kernel A's arrays, that array's
 // name and A's size.
 struct InputDecl {

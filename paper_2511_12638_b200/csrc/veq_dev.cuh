@@ -333,7 +333,7 @@ __device__ __forceinline__ Rat const_val(const Node &n) { return Rat{(long long)
 
 // Dense byte-order rank of the decimal string of i among the decimal strings
 // of 0..n-1 ("x_10" < "x_2", the order std::string::compare gives the
-// reference's Var names, expr.cpp:120 and pipeline.cpp:209).
+// reference's Var names, expr.cpp:120 and pipeline.cpp:116).
 __device__ inline uint64_t lexrank(uint64_t i, uint64_t n) {
   char s[24];
   int L = 0;

@@ -1,12 +1,12 @@
-"""check_equivalence over the C-ABI (mirror of proj/src/pipeline.cpp:234-360).
+"""check_equivalence over the C-ABI (mirror of proj/src/pipeline.cpp:141-267).
 
 Given two packed-IR batches of equal length (program i of A is checked
 against program i of B; one pair = one reference check_equivalence call),
 runs both on the GPU, builds one VC per Out cell in array-name order
-(pipeline.cpp:307-313), and assembles the reference's report: kernel errors
+(pipeline.cpp:214-220), and assembles the reference's report: kernel errors
 with their race/safety/deadlock payloads (harvest_errors, missing_output,
-pipeline.cpp:155-180, 278-305), per-VC verdicts and the side-condition union
-de-duplicated in VC order (pipeline.cpp:338-358).
+pipeline.cpp:62-87, 185-212), per-VC verdicts and the side-condition union
+de-duplicated in VC order (pipeline.cpp:245-265).
 
 Decision scope: the canonical fast path (decide.cpp:765-768). A VC whose
 canonical forms differ is reported as "undecided" — the exp-polynomial slow
@@ -76,7 +76,7 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
                 rep.error_kernel = side
                 rep.races, rep.safeties, rep.deadlock = rr.races, rr.safeties, rr.deadlock
                 break
-            # missing_output (pipeline.cpp:166-180): first unwritten Out cell
+            # missing_output (pipeline.cpp:73-87): first unwritten Out cell
             base = p * n_per
             off = 0
             miss = None

@@ -1,5 +1,5 @@
 """GPU parity of the whole check (reference check_equivalence report,
-pipeline.cpp:234-360) on the reference corpus (kernels/manifest.txt) and
+pipeline.cpp:141-267) on the reference corpus (kernels/manifest.txt) and
 extra pairs. Exact when the reference decides on the canonical fast path or
 a kernel fails; for pairs the reference settles on its host slow path, the
 per-VC fast-path bit (canonical forms identical) must match instead."""
