@@ -682,15 +682,22 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       EvalCtx E{log, log_stmt, base};
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
-      // one warp per work item, persistent over the sorted work list
+      // one warp per work item, persistent over the sorted work list;
       // persistent grid: exactly the resident capacity (no second wave)
+      const int smem = (int)(EVAL_PAGES * SPAGE);
+      CK(cudaFuncSetAttribute(k_eval_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_warp, 128, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_warp, EVAL_BLOCK, smem);
       if (per_sm < 1) per_sm = 1;
-      uint64_t threads = std::min<uint64_t>(n_work * 32, (uint64_t)nsm * per_sm * 128);
+      // every resident slot is launched (warps spread over all SMs); the
+      // claim size keeps all warps busy when the work list is short
+      uint64_t threads = (uint64_t)nsm * per_sm * EVAL_BLOCK;
+      const uint64_t warps = threads / 32;
+      const uint32_t grab = n_work >= warps * 16 ? 4 : (n_work >= warps * 4 ? 2 : 1);
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
-      LAUNCH(k_eval_warp<<<blocks(threads, 128), 128, 0, s>>>(B, ctx->T, E, wv2, n_work, cursor, ctx->pool,
-                                                               ctx->pool_used, ctx->pool_cap, chunk));
+      LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, wv2, n_work, cursor,
+                                                                                ctx->pool, ctx->pool_used,
+                                                                                ctx->pool_cap, chunk, grab));
       CK(cudaGetLastError());
       CK(cudaFreeAsync(tmp2, s));
       CK(cudaFreeAsync(cursor, s));

@@ -16,7 +16,10 @@ namespace veqd {
 // ctaeq::Kind order (expr.hpp:20): Const < NegInf < Var < Exp < Max < Div <
 // Neg < Mul < Add. The numeric value is the compare rank.
 enum Kind : uint8_t { K_CONST = 0, K_NEGINF, K_VAR, K_EXP, K_MAX, K_DIV, K_NEG, K_MUL, K_ADD };
-enum : uint8_t { F_HASDIV = 1, F_POSDEF = 2 };
+// F_COEF: a Mul whose first kid is a Const (a term with coefficient != 1).
+// Terms without it are determined by their factor vector, so two like terms
+// of a sum without F_COEF terms are the same interned id.
+enum : uint8_t { F_HASDIV = 1, F_POSDEF = 2, F_COEF = 4 };
 
 // 32-byte node. Const: p0 = num, p1 = den. Var: p0 = order key, p1 =
 // identity (input << 40 | cell, or the undef key). Composite: p0 = offset of
@@ -53,6 +56,10 @@ struct Table {
 };
 
 __device__ __forceinline__ void set_error(const Table &T, int code) { atomicCAS(T.error, 0, code); }
+
+// Release/acquire fence at GPU scope: orders this thread's (and, after a
+// __syncwarp, its warp's) prior writes before a later publishing store.
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // ---- loads that bypass L1 (nodes are published by other SMs) -------------
 __device__ __forceinline__ Node ld_node(const Table &T, uint32_t id) {
@@ -224,8 +231,9 @@ __device__ __forceinline__ uint64_t composite_prefix(uint8_t kind, uint32_t nk, 
   return ((uint64_t)kind << 60) | (nk >= 4095 ? (4095ull << 48) : (((uint64_t)nk << 48) | (kid0_prefix >> 16)));
 }
 // positive_definite (proj/src/decide.cpp:306-333) from kid flags
-__device__ __forceinline__ uint8_t composite_flags(uint8_t kind, bool any_pd, bool all_pd, bool any_div) {
-  uint8_t flags = 0;
+__device__ __forceinline__ uint8_t composite_flags(uint8_t kind, bool any_pd, bool all_pd, bool any_div,
+                                                  bool kid0_const = false) {
+  uint8_t flags = (kind == K_MUL && kid0_const) ? F_COEF : 0;
   if (any_div || kind == K_DIV) flags |= F_HASDIV;
   if (kind == K_EXP) flags |= F_POSDEF;
   else if (kind == K_MAX && any_pd) flags |= F_POSDEF;
@@ -246,7 +254,7 @@ __device__ inline uint32_t intern(const Table &T, uint8_t kind, uint64_t p0, uin
   } else if (kind == K_VAR) {
     h = hcomb(h, p0);
   } else if (kind != K_NEGINF) {
-    bool any_pd = false, all_pd = true, any_div = false;
+    bool any_pd = false, all_pd = true, any_div = false, k0c = false;
     uint64_t sum = 0;
     for (uint32_t i = 0; i < nk; i++) {
       Node kn = ld_node(T, kids[i]);
@@ -255,10 +263,13 @@ __device__ inline uint32_t intern(const Table &T, uint8_t kind, uint64_t p0, uin
       any_pd |= pd;
       all_pd &= pd;
       any_div |= (kn.flags & F_HASDIV) != 0;
-      if (i == 0) p1 = composite_prefix(kind, nk, prefix_of(kn));
+      if (i == 0) {
+        p1 = composite_prefix(kind, nk, prefix_of(kn));
+        k0c = kn.kind == K_CONST;
+      }
     }
     h = composite_hash(kind, nk, sum);
-    flags = composite_flags(kind, any_pd, all_pd, any_div);
+    flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
   }
   return intern_meta(T, kind, p0, p1, kids, nk, h, flags);
 }
@@ -298,7 +309,7 @@ __device__ inline uint32_t intern_meta(const Table &T, uint8_t kind, uint64_t p0
         n.p0 = (kind == K_CONST || kind == K_VAR || kind == K_NEGINF) ? p0 : off;
         n.p1 = p1;
         T.nodes[id] = n;
-        __threadfence();
+        fence_acq_rel();
         mine = (uint32_t)id;
       }
       uint32_t prev = atomicCAS(T.slots + slot, EMPTY, mine);

@@ -1079,24 +1079,32 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
 }
 
 // Warp-per-item variant: fused Add chains run warp-cooperatively
-// (veq_warp.cuh); every other operation runs on lane 0.
-// 64 registers/thread: 32 resident warps per SM (the latency-bound work
-// needs the warps; the rare single-thread paths may spill)
-__global__ void __launch_bounds__(128, 8) k_eval_warp(Batch B, Table T, EvalCtx E, const uint32_t *work, uint64_t n_work,
-                            unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
-                            uint64_t chunk) {
+// (veq_warp.cuh); every other operation runs on lane 0. Sums of at most 32
+// terms stay in registers; larger ones take pages of the block's shared-
+// memory pool (warp_add_smem); like terms, -inf leaves or an exhausted pool
+// use the global-scratch path (warp_add_nary).
+// 64 registers/thread: 32 resident warps per SM (4 blocks of 8 warps).
+constexpr uint32_t EVAL_BLOCK = 256, EVAL_PAGES = 13;
+__global__ void __launch_bounds__(EVAL_BLOCK, 4) k_eval_warp(Batch B, Table T, EvalCtx E, const uint32_t *work,
+                                                             uint64_t n_work, unsigned long long *cursor, char *pool,
+                                                             unsigned long long *pool_used, uint64_t pool_cap,
+                                                             uint64_t chunk, uint32_t grab) {
+  extern __shared__ __align__(16) char eval_smem[];
+  __shared__ uint32_t s_mask;
+  if (threadIdx.x == 0) s_mask = 0;
+  __syncthreads();
+  const SmemPool SP{&s_mask, eval_smem, EVAL_PAGES};
   Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, chunk, 0};
   const uint32_t lane = lane_id();
-  // items are claimed EVAL_GRAB at a time; a warp works through its run in
+  // items are claimed `grab` at a time; a warp works through its run in
   // order, and every dependency of an item lies earlier in the sorted list,
   // so progress is guaranteed.
-  constexpr uint32_t EVAL_GRAB = 4;
   unsigned long long w = 0, w_end = 0;
   for (;;) {
     if (w == w_end) {
-      if (lane == 0) w = atomicAdd(cursor, (unsigned long long)EVAL_GRAB);
+      if (lane == 0) w = atomicAdd(cursor, (unsigned long long)grab);
       w = __shfl_sync(kFull, w, 0);
-      w_end = w + EVAL_GRAB;
+      w_end = w + grab;
     }
     if (w >= n_work) break;
     const uint32_t i = work[w++];
@@ -1104,37 +1112,71 @@ __global__ void __launch_bounds__(128, 8) k_eval_warp(Batch B, Table T, EvalCtx 
     char *const mbase = A.base;
     A.item = i;
     const veq_stmt st = B.stmts[i];
-    uint32_t r = 0;
+    uint32_t r = UNSET;
     if (st.kind == VEQ_ST_BINOP && st.op == VEQ_BIN_ADD) {
       const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
       const uint32_t b = E.log_base[h], n = pos + 2;
-      uint32_t *ids = warp_get<uint32_t>(A, n);
-      if (ids) {
-        bool neg = false;
-        for (uint32_t k = lane; k < n; k += 32) {
-          ids[k] = wait_node(B, E.log[b + k]);
-          neg |= ids[k] == T.id_neginf;
+      // pass 1: operands ready, -inf check; sums of <= 32 terms finish in
+      // registers
+      uint32_t leaf0 = UNSET, m = 0;
+      bool neg = false;
+      for (uint32_t k = lane; k < n; k += 32) {
+        uint32_t x = wait_node(B, E.log[b + k]);
+        if (k < 32) leaf0 = x;
+        neg |= x == T.id_neginf;
+      }
+      neg = __any_sync(kFull, neg);
+      if (!neg) {
+        bool counted = false;
+        if (n <= 32) {
+          r = warp_add_lean(T, leaf0, n, m);
+          counted = true;
         }
-        __syncwarp();
-        uint32_t start = 0;
-        if (__any_sync(kFull, neg)) {
-          // -inf operands: same restart rule as eval_stmt, sequentially
-          if (lane == 0) {
-            for (uint32_t k = 0; k < n; k++) {
-              if (ids[k] != T.id_neginf) continue;
-              uint32_t s = E.log_stmt[b + k];
-              arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
-              uint32_t rr = k < 1 ? 1 : k;
-              ids[rr] = intern_undef(T, 3, s >> 29, s);
-              start = rr;
-              if (k == 0) k = 1;
-            }
+        if (r == UNSET && (!counted || m > 32)) {
+          if (!counted) {
+            for (uint32_t k = lane; k < n; k += 32) m += n_terms_of(T, wait_node(B, E.log[b + k]));
+            m = __reduce_add_sync(kFull, m);
           }
-          start = __shfl_sync(kFull, start, 0);
-          __syncwarp();
+          const uint32_t pages = (uint32_t)((add_smem_bytes(n, m) + SPAGE - 1) / SPAGE);
+          const int first = pool_acquire(SP, pages);
+          if (first >= 0) {
+            char *buf = SP.base + (uint64_t)first * SPAGE;
+            uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
+            for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
+            __syncwarp();
+            r = warp_add_smem(T, buf, n, m);
+            pool_release(SP, first, pages);
+          }
+        } else if (r == UNSET && n <= 32) {
+          r = warp_add_small_reg(T, leaf0, n);  // like terms / coefficients
         }
-        r = warp_add_small(T, ids + start, n - start);
-        if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
+      }
+      if (r == UNSET) {
+        uint32_t *ids = warp_get<uint32_t>(A, n);
+        r = T.id_zero;
+        if (ids) {
+          for (uint32_t k = lane; k < n; k += 32) ids[k] = wait_node(B, E.log[b + k]);
+          __syncwarp();
+          uint32_t start = 0;
+          if (neg) {
+            // -inf operands: same restart rule as eval_stmt, sequentially
+            if (lane == 0) {
+              for (uint32_t k = 0; k < n; k++) {
+                if (ids[k] != T.id_neginf) continue;
+                uint32_t s = E.log_stmt[b + k];
+                arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
+                uint32_t rr = k < 1 ? 1 : k;
+                ids[rr] = intern_undef(T, 3, s >> 29, s);
+                start = rr;
+                if (k == 0) k = 1;
+              }
+            }
+            start = __shfl_sync(kFull, start, 0);
+            __syncwarp();
+          }
+          r = warp_add_small(T, ids + start, n - start);
+          if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
+        }
       }
     } else {
       if (lane == 0) r = eval_stmt(B, T, A, E, i);
@@ -1142,7 +1184,7 @@ __global__ void __launch_bounds__(128, 8) k_eval_warp(Batch B, Table T, EvalCtx 
     }
     if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
     if (lane == 0) {
-      __threadfence();
+      fence_acq_rel();
       atomicExch(B.canon + i, r);
     }
   }

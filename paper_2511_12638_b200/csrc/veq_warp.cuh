@@ -74,7 +74,7 @@ __device__ inline void warp_bitonic(uint64_t *key, uint32_t *val, uint32_t n, Le
 __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint32_t *kids, uint32_t nk) {
   const uint32_t lane = lane_id();
   uint64_t sum = 0, p1 = 0;
-  bool any_pd = false, all_pd = true, any_div = false;
+  bool any_pd = false, all_pd = true, any_div = false, k0c = false;
   for (uint32_t i = lane; i < nk; i += 32) {
     Node kn = ld_node(T, kids[i]);
     sum += kid_term(i, kn.hash);
@@ -82,15 +82,19 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
     any_pd |= pd;
     all_pd &= pd;
     any_div |= (kn.flags & F_HASDIV) != 0;
-    if (i == 0) p1 = composite_prefix(kind, nk, prefix_of(kn));
+    if (i == 0) {
+      p1 = composite_prefix(kind, nk, prefix_of(kn));
+      k0c = kn.kind == K_CONST;
+    }
   }
   sum = warp_sum_u64(sum);
   p1 = __shfl_sync(kFull, p1, 0);
+  k0c = __shfl_sync(kFull, k0c, 0);
   any_pd = __any_sync(kFull, any_pd);
   all_pd = __all_sync(kFull, all_pd);
   any_div = __any_sync(kFull, any_div);
   const uint64_t h = composite_hash(kind, nk, sum);
-  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div);
+  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
   uint64_t slot = h & T.slot_mask;
   uint32_t mine = EMPTY;
   for (uint64_t probes = 0;; probes++) {
@@ -126,8 +130,8 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
           n.p1 = p1;
           T.nodes[id] = n;
         }
-        __threadfence();
         __syncwarp();
+        fence_acq_rel();
         mine = (uint32_t)id;
       }
       uint32_t prev = 0;
@@ -196,24 +200,42 @@ __device__ __forceinline__ void reg_bitonic(uint64_t &key, uint32_t &val, Less l
   }
 }
 
+__device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
+                                              bool pd, bool dv, uint64_t p1, bool k0c);
+
 // Interns a composite whose kid i is held by lane i (m <= 32 kids).
 __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32_t kid, uint32_t m) {
   const uint32_t lane = lane_id();
   uint64_t term = 0, p1 = 0;
-  bool pd = true, dv = false;
+  bool pd = true, dv = false, k0c = false;
   if (lane < m) {
     Node kn = ld_node(T, kid);
     term = kid_term(lane, kn.hash);
     pd = kn.flags & F_POSDEF;
     dv = (kn.flags & F_HASDIV) != 0;
-    if (lane == 0) p1 = composite_prefix(kind, m, prefix_of(kn));
+    if (lane == 0) {
+      p1 = composite_prefix(kind, m, prefix_of(kn));
+      k0c = kn.kind == K_CONST;
+    }
+  }
+  return warp_intern_regs_h(T, kind, kid, m, term, pd, dv, __shfl_sync(kFull, p1, 0), __shfl_sync(kFull, k0c, 0));
+}
+
+// Same, with each lane's kid term hash (kid_term(lane, hash)) and flags
+// already known; p1 = composite prefix, k0c = kid 0 is a Const.
+__device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
+                                              bool pd, bool dv, uint64_t p1, bool k0c) {
+  const uint32_t lane = lane_id();
+  if (lane >= m) {
+    term = 0;
+    pd = true;
+    dv = false;
   }
   const uint64_t sum = warp_sum_u64(term);
-  p1 = __shfl_sync(kFull, p1, 0);
   const bool any_pd = __any_sync(kFull, lane < m && pd), all_pd = __all_sync(kFull, pd);
   const bool any_div = __any_sync(kFull, dv);
   const uint64_t h = composite_hash(kind, m, sum);
-  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div);
+  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
   uint64_t slot = h & T.slot_mask;
   uint32_t mine = EMPTY;
   for (uint64_t probes = 0;; probes++) {
@@ -249,8 +271,8 @@ __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32
           n.p1 = p1;
           T.nodes[id] = n;
         }
-        __threadfence();
         __syncwarp();
+        fence_acq_rel();
         mine = (uint32_t)id;
       }
       uint32_t prev = 0;
@@ -321,6 +343,389 @@ __device__ inline uint32_t warp_add_small(const Table &T, const uint32_t *leaves
   if (lane >= m) id = UNSET;
   reg_bitonic(pk, id, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) { return canon_less(T, ka, va, kb, vb); });
   return warp_intern_regs(T, K_ADD, id, m);
+}
+
+// Register-leaf variant of warp_add_small: lane i holds leaf i (n <= 32).
+__device__ inline uint32_t warp_add_small_reg(const Table &T, uint32_t leaf_reg, uint32_t n) {
+  const uint32_t lane = lane_id();
+  uint32_t leaf = UNSET, c = 0, kind = 0;
+  uint64_t p0 = 0;
+  if (lane < n) {
+    leaf = leaf_reg;
+    Node ln = ld_node(T, leaf);
+    kind = ln.kind;
+    p0 = ln.p0;
+    c = ln.kind == K_ADD ? ln.nkids : 1;
+  }
+  uint32_t m;
+  const uint32_t ex = warp_excl_scan(c, m);
+  if (m > 32) return UNSET;
+  uint32_t src_leaf = 0;
+  for (uint32_t l = 0; l < n; l++) {
+    uint32_t el = __shfl_sync(kFull, ex, l), cl = __shfl_sync(kFull, c, l);
+    if (cl && el <= lane) src_leaf = l;
+  }
+  const uint32_t lk = __shfl_sync(kFull, kind, src_leaf);
+  const uint64_t lp = __shfl_sync(kFull, p0, src_leaf);
+  const uint32_t lid = __shfl_sync(kFull, leaf, src_leaf);
+  const uint32_t lex = __shfl_sync(kFull, ex, src_leaf);
+  uint32_t term_node = UNSET;
+  uint64_t key = ~0ull;
+  bool real = false;
+  if (lane < m) {
+    term_node = lk == K_ADD ? ld_kid(T, lp + (lane - lex)) : lid;
+    real = term_node != T.id_zero;
+    if (real) key = decompose_one(T, term_node).fh;
+  }
+  m = __popc(__ballot_sync(kFull, real));
+  uint32_t val = lane;
+  reg_bitonic(key, val, [](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return ka != kb ? ka < kb : va < vb;
+  });
+  const uint64_t prev = __shfl_up_sync(kFull, key, 1);
+  if (__any_sync(kFull, lane > 0 && lane < m && key == prev)) return UNSET;
+  if (m == 0) return T.id_zero;
+  if (m == 1) return __shfl_sync(kFull, term_node, __shfl_sync(kFull, val, 0) & 31);
+  uint32_t id = __shfl_sync(kFull, term_node, val & 31);
+  uint64_t pk = lane < m ? prefix_id(T, id) : ~0ull;
+  if (lane >= m) id = UNSET;
+  reg_bitonic(pk, id, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) { return canon_less(T, ka, va, kb, vb); });
+  return warp_intern_regs(T, K_ADD, id, m);
+}
+
+
+// Register bitonic over (key, id) carrying one extra payload lane index.
+template <class Less>
+__device__ __forceinline__ void reg_bitonic3(uint64_t &key, uint32_t &val, uint32_t &aux, Less less) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      uint64_t pk = __shfl_xor_sync(kFull, key, j);
+      uint32_t pv = __shfl_xor_sync(kFull, val, j);
+      uint32_t pa = __shfl_xor_sync(kFull, aux, j);
+      bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      bool take = (up == lower) ? less(pk, pv, key, val) : less(key, val, pk, pv);
+      if (take) {
+        key = pk;
+        val = pv;
+        aux = pa;
+      }
+    }
+  }
+}
+
+// Lean register path for a sum of at most 32 terms (canon_add_kids,
+// expr.cpp:415-424), lane k < n holding leaf k. Each term node is loaded
+// once; its hash, flags and order prefix travel with it through the sort.
+// Returns UNSET when the path does not apply: more than 32 terms (`m_out`
+// then holds the term count), a term with a coefficient (F_COEF: like terms
+// need factor-vector grouping), or like terms (equal ids after the sort).
+__device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t n, uint32_t &m_out) {
+  const uint32_t lane = lane_id();
+  uint32_t c = 0, kind = 0;
+  uint64_t p0 = 0;
+  if (lane < n) {
+    const Node ln = ld_node(T, leaf);
+    kind = ln.kind;
+    p0 = ln.p0;
+    c = ln.kind == K_ADD ? ln.nkids : 1;
+  }
+  uint32_t m;
+  const uint32_t ex = warp_excl_scan(c, m);
+  m_out = m;
+  if (m > 32) return UNSET;
+  // owning leaf of term `lane`: leaves with c >= 1 start at ex
+  const uint32_t starts = __reduce_or_sync(kFull, (lane < n && c) ? (1u << ex) : 0u);
+  const uint32_t src = __popc(starts & (lane == 31 ? ~0u : ((2u << lane) - 1))) - 1;
+  const uint32_t lk = __shfl_sync(kFull, kind, src & 31);
+  const uint64_t lp = __shfl_sync(kFull, p0, src & 31);
+  const uint32_t lid = __shfl_sync(kFull, leaf, src & 31);
+  const uint32_t lex = __shfl_sync(kFull, ex, src & 31);
+  uint32_t id = UNSET;
+  uint64_t key = ~0ull, hsh = 0;
+  uint8_t fl = 0, tk = 0;
+  Rat cv{0, 1};
+  if (lane < m) {
+    id = lk == K_ADD ? ld_kid(T, lp + (lane - lex)) : lid;
+    Node tn = ld_node(T, id);
+    key = prefix_of(tn);
+    hsh = tn.hash;
+    fl = tn.flags;
+    tk = tn.kind;
+    if (tk == K_CONST) cv = const_val(tn);
+  }
+  if (__any_sync(kFull, lane < m && tk == K_MUL && (fl & F_COEF))) return UNSET;
+  // fold the Const terms into one (dropped when zero)
+  const uint32_t cmask = __ballot_sync(kFull, lane < m && tk == K_CONST);
+  if (cmask) {
+    const uint32_t keep = __ffs(cmask) - 1;
+    const bool keep_zero = __shfl_sync(kFull, (uint32_t)(cv.n == 0), keep);
+    if (__popc(cmask) > 1 || keep_zero) {
+      // exact sum over the Const lanes (lane order; rational addition is exact)
+      Rat acc{0, 1};
+      for (uint32_t mm = cmask; mm; mm &= mm - 1) {
+        const uint32_t q = __ffs(mm) - 1;
+        Rat v{(long long)__shfl_sync(kFull, (unsigned long long)cv.n, q),
+              (long long)__shfl_sync(kFull, (unsigned long long)cv.d, q)};
+        acc = rat_add(T, acc, v);
+      }
+      uint32_t cid = UNSET;
+      if (lane == 0) cid = rat_is(acc, 0) ? UNSET : intern_const(T, acc);
+      cid = __shfl_sync(kFull, cid, 0);
+      if (lane < m && tk == K_CONST) {
+        if (lane == keep && cid != UNSET) {
+          id = cid;
+          Node cn = ld_node(T, cid);
+          hsh = cn.hash;
+          fl = cn.flags;
+          key = 0;
+        } else {
+          id = UNSET;
+          key = ~0ull;
+        }
+      }
+    }
+  }
+  uint32_t aux = lane;
+  reg_bitonic3(key, id, aux, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) { return canon_less(T, ka, va, kb, vb); });
+  const uint32_t real = __popc(__ballot_sync(kFull, id != UNSET));
+  // like terms (coefficient-free): equal ids, adjacent after the sort
+  const uint32_t prev = __shfl_up_sync(kFull, id, 1);
+  if (__any_sync(kFull, lane > 0 && lane < real && id == prev)) return UNSET;
+  if (real == 0) return T.id_zero;
+  if (real == 1) return __shfl_sync(kFull, id, 0);
+  const uint64_t kh = __shfl_sync(kFull, hsh, aux & 31);
+  const uint8_t kf = (uint8_t)__shfl_sync(kFull, (uint32_t)fl, aux & 31);
+  const uint64_t k0p = __shfl_sync(kFull, key, 0);
+  const bool k0c = __shfl_sync(kFull, (uint32_t)(key == 0), 0);
+  return warp_intern_regs_h(T, K_ADD, id, real, kid_term(lane, kh), kf & F_POSDEF, (kf & F_HASDIV) != 0,
+                            composite_prefix(K_ADD, real, k0p), k0c);
+}
+
+// ---- shared-memory path for large sums -------------------------------------
+// A block-wide pool of 4 KB shared-memory pages; a warp evaluating a sum with
+// more than 32 terms takes a contiguous page run for its working set and
+// returns it when the item completes (it never waits on other items while
+// holding pages, so the pool cannot deadlock; if no run is free the item
+// uses the global-scratch path instead).
+constexpr uint32_t SPAGE = 4096;
+struct SmemPool {
+  uint32_t *mask;  // bit i: page i taken
+  char *base;
+  uint32_t npages;
+};
+
+__device__ inline int pool_acquire(const SmemPool &P, uint32_t k) {
+  int got = -1;
+  if (lane_id() == 0 && k <= P.npages) {
+    const uint32_t all = P.npages >= 32 ? ~0u : ((1u << P.npages) - 1);
+    for (int tries = 0; tries < 4096 && got < 0; tries++) {
+      uint32_t m = *(volatile uint32_t *)P.mask;
+      uint32_t fr = ~m & all, x = fr;
+      for (uint32_t j = 1; j < k; j++) x &= fr >> j;
+      if (!x) {
+        __nanosleep(256);
+        continue;
+      }
+      int i = __ffs(x) - 1;
+      uint32_t bits = (k >= 32 ? ~0u : ((1u << k) - 1)) << i;
+      if (atomicCAS(P.mask, m, m | bits) == m) got = i;
+    }
+  }
+  return __shfl_sync(kFull, got, 0);
+}
+__device__ inline void pool_release(const SmemPool &P, int first, uint32_t k) {
+  __syncwarp();
+  if (lane_id() == 0) atomicAnd(P.mask, ~((k >= 32 ? ~0u : ((1u << k) - 1)) << first));
+}
+
+// Working-set bytes of warp_add_smem for n leaves and m terms.
+__device__ __forceinline__ uint32_t hash_slots(uint32_t m) {
+  uint32_t H = 64;
+  while (H < m + m / 2 + 1) H <<= 1;
+  return H;
+}
+__device__ __forceinline__ uint64_t add_smem_bytes(uint32_t n, uint32_t m) {
+  uint64_t a = ((uint64_t)(2 * n + 1 + m) * 4 + 7) & ~7ull;
+  uint64_t y = 8ull * m + (uint64_t)hash_slots(m) * 4;  // coefficient grouping
+  if (y < 12ull * m) y = 12ull * m;                      // merge ping-pong
+  return a + 8ull * m + y;
+}
+
+__device__ __forceinline__ bool pref_less(const Table &T, uint64_t pa, uint32_t a, uint64_t pb, uint32_t b) {
+  if (pa != pb) return pa < pb;
+  return cmp_nodes(T, a, b) < 0;
+}
+
+// canon_add_kids (expr.cpp:415-424) over n canonical leaves already stored in
+// lv[] (shared memory, inside `buf`), m terms in total. Fast path: every
+// non-constant term has a distinct factor vector (checked exactly via a
+// shared-memory hash table on factor-vector hashes; any hash hit, true or
+// false, defers to the exact global-scratch path by returning UNSET). Then
+// the result's kids are the terms themselves plus at most one folded Const,
+// and canonical order (Expr::compare) is produced by merging the leaves'
+// already-sorted kid runs with warp-parallel merge-path passes.
+__device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint32_t m) {
+  const uint32_t lane = lane_id();
+  uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
+  uint32_t *rs = lv + n;  // run starts = leaf term offsets, n + 1 entries
+  uint32_t *idA = rs + n + 1;
+  uint64_t *preA = reinterpret_cast<uint64_t *>(buf + (((uint64_t)(2 * n + 1 + m) * 4 + 7) & ~7ull));
+  char *Y = reinterpret_cast<char *>(preA + m);
+  const uint32_t H = hash_slots(m);
+  uint64_t *preB = reinterpret_cast<uint64_t *>(Y);
+  uint32_t *idB = reinterpret_cast<uint32_t *>(preB + m);
+  // 1. term offsets per leaf
+  uint32_t run = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    uint32_t i = base + lane;
+    uint32_t c = i < n ? n_terms_of(T, lv[i]) : 0;
+    uint32_t tot;
+    uint32_t ex = warp_excl_scan(c, tot);
+    if (i < n) rs[i] = run + ex;
+    run += tot;
+  }
+  if (lane == 0) rs[n] = run;
+  __syncwarp();
+  // 2. gather terms and their order prefixes; note coefficient terms
+  bool coef = false;
+  uint32_t nconst = 0;
+  for (uint32_t t = lane; t < m; t += 32) {
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) / 2;
+      if (rs[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    uint32_t leaf = lv[lo];
+    Node ln = ld_node(T, leaf);
+    uint32_t id = ln.kind == K_ADD ? ld_kid(T, ln.p0 + (t - rs[lo])) : leaf;
+    Node tn = ln.kind == K_ADD ? ld_node(T, id) : ln;
+    idA[t] = id;
+    preA[t] = prefix_of(tn);
+    nconst += tn.kind == K_CONST;
+    coef |= tn.kind == K_MUL && (tn.flags & F_COEF);
+  }
+  nconst = __reduce_add_sync(kFull, nconst);
+  coef = __any_sync(kFull, coef);
+  __syncwarp();
+  if (coef) {
+    // like terms may differ in id: exact grouping key = factor-vector hash
+    // in a shared-memory table; any hit (true or a hash collision) defers to
+    // the exact global-scratch path
+    bool dup = false;
+    uint64_t *fh = preB;  // Y is free until the sort
+    uint32_t *hs2 = reinterpret_cast<uint32_t *>(Y + 8ull * m);
+    for (uint32_t i = lane; i < H; i += 32) hs2[i] = EMPTY;
+    __syncwarp();
+    for (uint32_t t = lane; t < m; t += 32) {
+      Term tm = decompose_one(T, idA[t]);
+      if (tm.nf == 0) continue;
+      const uint64_t h = tm.fh;
+      fh[t] = h;
+      __threadfence_block();  // publish the hash before the slot that names it
+      uint32_t sl = (uint32_t)(h ^ (h >> 32)) & (H - 1);
+      for (;;) {
+        uint32_t prev = atomicCAS(hs2 + sl, EMPTY, t);
+        if (prev == EMPTY) break;
+        __threadfence_block();
+        if (fh[prev] == h) {
+          dup = true;
+          break;
+        }
+        sl = (sl + 1) & (H - 1);
+      }
+    }
+    __syncwarp();
+    if (__any_sync(kFull, dup)) return UNSET;
+  }
+  // 4. merge the sorted leaf runs pairwise until one run remains
+  uint32_t R = n;
+  uint64_t *ps = preA, *pd = preB;
+  uint32_t *is = idA, *id_ = idB;
+  const uint32_t E = (m + 31) / 32;
+  while (R > 1) {
+    const uint32_t npairs = (R + 1) / 2;
+    uint32_t pos = min(lane * E, m), end = min(pos + E, m);
+    while (pos < end) {
+      // pair p holding output position pos: largest p with rs[2p] <= pos
+      uint32_t lo = 0, hi = npairs;
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) / 2;
+        if (rs[2 * mid] <= pos) lo = mid;
+        else hi = mid;
+      }
+      const uint32_t a0 = rs[2 * lo], a1 = rs[min(2 * lo + 1, R)], b1 = rs[min(2 * lo + 2, R)];
+      const uint32_t d = pos - a0, la = a1 - a0, lb = b1 - a1;
+      // co-rank: i = number of A elements among the first d outputs
+      uint32_t ilo = d > lb ? d - lb : 0, ihi = min(d, la);
+      while (ilo < ihi) {
+        uint32_t mid = (ilo + ihi) / 2;
+        uint32_t bj = a1 + (d - mid - 1);
+        if (pref_less(T, ps[a0 + mid], is[a0 + mid], ps[bj], is[bj])) ilo = mid + 1;
+        else ihi = mid;
+      }
+      uint32_t i = a0 + ilo, j = a1 + (d - ilo);
+      const uint32_t stop = min(end, b1);
+      for (; pos < stop; pos++) {
+        bool takeA;
+        if (i >= a1) takeA = false;
+        else if (j >= b1) takeA = true;
+        else takeA = pref_less(T, ps[i], is[i], ps[j], is[j]);
+        if (takeA) {
+          pd[pos] = ps[i];
+          id_[pos] = is[i];
+          i++;
+        } else {
+          pd[pos] = ps[j];
+          id_[pos] = is[j];
+          j++;
+        }
+      }
+    }
+    __syncwarp();
+    // run starts of the merged runs: rs'[p] = rs[2p]
+    for (uint32_t base = 0; base <= npairs; base += 32) {
+      uint32_t p = base + lane;
+      uint32_t v = p <= npairs ? rs[min(2 * p, R)] : 0;
+      __syncwarp();
+      if (p <= npairs) rs[p] = v;
+      __syncwarp();
+    }
+    R = npairs;
+    uint64_t *tp = ps;
+    ps = pd;
+    pd = tp;
+    uint32_t *ti = is;
+    is = id_;
+    id_ = ti;
+  }
+  // like terms without coefficients are equal interned ids: adjacent now
+  {
+    bool dup = false;
+    for (uint32_t t = lane + 1; t < m; t += 32) dup |= is[t] == is[t - 1];
+    if (__any_sync(kFull, dup)) return UNSET;
+  }
+  // 5. fold the leading Const terms into one (dropped when zero)
+  uint32_t first = 0;
+  if (nconst) {
+    uint32_t cid = 0;
+    if (lane == 0) {
+      Rat c{0, 1};
+      for (uint32_t k = 0; k < nconst; k++) c = rat_add(T, c, const_val(ld_node(T, is[k])));
+      cid = rat_is(c, 0) ? UNSET : intern_const(T, c);
+      if (cid != UNSET) is[nconst - 1] = cid;
+    }
+    cid = __shfl_sync(kFull, cid, 0);
+    first = cid == UNSET ? nconst : nconst - 1;
+    __syncwarp();
+  }
+  const uint32_t nout = m - first;
+  if (nout == 0) return T.id_zero;
+  if (nout == 1) return is[first];
+  return warp_intern(T, K_ADD, is + first, nout);
 }
 
 // canon_add_kids over n canonical leaves (scratch), warp-cooperative.
