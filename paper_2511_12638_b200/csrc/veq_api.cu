@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -166,6 +167,8 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   if (!ctx->lim.max_kid_words) ctx->lim.max_kid_words = 256ull << 20;
   if (!ctx->lim.scratch_bytes) ctx->lim.scratch_bytes = 4ull << 30;
   if (ctx->lim.max_nodes >= (1ull << 31)) ctx->lim.max_nodes = (1ull << 31) - 1;
+  // kid-arena offsets travel as u32 in the eval kernel's shared working sets
+  if (ctx->lim.max_kid_words >= (1ull << 32)) ctx->lim.max_kid_words = (1ull << 32) - 1;
   auto bail = [&](int code, const char *what) {
     fprintf(stderr, "veq_open: %s\n", what);
     delete ctx;
@@ -188,7 +191,7 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   if (cudaMalloc(&ctx->nodes, ctx->lim.max_nodes * sizeof(Node)) != cudaSuccess) return bail(VEQ_E_OOM, "nodes");
   if (cudaMalloc(&ctx->kids, ctx->lim.max_kid_words * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "kids");
   if (cudaMalloc(&ctx->slots, slots * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "slots");
-  if (cudaMalloc(&ctx->counters, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "counters");
+  if (cudaMalloc(&ctx->counters, 8 * sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "counters");
   if (cudaMalloc(&ctx->error, sizeof(int)) != cudaSuccess) return bail(VEQ_E_OOM, "error");
   if (cudaMalloc(&ctx->dbg, 4 * sizeof(unsigned long long)) != cudaSuccess) return bail(VEQ_E_OOM, "dbg");
   if (cudaMalloc(&ctx->session_ids, 4 * sizeof(uint32_t)) != cudaSuccess) return bail(VEQ_E_OOM, "ids");
@@ -290,7 +293,7 @@ int veq_clear_terms(veq_ctx *ctx) {
   CK(cudaSetDevice(ctx->device));
   Table &T = ctx->T;
   CK(cudaMemsetAsync(ctx->slots, 0xff, ctx->n_slots * sizeof(uint32_t), ctx->stream));
-  CK(cudaMemsetAsync(ctx->counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  CK(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dbg, 0, 4 * sizeof(unsigned long long), ctx->stream));
   // a single thread interns -inf, 0, 1, -1 first into an empty table, so
@@ -332,76 +335,54 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   bd->thread_stmt.assign(d->thread_stmt, d->thread_stmt + Tn + 1);
   bd->n_stmts = S;
   bd->n_threads = Tn;
-  // ---- host preparation: thread->program, segments, canonical sync ids,
-  // release capacities, register offsets, cell bases
-  std::vector<uint32_t> thread_prog(Tn);
-  std::vector<uint64_t> seg_off(Tn + 1, 0), reg_off(Tn + 1, 0), rel_off(P + 1, 0);
-  std::vector<uint64_t> seg_start;
-  std::vector<uint32_t> seg_set, prog_full(P, UNSET);
-  uint64_t n_access = 0;
+  // ---- host preparation (per program / array / pool entry only): program
+  // ranges, register offsets, sync-set pool canonicalisation, cell bases.
+  // Everything per statement runs on the device (k_prep_*).
+  std::vector<uint64_t> reg_off(Tn + 1, 0);
   for (uint32_t p = 0; p < P; p++) {
     const veq_program_meta &m = d->progs[p];
-    if (m.thread_off + m.n_threads > Tn || m.array_off + m.n_arrays > d->n_arrays_total) {
+    if ((uint64_t)m.thread_off + m.n_threads > Tn || (uint64_t)m.array_off + m.n_arrays > d->n_arrays_total) {
       delete bd;
       return fail(ctx, VEQ_E_INVALID_IR, "program " + std::to_string(p) + " out of range");
     }
-    std::map<std::vector<uint64_t>, uint32_t> canon_sets;  // content -> canonical pool id
-    uint64_t nsync = 0;
-    for (uint32_t t = 0; t < m.n_threads; t++) {
-      uint32_t gt = m.thread_off + t;
-      thread_prog[gt] = p;
-      reg_off[gt + 1] = d->thread_nregs[gt];
-      uint64_t s0 = d->thread_stmt[gt], s1 = d->thread_stmt[gt + 1];
-      seg_start.push_back(s0);
-      for (uint64_t i = s0; i < s1; i++) {
-        const veq_stmt &st = d->stmts[i];
-        if (st.kind > VEQ_ST_SYNC) {
+  }
+  for (uint32_t t = 0; t < Tn; t++) {
+    if (d->thread_stmt[t + 1] < d->thread_stmt[t] || d->thread_stmt[t + 1] > S) {
+      delete bd;
+      return fail(ctx, VEQ_E_INVALID_IR, "thread statement ranges are not monotone");
+    }
+    reg_off[t + 1] = reg_off[t] + d->thread_nregs[t];
+  }
+  // content-equal sync sets share the id of their first pool entry; the
+  // full set of every program is the extra entry n_syncsets
+  const uint32_t NS = d->n_syncsets;
+  std::vector<uint32_t> set_canon(NS), set_pop(NS);
+  std::vector<veq_syncset> sets(d->syncsets, d->syncsets + NS);
+  sets.push_back(veq_syncset{1, 0, 0, 0});
+  {
+    std::unordered_map<std::string, uint32_t> seen;
+    std::string key;
+    for (uint32_t i = 0; i < NS; i++) {
+      const veq_syncset &q = d->syncsets[i];
+      uint32_t pop = 0;
+      key.assign(reinterpret_cast<const char *>(&q.full), 4);
+      if (!q.full) {
+        if ((uint64_t)q.word_off + (q.n_bits + 63) / 64 > d->n_set_words) {
           delete bd;
-          return fail(ctx, VEQ_E_INVALID_IR, "bad statement kind");
+          return fail(ctx, VEQ_E_INVALID_IR, "sync set words out of range");
         }
-        if ((st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE) && st.arr >= m.n_arrays) {
-          delete bd;
-          return fail(ctx, VEQ_E_INVALID_IR, "array index out of range");
-        }
-        if (st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE) n_access++;
-        if (st.kind == VEQ_ST_SYNC) {
-          if (st.a >= d->n_syncsets) {
-            delete bd;
-            return fail(ctx, VEQ_E_INVALID_IR, "sync set index out of range");
-          }
-          const veq_syncset &q = d->syncsets[st.a];
-          std::vector<uint64_t> key;
-          bool is_full = q.full != 0;
-          if (!is_full) {
-            // a window set covering every thread is the full set
-            uint64_t cnt = 0;
-            for (uint32_t k = 0; k < q.n_bits; k++)
-              if ((d->set_words[q.word_off + k / 64] >> (k % 64)) & 1ull) cnt++;
-            is_full = (cnt == m.n_threads);
-            key.push_back(q.lo);
-            key.push_back(q.n_bits);
-            for (uint32_t w = 0; w < (q.n_bits + 63) / 64; w++) key.push_back(d->set_words[q.word_off + w]);
-          }
-          uint32_t cid;
-          if (is_full) {
-            if (prog_full[p] == UNSET) prog_full[p] = st.a;
-            cid = prog_full[p];
-          } else {
-            auto it = canon_sets.find(key);
-            if (it == canon_sets.end()) it = canon_sets.emplace(key, st.a).first;
-            cid = it->second;
-          }
-          seg_set.push_back(cid);
-          seg_start.push_back(i + 1);
-          nsync++;
+        key.append(reinterpret_cast<const char *>(&q.lo), 8);
+        for (uint32_t w = 0; w < (q.n_bits + 63) / 64; w++) {
+          uint64_t x = d->set_words[q.word_off + w];
+          if (w == (q.n_bits - 1) / 64 && q.n_bits % 64) x &= (1ull << (q.n_bits % 64)) - 1;
+          pop += __builtin_popcountll(x);
+          key.append(reinterpret_cast<const char *>(&x), 8);
         }
       }
-      seg_set.push_back(UNSET);  // last segment has no ending sync
-      seg_off[gt + 1] = seg_start.size();
+      set_canon[i] = seen.emplace(key, i).first->second;
+      set_pop[i] = q.full ? ~0u : pop;
     }
-    rel_off[p + 1] = rel_off[p] + nsync;
   }
-  for (uint32_t t = 0; t < Tn; t++) reg_off[t + 1] += reg_off[t];
   std::vector<uint64_t> cell_base(d->n_arrays_total, UNSET64);
   uint64_t cells = 0;
   for (uint32_t a = 0; a < d->n_arrays_total; a++) {
@@ -422,10 +403,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   }
   bd->arr_cell_base = cell_base;
   bd->n_cells = cells;
-  bd->n_segs = seg_start.size();
-  bd->n_rel_cap = rel_off[P];
   bd->n_regs = reg_off[Tn];
-  bd->n_access_max = n_access;
   // ---- upload
   Batch &B = bd->B;
   B.n_progs = P;
@@ -433,34 +411,104 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   B.n_stmts = S;
   B.n_cells = cells;
   int r = 0;
+  cudaStream_t s = ctx->stream;
 #define UP(field, src, n, T_)                                                            \
   do {                                                                                   \
     T_ *p_ = nullptr;                                                                    \
     if ((r = dupload(ctx, bd, &p_, (const T_ *)(src), (n)))) { delete bd; return r; }   \
     B.field = p_;                                                                        \
   } while (0)
+#define AL(field, n, T_)                                                  \
+  do {                                                                    \
+    T_ *p_ = nullptr;                                                     \
+    if ((r = dalloc(ctx, bd, &p_, (n)))) { delete bd; return r; }        \
+    B.field = p_;                                                         \
+  } while (0)
   UP(progs, d->progs, P, veq_program_meta);
   UP(thread_stmt, d->thread_stmt, Tn + 1, uint64_t);
-  UP(thread_prog, thread_prog.data(), Tn, uint32_t);
   UP(stmts, d->stmts, S, veq_stmt);
   UP(arrays, d->arrays, d->n_arrays_total, veq_array);
   UP(arr_cell_base, cell_base.data(), cell_base.size(), uint64_t);
-  UP(sets, d->syncsets, d->n_syncsets, veq_syncset);
+  UP(sets, sets.data(), sets.size(), veq_syncset);
   UP(set_words, d->set_words, d->n_set_words, uint64_t);
-  UP(seg_off, seg_off.data(), Tn + 1, uint64_t);
-  UP(seg_start, seg_start.data(), seg_start.size(), uint64_t);
-  UP(seg_set, seg_set.data(), seg_set.size(), uint32_t);
-  UP(rel_off, rel_off.data(), P + 1, uint64_t);
   UP(reg_off, reg_off.data(), Tn + 1, uint64_t);
-  UP(prog_full_set, prog_full.data(), P, uint32_t);
-  {
-    std::vector<uint32_t> longs;
-    for (uint32_t t = 0; t < Tn; t++)
-      if (d->thread_stmt[t + 1] - d->thread_stmt[t] >= EXEC_WARP_MIN) longs.push_back(t);
-    B.n_long = (uint32_t)longs.size();
-    UP(long_threads, longs.data(), longs.size(), uint32_t);
+  AL(thread_prog, Tn, uint32_t);
+  AL(prog_full_set, P, uint32_t);
+  // ---- device preparation
+  uint32_t *d_canon = nullptr, *d_pop = nullptr, *d_long = nullptr;
+  unsigned long long *d_cnt = nullptr, *d_nlong = nullptr;
+  uint64_t *d_psync = nullptr;
+  if ((r = dupload(ctx, nullptr, &d_canon, set_canon.data(), NS)) || (r = dupload(ctx, nullptr, &d_pop, set_pop.data(), NS)) ||
+      (r = dalloc(ctx, nullptr, &d_cnt, S + 1)) || (r = dalloc(ctx, nullptr, &d_nlong, 1)) ||
+      (r = dalloc(ctx, nullptr, &d_psync, P + 1)) || (r = dalloc(ctx, bd, &d_long, Tn))) {
+    delete bd;
+    return r;
   }
-#undef UP
+  B.long_threads = d_long;
+  PrepArgs PA{P, Tn, NS, d->n_arrays_total, S, B.progs, B.thread_stmt, B.thread_prog, B.stmts, B.sets, d_canon, d_pop,
+              d_cnt, ctx->error};
+  CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(d_cnt + S, 0, 8, s));
+  CK(cudaMemsetAsync(d_nlong, 0, 8, s));
+  if (P) k_prep_thread_prog<<<P, 256, 0, s>>>(PA, (uint32_t *)B.thread_prog);
+  if (S) k_prep_stmts<<<blocks(S, 256), 256, 0, s>>>(PA);
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, d_cnt, d_cnt, (int64_t)(S + 1), s);
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tb, s));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, d_cnt, d_cnt, (int64_t)(S + 1), s);
+    CK(cudaFreeAsync(tmp, s));
+  }
+  if (Tn) k_prep_long<<<blocks(Tn, 256), 256, 0, s>>>(PA, d_long, d_nlong, EXEC_WARP_MIN);
+  unsigned long long tot = 0, nlong = 0;
+  int perr = 0;
+  CK(cudaMemcpyAsync(&tot, d_cnt + S, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&nlong, d_nlong, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&perr, ctx->error, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (perr) {
+    cudaFreeAsync(d_canon, s);
+    cudaFreeAsync(d_pop, s);
+    cudaFreeAsync(d_cnt, s);
+    cudaFreeAsync(d_nlong, s);
+    cudaFreeAsync(d_psync, s);
+    cudaMemsetAsync(ctx->error, 0, sizeof(int), s);
+    delete bd;
+    return fail(ctx, VEQ_E_INVALID_IR, perr == 1 ? "bad statement kind"
+                                       : perr == 2 ? "array index out of range"
+                                                   : "sync set index out of range");
+  }
+  const uint64_t n_syncs = tot & 0xffffffffull, n_access = tot >> 32;
+  B.n_long = (uint32_t)nlong;
+  bd->n_segs = (uint64_t)Tn + n_syncs;
+  bd->n_rel_cap = n_syncs;
+  bd->n_access_max = n_access;
+  AL(seg_off, Tn + 1, uint64_t);
+  AL(seg_start, bd->n_segs, uint64_t);
+  AL(seg_set, bd->n_segs, uint32_t);
+  AL(rel_off, P + 1, uint64_t);
+  k_prep_threads<<<blocks((uint64_t)Tn + 1, 256), 256, 0, s>>>(PA, (uint64_t *)B.seg_off, (uint64_t *)B.seg_start,
+                                                               (uint32_t *)B.seg_set);
+  if (S) k_prep_syncs<<<blocks(S, 256), 256, 0, s>>>(PA, (uint64_t *)B.seg_start, (uint32_t *)B.seg_set);
+  if (P) {
+    k_prep_progs<<<blocks(P, 256), 256, 0, s>>>(PA, d_psync, (uint32_t *)B.prog_full_set);
+    CK(cudaMemsetAsync(d_psync + P, 0, 8, s));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, d_psync, (uint64_t *)B.rel_off, (int64_t)(P + 1), s);
+    void *tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, tb, s));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, d_psync, (uint64_t *)B.rel_off, (int64_t)(P + 1), s);
+    CK(cudaFreeAsync(tmp, s));
+  } else {
+    CK(cudaMemsetAsync((void *)B.rel_off, 0, 8, s));
+  }
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(d_canon, s));
+  CK(cudaFreeAsync(d_pop, s));
+  CK(cudaFreeAsync(d_cnt, s));
+  CK(cudaFreeAsync(d_nlong, s));
+  CK(cudaFreeAsync(d_psync, s));
   uint32_t *cn = nullptr;
   veq_rat *dconsts = nullptr;
   if ((r = dalloc(ctx, bd, &cn, d->n_consts)) || (r = dupload(ctx, bd, &dconsts, d->consts, d->n_consts))) {
@@ -471,12 +519,6 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   bd->dconsts = dconsts;
   bd->n_consts = d->n_consts;
   // run-state buffers
-#define AL(field, n, T_)                                                  \
-  do {                                                                    \
-    T_ *p_ = nullptr;                                                     \
-    if ((r = dalloc(ctx, bd, &p_, (n)))) { delete bd; return r; }        \
-    B.field = p_;                                                         \
-  } while (0)
   AL(seg_base, bd->n_segs, uint32_t);
   AL(rel_step, bd->n_rel_cap, uint32_t);
   AL(rel_set, bd->n_rel_cap, uint32_t);
@@ -506,6 +548,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   AL(n_faults, 1, unsigned long long);
   B.fault_cap = fcap;
 #undef AL
+#undef UP
   ctx->batches.push_back(bd);
   *out = (uint32_t)(ctx->batches.size() - 1);
   return check_error_flag(ctx);
@@ -519,8 +562,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   cudaStream_t s = ctx->stream;
   const uint64_t S = bd->n_stmts;
   // reset run state
-  unsigned long long cnt0[2] = {0, 0};
-  CK(cudaMemcpyAsync(cnt0, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
+  unsigned long long cnt0[8] = {0};
+  CK(cudaMemcpyAsync(cnt0, ctx->counters, 64, cudaMemcpyDeviceToHost, s));
   CK(cudaMemsetAsync(B.seg_base, 0xff, bd->n_segs * 4, s));
   CK(cudaMemsetAsync(B.regfile, 0xff, std::max<uint64_t>(bd->n_regs, 1) * 4, s));
   CK(cudaMemsetAsync(B.st_step, 0xff, S * 4, s));
@@ -544,13 +587,19 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   if (B.n_progs) {
     uint32_t maxT = 0;
     for (const veq_program_meta &m : bd->progs) maxT = std::max(maxT, m.n_threads);
-    // on-chip control state sized to the largest CTA of the batch, so small
-    // CTAs keep many scheduler blocks resident per SM
-    size_t smem = maxT <= SCHED_SMEM_T ? ((size_t)maxT * 9 + 15) / 16 * 16 : 0;
-    B.sched_on_chip = smem > 0 ? maxT : 0;
-    if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute(k_schedule_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    LAUNCH(k_schedule_smem<<<B.n_progs, SCHED_BLOCK, smem, s>>>(B));
+    if (maxT <= 1024) {
+      // one CUDA thread per symbolic thread, control state in registers
+      const uint32_t bt = std::max<uint32_t>(32, (maxT + 31) / 32 * 32);
+      LAUNCH(k_schedule_lanes<<<B.n_progs, bt, 0, s>>>(B));
+    } else {
+      // on-chip control state sized to the largest CTA of the batch, so small
+      // CTAs keep many scheduler blocks resident per SM
+      size_t smem = maxT <= SCHED_SMEM_T ? ((size_t)maxT * 9 + 15) / 16 * 16 : 0;
+      B.sched_on_chip = smem > 0 ? maxT : 0;
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_schedule_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LAUNCH(k_schedule_smem<<<B.n_progs, SCHED_BLOCK, smem, s>>>(B));
+    }
   }
   PH1(VEQ_PH_SCHEDULE);
   CK(cudaGetLastError());
@@ -679,7 +728,16 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       unsigned long long *cursor = nullptr;
       CK(cudaMallocAsync(&cursor, 8, s));
       CK(cudaMemsetAsync(cursor, 0, 8, s));
-      EvalCtx E{log, log_stmt, base};
+      static const bool prof_on = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
+      unsigned long long *prof = nullptr;
+      if (prof_on) {
+        CK(cudaMallocAsync(&prof, 16 * 8, s));
+        CK(cudaMemsetAsync(prof, 0, 16 * 8, s));
+      }
+      EvalCtx E{log, log_stmt, base, prof};
+      uint4 *desc = nullptr;
+      CK(cudaMallocAsync(&desc, n_work * sizeof(uint4), s));
+      LAUNCH(k_make_desc<<<blocks(n_work, 256), 256, 0, s>>>(B, E, wv2, n_work, desc));
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
       // one warp per work item, persistent over the sorted work list;
@@ -695,9 +753,22 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       const uint64_t warps = threads / 32;
       const uint32_t grab = n_work >= warps * 16 ? 4 : (n_work >= warps * 4 ? 2 : 1);
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
-      LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, wv2, n_work, cursor,
+      LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, desc, n_work, cursor,
                                                                                 ctx->pool, ctx->pool_used,
                                                                                 ctx->pool_cap, chunk, grab));
+      CK(cudaFreeAsync(desc, s));
+      if (prof) {
+        unsigned long long hp[16];
+        CK(cudaMemcpyAsync(hp, prof, 16 * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "[veq prof] items %llu warps %llu grab %u | wait %.1f us/item |", (unsigned long long)n_work,
+                (unsigned long long)warps, grab, hp[0] / 1965.0 / std::max<double>(1, n_work));
+        const char *nm[5] = {"other", "lean", "smem", "small", "global"};
+        for (int k = 0; k < 5; k++)
+          if (hp[6 + k]) fprintf(stderr, " %s n=%llu %.2f us", nm[k], hp[6 + k], hp[1 + k] / 1965.0 / hp[6 + k]);
+        fprintf(stderr, "\n");
+        CK(cudaFreeAsync(prof, s));
+      }
       CK(cudaGetLastError());
       CK(cudaFreeAsync(tmp2, s));
       CK(cudaFreeAsync(cursor, s));
@@ -729,8 +800,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaMemcpyAsync(&nf, B.n_faults, 8, cudaMemcpyDeviceToHost, s));
   std::vector<uint32_t> dead(P);
   CK(cudaMemcpyAsync(dead.data(), B.prog_dead, P * 4, cudaMemcpyDeviceToHost, s));
-  unsigned long long nn[2] = {0, 0};
-  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
+  unsigned long long nn[8] = {0};
+  CK(cudaMemcpyAsync(nn, ctx->counters, 64, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   int er = check_error_flag(ctx);
   if (er) return er;
@@ -774,15 +845,16 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     out->thread_state = bd->th_state.data();
     out->thread_block_set = bd->th_bset.data();
     out->thread_block_stmt = bd->th_bstmt.data();
-    out->n_nodes = nn[0];
-    out->n_kid_words = nn[1];
+    out->n_nodes = nn[0] - nn[4];
+    out->n_kid_words = nn[1] - nn[5];
     out->n_work = n_work;
     out->n_access = n_tup;
     uint64_t executed = 0;
     for (uint32_t p = 0; p < P; p++) executed += bd->res[p].steps - bd->res[p].releases;
     out->n_stmts_executed = executed;
-    out->n_new_nodes = nn[0] - cnt0[0];
-    out->n_new_kid_words = nn[1] - cnt0[1];
+    // allocation chunks leave holes (counters[4], [5]); stats count real nodes
+    out->n_new_nodes = (nn[0] - nn[4]) - (cnt0[0] - cnt0[4]);
+    out->n_new_kid_words = (nn[1] - nn[5]) - (cnt0[1] - cnt0[5]);
     out->n_launches = ctx->launches - launches0;
     out->n_phases = VEQ_MAX_PHASES;
     for (int i = 0; i < VEQ_MAX_PHASES; i++) {

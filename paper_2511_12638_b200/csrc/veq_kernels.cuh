@@ -83,6 +83,111 @@ __device__ __forceinline__ void emit_fault(const Batch &B, const veq_fault &f) {
 }
 
 // ---------------------------------------------------------------------------
+// Batch preparation (veq_load_batch): control segments of every thread are
+// cut at its Sync statements, and each Sync gets the canonical id of its set
+// (content-equal sets share one id; a set covering every thread of the CTA
+// is the full set, id = n_syncsets). Control is value-independent
+// (symexec.cpp:764-781), so this needs only the IR.
+struct PrepArgs {
+  uint32_t n_progs, n_threads, n_syncsets, n_arrays_total;
+  uint64_t n_stmts;
+  const veq_program_meta *progs;
+  const uint64_t *thread_stmt;
+  const uint32_t *thread_prog;
+  const veq_stmt *stmts;
+  const veq_syncset *sets;
+  const uint32_t *set_canon;  // pool index -> first pool index with equal content
+  const uint32_t *set_pop;    // members per pool entry
+  unsigned long long *cnt;    // per stmt: is_sync | is_access << 32 (then its exclusive scan)
+  int *error;
+};
+
+__device__ __forceinline__ uint32_t thread_of_stmt(const uint64_t *thread_stmt, uint32_t n_threads, uint64_t i) {
+  uint32_t lo = 0, hi = n_threads;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) / 2;
+    if (thread_stmt[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_prep_thread_prog(PrepArgs A, uint32_t *thread_prog) {
+  const uint32_t p = blockIdx.x;
+  const veq_program_meta m = A.progs[p];
+  for (uint32_t t = threadIdx.x; t < m.n_threads; t += blockDim.x) thread_prog[m.thread_off + t] = p;
+}
+
+// per statement: validation and the (sync, access) counts to scan
+__global__ void k_prep_stmts(PrepArgs A) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n_stmts) return;
+  const veq_stmt st = A.stmts[i];
+  unsigned long long c = 0;
+  if (st.kind > VEQ_ST_SYNC) {
+    atomicCAS(A.error, 0, 1);
+  } else if (st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE) {
+    c = 1ull << 32;
+    const uint32_t t = thread_of_stmt(A.thread_stmt, A.n_threads, i);
+    if (st.arr >= A.progs[A.thread_prog[t]].n_arrays) atomicCAS(A.error, 0, 2);
+  } else if (st.kind == VEQ_ST_SYNC) {
+    c = 1;
+    if (st.a >= A.n_syncsets) atomicCAS(A.error, 0, 3);
+  }
+  A.cnt[i] = c;
+}
+
+// per thread: segment offsets, first segment start, last segment's set
+// (cnt has n_stmts + 1 entries after the scan: cnt[n_stmts] is the total)
+__global__ void k_prep_threads(PrepArgs A, uint64_t *seg_off, uint64_t *seg_start, uint32_t *seg_set) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > A.n_threads) return;
+  auto syncs_before = [&](uint64_t i) -> uint64_t { return A.cnt[i] & 0xffffffffull; };
+  const uint64_t so = t + syncs_before(A.thread_stmt[t]);
+  seg_off[t] = so;
+  if (t == A.n_threads) return;
+  seg_start[so] = A.thread_stmt[t];
+  const uint64_t nsync = syncs_before(A.thread_stmt[t + 1]) - syncs_before(A.thread_stmt[t]);
+  seg_set[so + nsync] = UNSET;  // the last segment ends the thread, not at a sync
+}
+
+// per Sync statement: canonical set id of the segment it ends, next start
+__global__ void k_prep_syncs(PrepArgs A, uint64_t *seg_start, uint32_t *seg_set) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n_stmts) return;
+  const veq_stmt st = A.stmts[i];
+  if (st.kind != VEQ_ST_SYNC || st.a >= A.n_syncsets) return;
+  const uint32_t t = thread_of_stmt(A.thread_stmt, A.n_threads, i);
+  const uint32_t p = A.thread_prog[t];
+  const uint64_t j = t + (A.cnt[i] & 0xffffffffull);
+  const bool full = A.sets[st.a].full || A.set_pop[st.a] == A.progs[p].n_threads;
+  seg_set[j] = full ? A.n_syncsets : A.set_canon[st.a];
+  seg_start[j + 1] = i + 1;
+}
+
+// per program: sync count (release capacity) for the rel_off scan
+__global__ void k_prep_progs(PrepArgs A, uint64_t *prog_sync, uint32_t *prog_full) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.n_progs) return;
+  const veq_program_meta m = A.progs[p];
+  auto syncs_before = [&](uint64_t i) -> uint64_t { return A.cnt[i] & 0xffffffffull; };
+  prog_sync[p] = syncs_before(A.thread_stmt[m.thread_off + m.n_threads]) - syncs_before(A.thread_stmt[m.thread_off]);
+  prog_full[p] = A.n_syncsets;
+}
+
+// threads with >= EXEC_WARP_MIN statements (they run on k_exec_warp)
+__global__ void k_prep_long(PrepArgs A, uint32_t *longs, unsigned long long *n_long, uint64_t min_len) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.n_threads) return;
+  if (A.thread_stmt[t + 1] - A.thread_stmt[t] >= min_len) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(n_long, (unsigned long long)g.size());
+    longs[g.shfl(base, 0) + g.thread_rank()] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K0: schedule. One block per program, symbolic threads in contiguous chunks
 // per CUDA thread so an ordered block scan gives round-robin step offsets.
 constexpr int SCHED_BLOCK = 256;
@@ -245,7 +350,9 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
         if (skip) continue;
       }
       if (ok) {
-        unsigned long long key = ((unsigned long long)mn << 32) | I;
+        // releasable_syncs order (symexec.cpp:616-654): smallest min tid,
+        // ties in discovery order = smallest blocked member (t checks I)
+        unsigned long long key = ((unsigned long long)mn << 32) | t;
         best = key < best ? key : best;
       }
     }
@@ -253,7 +360,7 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
     __syncthreads();
     const unsigned long long sb = s_best;
     if (sb != ~0ull) {
-      const uint32_t I = (uint32_t)(sb & 0xffffffffu);
+      const uint32_t I = bs[(uint32_t)(sb & 0xffffffffu)];
       uint32_t c = 0;
       for (uint32_t t = lo; t < hi; t++) {
         if (st[t] != TS_BLOCK || bs[t] != I) continue;
@@ -291,6 +398,172 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
     B.prog_nrel[p] = s_nrel;
     B.prog_steps[p] = s_step;
     B.prog_dead[p] = s_ret != T;
+  }
+}
+
+// K0 for CTAs of at most 1024 threads: one CUDA thread per symbolic thread,
+// control state in registers. A round is one block scan of the runnable
+// threads' segment lengths (their step numbers) plus one release decision.
+// Sets inside one 32-thread window are decided with warp votes: the lanes
+// blocked on I are a __match_any_sync group, and I is releasable iff its
+// members are all in that group or returned (releasable_syncs,
+// symexec.cpp:616-654). The full set uses block counts; any other set is
+// checked member by member from shared memory.
+constexpr uint32_t TS_NONE = 3;  // lane beyond the CTA's thread count
+__global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
+  __shared__ uint8_t s_st[1024];
+  __shared__ uint32_t s_bs[1024];
+  __shared__ unsigned long long s_scan[33];
+  __shared__ unsigned long long s_best;
+  __shared__ uint32_t s_blkfull;
+  const uint32_t p = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  const veq_program_meta pm = B.progs[p];
+  const uint32_t T = pm.n_threads, full = B.prog_full_set[p];
+  const uint32_t g = pm.thread_off + t;
+  uint8_t st = TS_NONE;
+  uint32_t bset = UNSET;
+  uint64_t sj = 0, sj_end = 0, s_end = 0, cur_start = 0, next_start = 0;
+  if (t < T) {
+    sj = B.seg_off[g];
+    sj_end = B.seg_off[g + 1];
+    s_end = B.thread_stmt[g + 1];
+    cur_start = B.seg_start[sj];
+    next_start = sj + 1 < sj_end ? B.seg_start[sj + 1] : s_end;
+    st = cur_start == s_end ? TS_RET : TS_RUN;
+  }
+  s_st[t] = st;
+  s_bs[t] = UNSET;
+  unsigned long long step = 0;
+  uint32_t nrel = 0;
+  uint32_t ret_count = __syncthreads_count(st == TS_RET);
+  while (ret_count != T) {
+    // ---- run phase: every runnable thread executes its current segment;
+    // an ordered block scan of the lengths gives round-robin step numbers
+    const unsigned long long len = st == TS_RUN ? next_start - cur_start : 0;
+    unsigned long long x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(kFull, x, o);
+      if (lane >= (unsigned)o) x += y;
+    }
+    if (lane == 31) s_scan[wid] = x;
+    if (t == 0) {
+      s_best = ~0ull;
+      s_blkfull = 0;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const unsigned long long v = lane < nw ? s_scan[lane] : 0;
+      unsigned long long z = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(kFull, z, o);
+        if (lane >= (unsigned)o) z += y;
+      }
+      if (lane < nw) s_scan[lane] = z - v;
+      if (lane == 31) s_scan[32] = z;
+    }
+    __syncthreads();
+    const unsigned long long total = s_scan[32];
+    if (st == TS_RUN) {
+      B.seg_base[sj] = (uint32_t)(step + s_scan[wid] + x - len);
+      if (sj + 1 >= sj_end) {
+        st = TS_RET;
+      } else {
+        st = TS_BLOCK;
+        bset = B.seg_set[sj];
+        s_bs[t] = bset;
+      }
+      s_st[t] = st;
+    }
+    step += total;
+    {
+      const uint32_t cf = __popc(__ballot_sync(kFull, st == TS_BLOCK && bset == full));
+      if (lane == 0 && cf) atomicAdd(&s_blkfull, cf);
+    }
+    ret_count = __syncthreads_count(st == TS_RET);
+    // ---- release phase: the releasable set with the smallest min tid, ties
+    // in discovery order = smallest blocked member (releasable_syncs)
+    const uint32_t blkd = __ballot_sync(kFull, st == TS_BLOCK);
+    const uint32_t retm = __ballot_sync(kFull, st == TS_RET);
+    if (st == TS_BLOCK) {
+      const uint32_t grp = __match_any_sync(blkd, bset);
+      if ((uint32_t)(__ffs(grp) - 1) == lane) {  // smallest lane blocked on I here
+        bool ok;
+        uint32_t mn, first = t;
+        if (bset == full) {
+          ok = s_blkfull + ret_count == T;
+          mn = 0;
+        } else {
+          const veq_syncset q = B.sets[bset];
+          const uint32_t w0 = wid * 32;
+          if (q.lo >= w0 && q.lo + q.n_bits <= w0 + 32) {
+            // window inside this warp: one vote decides it (members beyond
+            // the CTA are TS_NONE lanes, so they fail the test)
+            const uint64_t bits = B.set_words[q.word_off] & (q.n_bits >= 64 ? ~0ull : ((1ull << q.n_bits) - 1));
+            const uint32_t M = (uint32_t)(bits << (q.lo - w0));
+            ok = M != 0 && (M & ~(grp | retm)) == 0;
+            mn = M ? w0 + __ffs(M) - 1 : q.lo;
+          } else {
+            ok = true;
+            mn = UNSET;
+            for (uint32_t k = 0; k < q.n_bits; k++) {
+              if (!((B.set_words[q.word_off + k / 64] >> (k % 64)) & 1ull)) continue;
+              const uint32_t m = q.lo + k;
+              if (mn == UNSET) mn = m;
+              if (m >= T) {
+                ok = false;
+                break;
+              }
+              const uint8_t sm = s_st[m];
+              if (sm == TS_RET) continue;
+              if (sm == TS_BLOCK && s_bs[m] == bset) {
+                first = m < first ? m : first;
+                continue;
+              }
+              ok = false;
+              break;
+            }
+            if (mn == UNSET) mn = q.lo;
+          }
+        }
+        if (ok) atomicMin(&s_best, ((unsigned long long)mn << 32) | first);
+      }
+    }
+    __syncthreads();
+    const unsigned long long sb = s_best;
+    const bool released = sb != ~0ull;
+    if (released) {
+      const uint32_t I = s_bs[(uint32_t)(sb & 0xffffffffu)];
+      if (st == TS_BLOCK && bset == I) {
+        sj++;
+        cur_start = next_start;
+        next_start = sj + 1 < sj_end ? B.seg_start[sj + 1] : s_end;
+        st = cur_start == s_end ? TS_RET : TS_RUN;
+        s_st[t] = st;
+      }
+      if (t == 0) {
+        const uint64_t r = B.rel_off[p] + nrel;
+        if (r < B.rel_off[p + 1]) {
+          B.rel_step[r] = (uint32_t)step;
+          B.rel_set[r] = I;
+        }
+      }
+      nrel++;
+      step += 1;
+    }
+    ret_count = __syncthreads_count(st == TS_RET);
+    if (total == 0 && !released) break;
+  }
+  if (t < T) {
+    B.th_state[g] = st;
+    B.th_seg[g] = (uint32_t)(sj - B.seg_off[g]);
+    B.th_bset[g] = st == TS_BLOCK ? bset : UNSET;
+  }
+  if (t == 0) {
+    B.prog_nrel[p] = nrel;
+    B.prog_steps[p] = step;
+    B.prog_dead[p] = ret_count != T;
   }
 }
 
@@ -980,6 +1253,7 @@ __device__ __forceinline__ uint32_t wait_node(const Batch &B, uint32_t r) {
 
 struct EvalCtx {
   const uint32_t *log, *log_stmt, *log_base;
+  unsigned long long *prof;  // optional eval profile (VEQ_PROF=1), see veq_api.cu
 };
 
 __device__ inline void arith_fault(const Batch &B, uint32_t stmt, uint8_t detail) {
@@ -1078,14 +1352,36 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
   return intern(T, K_EXP, 0, 0, &a, 1);
 }
 
-// Warp-per-item variant: fused Add chains run warp-cooperatively
+// Work descriptor per sorted item: statement, chain-log base and leaf count
+// (chain Adds), statement kind and op — one 16-byte load replaces the
+// stmts -> chain_head/pos -> log_base chain of dependent reads.
+__global__ void k_make_desc(Batch B, EvalCtx E, const uint32_t *work, uint64_t n_work, uint4 *desc) {
+  uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n_work) return;
+  const uint32_t i = work[w];
+  const veq_stmt st = B.stmts[i];
+  uint4 d{i, 0u, 0u, (uint32_t)st.kind | ((uint32_t)st.op << 8)};
+  if (st.kind == VEQ_ST_BINOP && st.op == VEQ_BIN_ADD) {
+    d.y = E.log_base[B.chain_head[i]];
+    d.z = B.chain_pos[i] + 2;
+  }
+  desc[w] = d;
+}
+
+__device__ __forceinline__ bool desc_is_add(const uint4 &d) {
+  return (d.w & 0xff) == VEQ_ST_BINOP && ((d.w >> 8) & 0xff) == VEQ_BIN_ADD;
+}
+
+// Warp-per-item evaluation: fused Add chains run warp-cooperatively
 // (veq_warp.cuh); every other operation runs on lane 0. Sums of at most 32
 // terms stay in registers; larger ones take pages of the block's shared-
 // memory pool (warp_add_smem); like terms, -inf leaves or an exhausted pool
-// use the global-scratch path (warp_add_nary).
-// 64 registers/thread: 32 resident warps per SM (4 blocks of 8 warps).
-constexpr uint32_t EVAL_BLOCK = 256, EVAL_PAGES = 13;
-__global__ void __launch_bounds__(EVAL_BLOCK, 4) k_eval_warp(Batch B, Table T, EvalCtx E, const uint32_t *work,
+// use the global-scratch path (warp_add_nary). The next item's descriptor
+// and first 32 chain-log entries are loaded while the current one runs.
+// 64 registers/thread: 32 resident warps per SM (2 blocks of 16 warps, each
+// block with a 108 KB page pool).
+constexpr uint32_t EVAL_BLOCK = 512, EVAL_PAGES = 27;
+__global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
                                                              uint64_t n_work, unsigned long long *cursor, char *pool,
                                                              unsigned long long *pool_used, uint64_t pool_cap,
                                                              uint64_t chunk, uint32_t grab) {
@@ -1095,42 +1391,61 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 4) k_eval_warp(Batch B, Table T, E
   __syncthreads();
   const SmemPool SP{&s_mask, eval_smem, EVAL_PAGES};
   Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, chunk, 0};
+  WarpAlloc W{0, 0, 0, 0};
   const uint32_t lane = lane_id();
   // items are claimed `grab` at a time; a warp works through its run in
   // order, and every dependency of an item lies earlier in the sorted list,
   // so progress is guaranteed.
-  unsigned long long w = 0, w_end = 0;
-  for (;;) {
-    if (w == w_end) {
-      if (lane == 0) w = atomicAdd(cursor, (unsigned long long)grab);
-      w = __shfl_sync(kFull, w, 0);
-      w_end = w + grab;
+  // first window: fixed, interleaved across blocks (warp j of block b takes
+  // window j * gridDim + b), so a short work list spreads over every SM and
+  // every block's page pool; later windows come from the shared cursor
+  const uint32_t wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const unsigned long long first_windows = (unsigned long long)gridDim.x * wpb;
+  auto claim = [&]() -> unsigned long long {
+    unsigned long long x = 0;
+    if (lane == 0) x = atomicAdd(cursor, (unsigned long long)grab);
+    return __shfl_sync(kFull, x, 0) + first_windows * grab;
+  };
+  auto fetch = [&](unsigned long long w, uint4 &d, uint32_t &lg) {
+    d = w < n_work ? __ldg(desc + w) : make_uint4(0, 0, 0, 0xff);
+    lg = (w < n_work && desc_is_add(d) && lane < d.z) ? __ldg(E.log + d.y + lane) : UNSET;
+  };
+  unsigned long long prof_wait = 0, prof_work[5] = {0, 0, 0, 0, 0}, prof_n[5] = {0, 0, 0, 0, 0};
+  unsigned long long w = ((unsigned long long)wib * gridDim.x + blockIdx.x) * grab, w_end = w + grab;
+  uint4 d;
+  uint32_t lg;
+  fetch(w, d, lg);
+  while (w < n_work) {
+    unsigned long long wn = w + 1;
+    if (wn == w_end) {
+      wn = claim();
+      w_end = wn + grab;
     }
-    if (w >= n_work) break;
-    const uint32_t i = work[w++];
+    uint4 dn;
+    uint32_t lgn;
+    fetch(wn, dn, lgn);
+    const uint32_t i = d.x;
     const uint64_t mark = A.used;
     char *const mbase = A.base;
     A.item = i;
-    const veq_stmt st = B.stmts[i];
     uint32_t r = UNSET;
-    if (st.kind == VEQ_ST_BINOP && st.op == VEQ_BIN_ADD) {
-      const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
-      const uint32_t b = E.log_base[h], n = pos + 2;
-      // pass 1: operands ready, -inf check; sums of <= 32 terms finish in
-      // registers
-      uint32_t leaf0 = UNSET, m = 0;
-      bool neg = false;
-      for (uint32_t k = lane; k < n; k += 32) {
-        uint32_t x = wait_node(B, E.log[b + k]);
-        if (k < 32) leaf0 = x;
-        neg |= x == T.id_neginf;
-      }
+    bool created = false;
+    int path = 0;  // 0 other, 1 lean, 2 smem, 3 small_reg, 4 global
+    long long t0 = E.prof ? clock64() : 0, t1 = 0;
+    if (desc_is_add(d)) {
+      const uint32_t b = d.y, n = d.z;
+      // operands ready, -inf check; sums of <= 32 terms finish in registers
+      uint32_t leaf0 = lane < n ? wait_node(B, lg) : UNSET, m = 0;
+      bool neg = leaf0 == T.id_neginf;
+      for (uint32_t k = lane + 32; k < n; k += 32) neg |= wait_node(B, E.log[b + k]) == T.id_neginf;
       neg = __any_sync(kFull, neg);
+      if (E.prof) t1 = clock64();
       if (!neg) {
         bool counted = false;
         if (n <= 32) {
-          r = warp_add_lean(T, leaf0, n, m);
+          r = warp_add_lean(T, leaf0, n, m, &W, &created);
           counted = true;
+          path = 1;
         }
         if (r == UNSET && (!counted || m > 32)) {
           if (!counted) {
@@ -1144,14 +1459,17 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 4) k_eval_warp(Batch B, Table T, E
             uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
             for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
             __syncwarp();
-            r = warp_add_smem(T, buf, n, m);
+            r = warp_add_smem(T, buf, n, m, &W);
             pool_release(SP, first, pages);
+            path = 2;
           }
         } else if (r == UNSET && n <= 32) {
           r = warp_add_small_reg(T, leaf0, n);  // like terms / coefficients
+          path = 3;
         }
       }
       if (r == UNSET) {
+        path = 4;
         uint32_t *ids = warp_get<uint32_t>(A, n);
         r = T.id_zero;
         if (ids) {
@@ -1184,8 +1502,30 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 4) k_eval_warp(Batch B, Table T, E
     }
     if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
     if (lane == 0) {
-      fence_acq_rel();
+      // a node this warp created was fenced before its slot was claimed;
+      // anything else needs the fence for cumulativity
+      if (!created) fence_acq_rel();
       atomicExch(B.canon + i, r);
+      if (E.prof) {
+        long long t2 = clock64();
+        if (!t1) t1 = t0;
+        prof_wait += t1 - t0;
+        prof_work[path] += t2 - t1;
+        prof_n[path]++;
+      }
+    }
+    w = wn;
+    d = dn;
+    lg = lgn;
+  }
+  if (lane == 0) {
+    wa_flush(T, W);
+    if (E.prof) {
+      atomicAdd(E.prof, prof_wait);
+      for (int k = 0; k < 5; k++) {
+        atomicAdd(E.prof + 1 + k, prof_work[k]);
+        atomicAdd(E.prof + 6 + k, prof_n[k]);
+      }
     }
   }
 }

@@ -37,6 +37,49 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t &total) 
   return x - v;
 }
 
+// Per-warp bump allocation of node ids and kid words (held by lane 0):
+// chunks come from the table's global counters, so the hot path issues no
+// contended atomic per node. Unused chunk tails are holes, counted in
+// counters[4] (ids) and counters[5] (kid words) when the warp exits.
+struct WarpAlloc {
+  uint64_t id_next, id_end, kid_next, kid_end;
+};
+constexpr uint64_t WA_IDS = 32, WA_KIDS = 2048;
+
+// Lane 0 only. False when the table is full (E_BUDGET set).
+__device__ inline bool wa_alloc(const Table &T, WarpAlloc &W, uint32_t nk, uint64_t &id, uint64_t &off) {
+  if (W.id_next == W.id_end) {
+    unsigned long long b = atomicAdd(&T.counters[0], (unsigned long long)WA_IDS);
+    W.id_next = b;
+    W.id_end = b + WA_IDS;
+  }
+  if (W.kid_next + nk > W.kid_end) {
+    const uint64_t want = nk > WA_KIDS ? nk : WA_KIDS;
+    if (W.kid_end > W.kid_next) atomicAdd(&T.counters[5], (unsigned long long)(W.kid_end - W.kid_next));
+    unsigned long long b = atomicAdd(&T.counters[1], (unsigned long long)want);
+    W.kid_next = b;
+    W.kid_end = b + want;
+  }
+  id = W.id_next++;
+  off = W.kid_next;
+  W.kid_next += nk;
+  if (id >= T.max_nodes || off + nk > T.max_kids) {
+    set_error(T, E_BUDGET);
+    return false;
+  }
+  return true;
+}
+__device__ inline void wa_flush(const Table &T, WarpAlloc &W) {
+  if (W.id_end > W.id_next) atomicAdd(&T.counters[4], (unsigned long long)(W.id_end - W.id_next));
+  if (W.kid_end > W.kid_next) atomicAdd(&T.counters[5], (unsigned long long)(W.kid_end - W.kid_next));
+  W.id_next = W.id_end = W.kid_next = W.kid_end = 0;
+}
+// an id / kid range allocated speculatively and then not published
+__device__ inline void wa_waste(const Table &T, uint32_t nk) {
+  atomicAdd(&T.counters[4], 1ull);
+  atomicAdd(&T.counters[5], (unsigned long long)nk);
+}
+
 // Bitonic sort of n (key, val) pairs held in scratch; capacity must be the
 // next power of two >= n (padding is filled here). less(ka, va, kb, vb).
 template <class Less>
@@ -71,10 +114,12 @@ __device__ inline void warp_bitonic(uint64_t *key, uint32_t *val, uint32_t n, Le
 }
 
 // Insert-or-find of a composite whose kids sit in scratch (all lanes call).
-__device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint32_t *kids, uint32_t nk) {
+__device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint32_t *kids, uint32_t nk,
+                                       WarpAlloc *W = nullptr) {
   const uint32_t lane = lane_id();
   uint64_t sum = 0, p1 = 0;
   bool any_pd = false, all_pd = true, any_div = false, k0c = false;
+#pragma unroll 4
   for (uint32_t i = lane; i < nk; i += 32) {
     Node kn = ld_node(T, kids[i]);
     sum += kid_term(i, kn.hash);
@@ -108,13 +153,18 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
     if (cur == EMPTY) {
       if (mine == EMPTY) {
         unsigned long long id = 0, off = 0;
+        bool ok = true;
         if (lane == 0) {
-          id = atomicAdd(&T.counters[0], 1ull);
-          off = atomicAdd(&T.counters[1], (unsigned long long)nk);
+          if (W) {
+            ok = wa_alloc(T, *W, nk, (uint64_t &)id, (uint64_t &)off);
+          } else {
+            id = atomicAdd(&T.counters[0], 1ull);
+            off = atomicAdd(&T.counters[1], (unsigned long long)nk);
+          }
         }
         id = __shfl_sync(kFull, id, 0);
         off = __shfl_sync(kFull, off, 0);
-        if (id >= T.max_nodes || off + nk > T.max_kids) {
+        if (!__shfl_sync(kFull, ok, 0) || id >= T.max_nodes || off + nk > T.max_kids) {
           if (lane == 0) set_error(T, E_BUDGET);
           return T.id_zero;
         }
@@ -201,7 +251,8 @@ __device__ __forceinline__ void reg_bitonic(uint64_t &key, uint32_t &val, Less l
 }
 
 __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
-                                              bool pd, bool dv, uint64_t p1, bool k0c);
+                                              bool pd, bool dv, uint64_t p1, bool k0c, WarpAlloc *W = nullptr,
+                                              bool *created = nullptr);
 
 // Interns a composite whose kid i is held by lane i (m <= 32 kids).
 __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32_t kid, uint32_t m) {
@@ -224,7 +275,8 @@ __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32
 // Same, with each lane's kid term hash (kid_term(lane, hash)) and flags
 // already known; p1 = composite prefix, k0c = kid 0 is a Const.
 __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
-                                              bool pd, bool dv, uint64_t p1, bool k0c) {
+                                              bool pd, bool dv, uint64_t p1, bool k0c, WarpAlloc *W,
+                                              bool *created) {
   const uint32_t lane = lane_id();
   if (lane >= m) {
     term = 0;
@@ -238,14 +290,41 @@ __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint
   const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
   uint64_t slot = h & T.slot_mask;
   uint32_t mine = EMPTY;
+  if (W) {
+    // speculative insert: write the node first, then claim the home slot
+    // directly (one round trip fewer for the common new-node case)
+    unsigned long long id = 0, off = 0;
+    bool ok = true;
+    if (lane == 0) ok = wa_alloc(T, *W, m, (uint64_t &)id, (uint64_t &)off);
+    if (!__shfl_sync(kFull, ok, 0)) return T.id_zero;
+    id = __shfl_sync(kFull, id, 0);
+    off = __shfl_sync(kFull, off, 0);
+    if (lane < m) T.kids[off + lane] = kid;
+    if (lane == 0) {
+      Node n;
+      n.kind = kind;
+      n.flags = flags;
+      n.pad = 0;
+      n.nkids = m;
+      n.hash = h;
+      n.p0 = off;
+      n.p1 = p1;
+      T.nodes[id] = n;
+    }
+    __syncwarp();
+    fence_acq_rel();
+    mine = (uint32_t)id;
+  }
   for (uint64_t probes = 0;; probes++) {
     if (probes > T.slot_mask) {
       if (lane == 0) set_error(T, E_BUDGET);
       return T.id_zero;
     }
-    uint32_t cur = 0;
-    if (lane == 0) cur = *((volatile uint32_t *)(T.slots + slot));
-    cur = __shfl_sync(kFull, cur, 0);
+    uint32_t cur = EMPTY;
+    if (mine == EMPTY) {
+      if (lane == 0) cur = *((volatile uint32_t *)(T.slots + slot));
+      cur = __shfl_sync(kFull, cur, 0);
+    }
     if (cur == EMPTY) {
       if (mine == EMPTY) {
         unsigned long long id = 0, off = 0;
@@ -278,14 +357,20 @@ __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint
       uint32_t prev = 0;
       if (lane == 0) prev = atomicCAS(T.slots + slot, EMPTY, mine);
       prev = __shfl_sync(kFull, prev, 0);
-      if (prev == EMPTY) return mine;
+      if (prev == EMPTY) {
+        if (created) *created = true;
+        return mine;
+      }
       cur = prev;
     }
     Node c = ld_node(T, cur);
     bool same = c.hash == h && c.kind == kind && c.nkids == m;
     if (__all_sync(kFull, same)) {
       bool eq = lane >= m || ld_kid(T, c.p0 + lane) == kid;
-      if (__all_sync(kFull, eq)) return cur;
+      if (__all_sync(kFull, eq)) {
+        if (W && lane == 0) wa_waste(T, m);
+        return cur;
+      }
     }
     slot = (slot + 1) & T.slot_mask;
   }
@@ -422,7 +507,8 @@ __device__ __forceinline__ void reg_bitonic3(uint64_t &key, uint32_t &val, uint3
 // Returns UNSET when the path does not apply: more than 32 terms (`m_out`
 // then holds the term count), a term with a coefficient (F_COEF: like terms
 // need factor-vector grouping), or like terms (equal ids after the sort).
-__device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t n, uint32_t &m_out) {
+__device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t n, uint32_t &m_out, WarpAlloc *W,
+                                       bool *created) {
   const uint32_t lane = lane_id();
   uint32_t c = 0, kind = 0;
   uint64_t p0 = 0;
@@ -501,7 +587,7 @@ __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t
   const uint64_t k0p = __shfl_sync(kFull, key, 0);
   const bool k0c = __shfl_sync(kFull, (uint32_t)(key == 0), 0);
   return warp_intern_regs_h(T, K_ADD, id, real, kid_term(lane, kh), kf & F_POSDEF, (kf & F_HASDIV) != 0,
-                            composite_prefix(K_ADD, real, k0p), k0c);
+                            composite_prefix(K_ADD, real, k0p), k0c, W, created);
 }
 
 // ---- shared-memory path for large sums -------------------------------------
@@ -567,7 +653,7 @@ __device__ __forceinline__ bool pref_less(const Table &T, uint64_t pa, uint32_t 
 // the result's kids are the terms themselves plus at most one folded Const,
 // and canonical order (Expr::compare) is produced by merging the leaves'
 // already-sorted kid runs with warp-parallel merge-path passes.
-__device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint32_t m) {
+__device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint32_t m, WarpAlloc *W) {
   const uint32_t lane = lane_id();
   uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
   uint32_t *rs = lv + n;  // run starts = leaf term offsets, n + 1 entries
@@ -578,10 +664,17 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   uint64_t *preB = reinterpret_cast<uint64_t *>(Y);
   uint32_t *idB = reinterpret_cast<uint32_t *>(preB + m);
   // 1. term offsets per leaf
+  // (an Add leaf's slot in lv is replaced by its kid-arena offset: the
+  // gather below then reads kid words without reloading the node)
   uint32_t run = 0;
   for (uint32_t base = 0; base < n; base += 32) {
     uint32_t i = base + lane;
-    uint32_t c = i < n ? n_terms_of(T, lv[i]) : 0;
+    uint32_t c = 0;
+    if (i < n) {
+      const Node ln = ld_node(T, lv[i]);
+      c = ln.kind == K_ADD ? ln.nkids : 1;
+      if (ln.kind == K_ADD) lv[i] = (uint32_t)ln.p0;
+    }
     uint32_t tot;
     uint32_t ex = warp_excl_scan(c, tot);
     if (i < n) rs[i] = run + ex;
@@ -589,9 +682,12 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   }
   if (lane == 0) rs[n] = run;
   __syncwarp();
-  // 2. gather terms and their order prefixes; note coefficient terms
+  // 2. gather terms and their order prefixes; note coefficient terms.
+  // Two passes so each lane keeps several independent loads in flight:
+  // term ids (kid words of Add leaves), then the term nodes.
   bool coef = false;
   uint32_t nconst = 0;
+#pragma unroll 4
   for (uint32_t t = lane; t < m; t += 32) {
     uint32_t lo = 0, hi = n;
     while (hi - lo > 1) {
@@ -599,11 +695,15 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
       if (rs[mid] <= t) lo = mid;
       else hi = mid;
     }
-    uint32_t leaf = lv[lo];
-    Node ln = ld_node(T, leaf);
-    uint32_t id = ln.kind == K_ADD ? ld_kid(T, ln.p0 + (t - rs[lo])) : leaf;
-    Node tn = ln.kind == K_ADD ? ld_node(T, id) : ln;
-    idA[t] = id;
+    // a leaf with several terms is an Add (lv holds its kid offset); a
+    // canonical Add has at least two kids, so a one-term leaf is the term
+    const uint32_t nl = rs[lo + 1] - rs[lo];
+    idA[t] = nl > 1 ? ld_kid(T, (uint64_t)lv[lo] + (t - rs[lo])) : lv[lo];
+  }
+  __syncwarp();
+#pragma unroll 4
+  for (uint32_t t = lane; t < m; t += 32) {
+    const Node tn = ld_node(T, idA[t]);
     preA[t] = prefix_of(tn);
     nconst += tn.kind == K_CONST;
     coef |= tn.kind == K_MUL && (tn.flags & F_COEF);
@@ -725,7 +825,7 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   const uint32_t nout = m - first;
   if (nout == 0) return T.id_zero;
   if (nout == 1) return is[first];
-  return warp_intern(T, K_ADD, is + first, nout);
+  return warp_intern(T, K_ADD, is + first, nout, W);
 }
 
 // canon_add_kids over n canonical leaves (scratch), warp-cooperative.

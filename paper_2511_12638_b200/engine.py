@@ -224,6 +224,8 @@ def render(nodes, kids, roots: List[int], inputs: Sequence[Tuple[str, int]]) -> 
 
 
 def _set_tids(b: Batch, s: int, n_threads: int) -> List[int]:
+    if s >= len(b.syncsets):  # the device's full-set id (veq.h: n_syncsets)
+        return list(range(n_threads))
     q = b.syncsets[s]
     if q["full"]:
         return list(range(n_threads))
