@@ -766,6 +766,9 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
         const char *nm[5] = {"other", "lean", "smem", "small", "global"};
         for (int k = 0; k < 5; k++)
           if (hp[6 + k]) fprintf(stderr, " %s n=%llu %.2f us", nm[k], hp[6 + k], hp[1 + k] / 1965.0 / hp[6 + k]);
+        if (hp[7])
+          fprintf(stderr, " | lean phases: loads %.2f sort %.2f intern %.2f us", hp[11] / 1965.0 / hp[7],
+                  hp[12] / 1965.0 / hp[7], hp[13] / 1965.0 / hp[7]);
         fprintf(stderr, "\n");
         CK(cudaFreeAsync(prof, s));
       }

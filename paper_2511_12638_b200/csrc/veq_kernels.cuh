@@ -1410,7 +1410,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
     d = w < n_work ? __ldg(desc + w) : make_uint4(0, 0, 0, 0xff);
     lg = (w < n_work && desc_is_add(d) && lane < d.z) ? __ldg(E.log + d.y + lane) : UNSET;
   };
-  unsigned long long prof_wait = 0, prof_work[5] = {0, 0, 0, 0, 0}, prof_n[5] = {0, 0, 0, 0, 0};
+  unsigned long long prof_wait = 0, prof_work[5] = {0, 0, 0, 0, 0}, prof_n[5] = {0, 0, 0, 0, 0}, prof_lean[3] = {0, 0, 0};
   unsigned long long w = ((unsigned long long)wib * gridDim.x + blockIdx.x) * grab, w_end = w + grab;
   uint4 d;
   uint32_t lg;
@@ -1443,7 +1443,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
       if (!neg) {
         bool counted = false;
         if (n <= 32) {
-          r = warp_add_lean(T, leaf0, n, m, &W, &created);
+          r = warp_add_lean(T, leaf0, n, m, &W, &created, E.prof ? prof_lean : nullptr);
           counted = true;
           path = 1;
         }
@@ -1526,6 +1526,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
         atomicAdd(E.prof + 1 + k, prof_work[k]);
         atomicAdd(E.prof + 6 + k, prof_n[k]);
       }
+      for (int k = 0; k < 3; k++) atomicAdd(E.prof + 11 + k, prof_lean[k]);
     }
   }
 }

@@ -479,6 +479,24 @@ __device__ inline uint32_t warp_add_small_reg(const Table &T, uint32_t leaf_reg,
 }
 
 
+// Register bitonic over a 64-bit key with a 32-bit payload, plain unsigned
+// key order (ties keep an arbitrary order; callers detect them).
+__device__ __forceinline__ void reg_bitonic_u64(uint64_t &key, uint32_t &val) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t pk = __shfl_xor_sync(kFull, key, j);
+      const uint32_t pv = __shfl_xor_sync(kFull, val, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      const bool take = (up == lower) ? (pk < key) : (key < pk);
+      key = take ? pk : key;
+      val = take ? pv : val;
+    }
+  }
+}
+
 // Register bitonic over (key, id) carrying one extra payload lane index.
 template <class Less>
 __device__ __forceinline__ void reg_bitonic3(uint64_t &key, uint32_t &val, uint32_t &aux, Less less) {
@@ -508,8 +526,9 @@ __device__ __forceinline__ void reg_bitonic3(uint64_t &key, uint32_t &val, uint3
 // then holds the term count), a term with a coefficient (F_COEF: like terms
 // need factor-vector grouping), or like terms (equal ids after the sort).
 __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t n, uint32_t &m_out, WarpAlloc *W,
-                                       bool *created) {
+                                       bool *created, unsigned long long *ph = nullptr) {
   const uint32_t lane = lane_id();
+  long long c0 = ph ? clock64() : 0;
   uint32_t c = 0, kind = 0;
   uint64_t p0 = 0;
   if (lane < n) {
@@ -543,6 +562,7 @@ __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t
     if (tk == K_CONST) cv = const_val(tn);
   }
   if (__any_sync(kFull, lane < m && tk == K_MUL && (fl & F_COEF))) return UNSET;
+  long long c1 = ph ? clock64() : 0;
   // fold the Const terms into one (dropped when zero)
   const uint32_t cmask = __ballot_sync(kFull, lane < m && tk == K_CONST);
   if (cmask) {
@@ -574,9 +594,25 @@ __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t
       }
     }
   }
+  // canonical order: bitonic on the 64-bit order prefix with the source
+  // lane as payload (branch-free); equal prefixes need Expr::compare, so a
+  // tie re-sorts with the full comparator
+  const uint32_t real = __popc(__ballot_sync(kFull, id != UNSET));  // real terms sort first
   uint32_t aux = lane;
-  reg_bitonic3(key, id, aux, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) { return canon_less(T, ka, va, kb, vb); });
-  const uint32_t real = __popc(__ballot_sync(kFull, id != UNSET));
+  reg_bitonic_u64(key, aux);
+  {
+    const uint64_t pk = __shfl_up_sync(kFull, key, 1);
+    if (__any_sync(kFull, lane > 0 && lane < real && key == pk)) {
+      id = __shfl_sync(kFull, id, aux & 31);
+      uint32_t a2 = aux;
+      reg_bitonic3(key, id, a2, [&](uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+        return canon_less(T, ka, va, kb, vb);
+      });
+      aux = a2;
+    } else {
+      id = __shfl_sync(kFull, id, aux & 31);
+    }
+  }
   // like terms (coefficient-free): equal ids, adjacent after the sort
   const uint32_t prev = __shfl_up_sync(kFull, id, 1);
   if (__any_sync(kFull, lane > 0 && lane < real && id == prev)) return UNSET;
@@ -586,8 +622,16 @@ __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t
   const uint8_t kf = (uint8_t)__shfl_sync(kFull, (uint32_t)fl, aux & 31);
   const uint64_t k0p = __shfl_sync(kFull, key, 0);
   const bool k0c = __shfl_sync(kFull, (uint32_t)(key == 0), 0);
-  return warp_intern_regs_h(T, K_ADD, id, real, kid_term(lane, kh), kf & F_POSDEF, (kf & F_HASDIV) != 0,
-                            composite_prefix(K_ADD, real, k0p), k0c, W, created);
+  long long c2 = ph ? clock64() : 0;
+  const uint32_t res = warp_intern_regs_h(T, K_ADD, id, real, kid_term(lane, kh), kf & F_POSDEF, (kf & F_HASDIV) != 0,
+                                          composite_prefix(K_ADD, real, k0p), k0c, W, created);
+  if (ph && lane == 0) {
+    long long c3 = clock64();
+    ph[0] += c1 - c0;
+    ph[1] += c2 - c1;
+    ph[2] += c3 - c2;
+  }
+  return res;
 }
 
 // ---- shared-memory path for large sums -------------------------------------
