@@ -40,6 +40,7 @@ struct BatchDev {
   std::vector<uint64_t> thread_stmt;
   uint64_t n_stmts = 0, n_cells = 0, n_segs = 0, n_rel_cap = 0, n_regs = 0, n_access_max = 0;
   uint32_t n_threads = 0;
+  unsigned int sched_flags = 0;  // written by k_prep_syncs (valid after the load's final sync)
   // device arrays (owned)
   std::vector<void *> owned;
   veq_rat *dconsts = nullptr;
@@ -70,6 +71,8 @@ struct veq_ctx {
   unsigned long long *dbg = nullptr;
   uint32_t *session_ids = nullptr;
   uint64_t *in_base = nullptr, *in_size = nullptr;
+  uint32_t *in_cache = nullptr;
+  uint64_t in_cache_n = 0, in_cells = 0;
   uint64_t n_slots = 0;
   // scratch pool
   char *pool = nullptr;
@@ -232,6 +235,7 @@ void veq_close(veq_ctx *ctx) {
   cudaFree(ctx->pool_used);
   cudaFree(ctx->in_base);
   cudaFree(ctx->in_size);
+  cudaFree(ctx->in_cache);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -274,6 +278,15 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
   if (acc >= (1ull << 43)) return fail(ctx, VEQ_E_UNSUPPORTED, "too many input symbols");
   cudaFree(ctx->in_base);
   cudaFree(ctx->in_size);
+  // input-symbol cache (dense rank -> node id), kept across sessions when
+  // large enough; inputs beyond 2^28 symbols go uncached
+  ctx->in_cells = acc;
+  if (acc <= (1ull << 28) && acc > ctx->in_cache_n) {
+    cudaFree(ctx->in_cache);
+    ctx->in_cache = nullptr;
+    ctx->in_cache_n = 0;
+    if (cudaMalloc(&ctx->in_cache, std::max<uint64_t>(acc, 1) * 4) == cudaSuccess) ctx->in_cache_n = acc;
+  }
   CK(cudaMalloc(&ctx->in_base, base.size() * 8));
   CK(cudaMalloc(&ctx->in_size, size.size() * 8));
   CK(cudaMemcpyAsync(ctx->in_base, base.data(), base.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -282,6 +295,7 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
   T.in_base = ctx->in_base;
   T.in_size = ctx->in_size;
   T.n_inputs = n;
+  T.in_cache = (acc <= ctx->in_cache_n && acc) ? ctx->in_cache : nullptr;
   int r = veq_clear_terms(ctx);
   if (r) return r;
   CK(cudaStreamSynchronize(ctx->stream));
@@ -296,6 +310,7 @@ int veq_clear_terms(veq_ctx *ctx) {
   CK(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dbg, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  if (T.in_cache) CK(cudaMemsetAsync(T.in_cache, 0xff, ctx->in_cells * 4, ctx->stream));
   // a single thread interns -inf, 0, 1, -1 first into an empty table, so
   // their ids are 0..3 without a host round trip
   k_session_init<<<1, 32, 0, ctx->stream>>>(T, ctx->session_ids);
@@ -404,6 +419,30 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   bd->arr_cell_base = cell_base;
   bd->n_cells = cells;
   bd->n_regs = reg_off[Tn];
+  // programs laid out in order (thread and statement ranges contiguous)
+  // allow a statement -> program search over P+1 boundaries
+  std::vector<uint64_t> prog_stmt(P + 1, 0);
+  bool in_order = true;
+  for (uint32_t p = 0; p < P; p++) {
+    const veq_program_meta &m = d->progs[p];
+    if (p + 1 < P && d->progs[p + 1].thread_off != m.thread_off + m.n_threads) in_order = false;
+    prog_stmt[p] = d->thread_stmt[m.thread_off];
+  }
+  if (P) prog_stmt[P] = d->thread_stmt[d->progs[P - 1].thread_off + d->progs[P - 1].n_threads];
+  // sort-key field widths: steps of a program are at most its statements
+  // plus its releases (<= statements), programs < P
+  {
+    uint64_t maxps = 0;
+    for (uint32_t p = 0; p < P; p++) {
+      const veq_program_meta &m = d->progs[p];
+      maxps = std::max<uint64_t>(maxps, d->thread_stmt[m.thread_off + m.n_threads] - d->thread_stmt[m.thread_off]);
+    }
+    uint32_t sb = 1, pb = 1;
+    while ((1ull << sb) < 2 * maxps + 2 && sb < 32) sb++;
+    while ((1ull << pb) < (uint64_t)P + 1 && pb < 20) pb++;
+    bd->B.step_bits = sb;
+    bd->B.prog_bits = pb;
+  }
   // ---- upload
   Batch &B = bd->B;
   B.n_progs = P;
@@ -432,6 +471,8 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   UP(sets, sets.data(), sets.size(), veq_syncset);
   UP(set_words, d->set_words, d->n_set_words, uint64_t);
   UP(reg_off, reg_off.data(), Tn + 1, uint64_t);
+  if (in_order && P) UP(prog_stmt, prog_stmt.data(), P + 1, uint64_t);
+  else B.prog_stmt = nullptr;
   AL(thread_prog, Tn, uint32_t);
   AL(prog_full_set, P, uint32_t);
   // ---- device preparation
@@ -445,8 +486,14 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     return r;
   }
   B.long_threads = d_long;
+  unsigned int *d_flags = nullptr;
+  if ((r = dalloc(ctx, nullptr, &d_flags, 1))) {
+    delete bd;
+    return r;
+  }
+  CK(cudaMemsetAsync(d_flags, 0, 4, s));
   PrepArgs PA{P, Tn, NS, d->n_arrays_total, S, B.progs, B.thread_stmt, B.thread_prog, B.stmts, B.sets, d_canon, d_pop,
-              d_cnt, ctx->error};
+              d_cnt, ctx->error, B.set_words, d_flags};
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), s));
   CK(cudaMemsetAsync(d_cnt + S, 0, 8, s));
   CK(cudaMemsetAsync(d_nlong, 0, 8, s));
@@ -504,6 +551,8 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     CK(cudaMemsetAsync((void *)B.rel_off, 0, 8, s));
   }
   CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&bd->sched_flags, d_flags, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d_flags, s));
   CK(cudaFreeAsync(d_canon, s));
   CK(cudaFreeAsync(d_pop, s));
   CK(cudaFreeAsync(d_cnt, s));
@@ -587,7 +636,12 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   if (B.n_progs) {
     uint32_t maxT = 0;
     for (const veq_program_meta &m : bd->progs) maxT = std::max(maxT, m.n_threads);
-    if (maxT <= 1024) {
+    if (maxT <= 1024 && !(bd->sched_flags & 1u)) {
+      // one warp per CTA, chunked round-robin emulation
+      const size_t smem = SW_WARPS * sizeof(SchedWarpSmem);
+      CK(cudaFuncSetAttribute(k_schedule_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      LAUNCH(k_schedule_warp<<<blocks(B.n_progs, SW_WARPS), SW_WARPS * 32, smem, s>>>(B));
+    } else if (maxT <= 1024) {
       // one CUDA thread per symbolic thread, control state in registers
       const uint32_t bt = std::max<uint32_t>(32, (maxT + 31) / 32 * 32);
       LAUNCH(k_schedule_lanes<<<B.n_progs, bt, 0, s>>>(B));
@@ -603,8 +657,9 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   }
   PH1(VEQ_PH_SCHEDULE);
   CK(cudaGetLastError());
-  // K3
+  // K3 (direct input loads are interned first, in parallel)
   PH0(VEQ_PH_EXEC);
+  if (S) LAUNCH(k_pre_inputs<<<blocks(S, 256), 256, 0, s>>>(B, ctx->T));
   // short threads: one CUDA thread each; long threads: one warp each
   if (B.n_threads) LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
   if (B.n_long) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_long * 32, 128), 128, 0, s>>>(B, ctx->T));
@@ -627,7 +682,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMallocAsync(&rs, n_tup * sizeof(Reader), s));
     int cb = 1;
     while ((1ull << cb) < bd->n_cells + 1) cb++;
-    int end_bit = 32 + cb;
+    int end_bit = (int)B.step_bits + cb;
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
     void *tmp = nullptr;
@@ -635,7 +690,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
     ctx->launches += (end_bit + 7) / 8 + 1;
     CK(cudaMemsetAsync(n_starts, 0, 8, s));
-    LAUNCH(k_seg_heads<<<blocks(n_tup, 256), 256, 0, s>>>(k2, n_tup, starts, n_starts));
+    LAUNCH(k_seg_heads<<<blocks(n_tup, 256), 256, 0, s>>>(k2, n_tup, starts, n_starts, B.step_bits));
     PH1(VEQ_PH_SORT);
     unsigned long long nseg = 0;
     CK(cudaMemcpyAsync(&nseg, n_starts, 8, cudaMemcpyDeviceToHost, s));
@@ -655,24 +710,22 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     PH0(VEQ_PH_MEMSCAN);
     PH1(VEQ_PH_MEMSCAN);
   }
-  // resolve loads, then operands, then count uses (incl. final cells)
+  // resolve operands through loads, count uses (incl. final cells), size
+  // the chain logs — one pass over the statements
+  uint32_t *sz = nullptr, *base = nullptr, *log = nullptr, *log_stmt = nullptr;
+  unsigned long long n_work = 0;
   PH0(VEQ_PH_RESOLVE);
   if (S) {
-    LAUNCH(k_resolve_loads<<<blocks(S, 256), 256, 0, s>>>(B));
-    LAUNCH(k_resolve<<<blocks(S, 256), 256, 0, s>>>(B));
-    LAUNCH(k_count_uses<<<blocks(S, 256), 256, 0, s>>>(B));
+    CK(cudaMallocAsync(&sz, S * 4, s));
+    CK(cudaMallocAsync(&base, S * 4, s));
+    LAUNCH(k_resolve_all<<<blocks(S, 256), 256, 0, s>>>(B, sz));
   }
   if (bd->n_cells) LAUNCH(k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
   PH1(VEQ_PH_RESOLVE);
   CK(cudaGetLastError());
   // chain logs
-  uint32_t *sz = nullptr, *base = nullptr, *log = nullptr, *log_stmt = nullptr;
-  unsigned long long n_work = 0;
   if (S) {
     PH0(VEQ_PH_CHAINS);
-    CK(cudaMallocAsync(&sz, S * 4, s));
-    CK(cudaMallocAsync(&base, S * 4, s));
-    LAUNCH(k_chain_sizes<<<blocks(S, 256), 256, 0, s>>>(B, sz));
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, base, (int64_t)S, s);
     void *tmp = nullptr;
@@ -686,10 +739,10 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     uint64_t nlog = (uint64_t)last_sz + last_base;
     CK(cudaMallocAsync(&log, std::max<uint64_t>(nlog, 1) * 4, s));
     CK(cudaMallocAsync(&log_stmt, std::max<uint64_t>(nlog, 1) * 4, s));
-    LAUNCH(k_chain_scatter<<<blocks(S, 256), 256, 0, s>>>(B, base, log, log_stmt));
     CK(cudaFreeAsync(tmp, s));
     PH1(VEQ_PH_CHAINS);
-    // work list sorted by (program, step)
+    // chain-log entries and the work list, one pass; work sorted by
+    // (step, program)
     PH0(VEQ_PH_WORKLIST);
     unsigned long long *wk = nullptr, *wk2 = nullptr, *nw = nullptr;
     uint32_t *wv = nullptr, *wv2 = nullptr;
@@ -699,23 +752,13 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMallocAsync(&wv2, S * 4, s));
     CK(cudaMallocAsync(&nw, 8, s));
     CK(cudaMemsetAsync(nw, 0, 8, s));
-    LAUNCH(k_make_work<<<blocks(S, 256), 256, 0, s>>>(B, wk, wv, nw));
+    LAUNCH(k_scatter_work<<<blocks(S, 256), 256, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
     CK(cudaMemcpyAsync(&n_work, nw, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     void *tmp2 = nullptr;
     if (n_work) {
-      // key = step << 20 | program; sort only the bits in use (steps of a
-      // program are bounded by its statements plus releases)
-      uint64_t max_step = 0;
-      for (uint32_t p = 0; p < B.n_progs; p++) {
-        const veq_program_meta &m = bd->progs[p];
-        uint64_t st = bd->thread_stmt[m.thread_off + m.n_threads] - bd->thread_stmt[m.thread_off];
-        max_step = std::max<uint64_t>(max_step, st);
-      }
-      max_step += bd->n_rel_cap;
-      int sb = 1;
-      while ((1ull << sb) < max_step + 1 && sb < 44) sb++;
-      const int end_bit = 20 + sb;
+      // key = step << prog_bits | program: sort only the bits in use
+      const int end_bit = (int)(B.prog_bits + B.step_bits);
       size_t tb2 = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, end_bit, s);
       CK(cudaMallocAsync(&tmp2, tb2, s));

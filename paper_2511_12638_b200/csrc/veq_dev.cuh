@@ -53,6 +53,7 @@ struct Table {
   const uint64_t *in_base;  // per declared input: first dense rank of its group
   const uint64_t *in_size;
   uint32_t n_inputs;
+  uint32_t *in_cache;       // node id per input symbol (dense rank), UNSET = not yet interned
 };
 
 __device__ __forceinline__ void set_error(const Table &T, int code) { atomicCAS(T.error, 0, code); }
@@ -383,9 +384,18 @@ __device__ inline uint64_t lexrank(uint64_t i, uint64_t n) {
   return count;
 }
 
+// Input symbols are interned once per term table: a per-symbol cache (reset
+// with the table) turns every later load of the same cell into one read.
 __device__ __forceinline__ uint32_t intern_input_var(const Table &T, uint32_t input, uint64_t cell) {
+  const uint64_t ci = T.in_base[input] + cell;  // dense and injective (cell < size)
+  if (T.in_cache) {
+    const uint32_t v = __ldcg(T.in_cache + ci);
+    if (v != UNSET) return v;
+  }
   uint64_t key = INPUT_KEY + T.in_base[input] + lexrank(cell, T.in_size[input]);
-  return intern(T, K_VAR, key, ((uint64_t)input << 40) | cell, nullptr, 0);
+  const uint32_t v = intern(T, K_VAR, key, ((uint64_t)input << 40) | cell, nullptr, 0);
+  if (T.in_cache) T.in_cache[ci] = v;
+  return v;
 }
 // Undefined symbols (!undef<k>, symexec.cpp:316): their identity is a
 // (class, a, b) triple; they sort before every input symbol, as '!' does.

@@ -49,6 +49,8 @@ struct Batch {
   uint32_t sched_on_chip;  // K0: capacity (threads) of its on-chip control state, 0 = global
   const uint32_t *long_threads;  // threads with >= EXEC_WARP_MIN statements (warp executor)
   uint32_t n_long;
+  const uint64_t *prog_stmt;  // [P+1] first statement of each program when programs are laid out in order, else null
+  uint32_t step_bits, prog_bits;  // widths of step / program fields in the sort keys
   // run state
   uint32_t *seg_base;
   uint32_t *rel_step, *rel_set;
@@ -68,6 +70,28 @@ struct Batch {
   unsigned long long *n_faults;
   uint64_t fault_cap;
 };
+
+// Program of a batch-global statement: a search over the P+1 program
+// boundaries (L1-resident), or over the thread table when programs are not
+// laid out in order.
+__device__ __forceinline__ uint32_t prog_of_stmt(const Batch &B, uint64_t i) {
+  if (B.prog_stmt) {
+    uint32_t lo = 0, hi = B.n_progs;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) / 2;
+      if (__ldg(B.prog_stmt + mid) <= i) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  }
+  uint32_t lo = 0, hi = B.n_threads;
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) / 2;
+    if (B.thread_stmt[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return B.thread_prog[lo];
+}
 
 // Warp-aggregated slot allocation: one atomic per group of converged lanes.
 __device__ __forceinline__ unsigned long long agg_inc(unsigned long long *ctr) {
@@ -100,6 +124,8 @@ struct PrepArgs {
   const uint32_t *set_pop;    // members per pool entry
   unsigned long long *cnt;    // per stmt: is_sync | is_access << 32 (then its exclusive scan)
   int *error;
+  const uint64_t *set_words;
+  unsigned int *sched_flags;  // bit 0: some sync set does not suit k_schedule_warp
 };
 
 __device__ __forceinline__ uint32_t thread_of_stmt(const uint64_t *thread_stmt, uint32_t n_threads, uint64_t i) {
@@ -163,6 +189,16 @@ __global__ void k_prep_syncs(PrepArgs A, uint64_t *seg_start, uint32_t *seg_set)
   const bool full = A.sets[st.a].full || A.set_pop[st.a] == A.progs[p].n_threads;
   seg_set[j] = full ? A.n_syncsets : A.set_canon[st.a];
   seg_start[j + 1] = i + 1;
+  if (!full && A.sched_flags) {
+    // k_schedule_warp needs every window set inside one aligned 32-thread
+    // chunk and every syncing thread to be a member of its set
+    const veq_syncset q = A.sets[st.a];
+    const uint32_t tid = t - A.progs[p].thread_off;
+    const bool member = tid >= q.lo && tid < q.lo + q.n_bits &&
+                        ((A.set_words[q.word_off + (tid - q.lo) / 64] >> ((tid - q.lo) % 64)) & 1ull);
+    const bool chunk = q.n_bits == 0 || q.lo / 32 == (q.lo + q.n_bits - 1) / 32;
+    if (!member || !chunk) atomicOr(A.sched_flags, 1u);
+  }
 }
 
 // per program: sync count (release capacity) for the rel_off scan
@@ -410,7 +446,7 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
 // symexec.cpp:616-654). The full set uses block counts; any other set is
 // checked member by member from shared memory.
 constexpr uint32_t TS_NONE = 3;  // lane beyond the CTA's thread count
-__global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
+__global__ void __launch_bounds__(1024, 2) k_schedule_lanes(Batch B) {
   __shared__ uint8_t s_st[1024];
   __shared__ uint32_t s_bs[1024];
   __shared__ unsigned long long s_scan[33];
@@ -421,14 +457,25 @@ __global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
   const uint32_t T = pm.n_threads, full = B.prog_full_set[p];
   const uint32_t g = pm.thread_off + t;
   uint8_t st = TS_NONE;
-  uint32_t bset = UNSET;
-  uint64_t sj = 0, sj_end = 0, s_end = 0, cur_start = 0, next_start = 0;
+  uint32_t bset = UNSET, nset = UNSET;
+  uint64_t sj = 0, sj_end = 0, s_end = 0, cur_start = 0, next_start = 0, nword = 0;
+  veq_syncset nq{};
+  // the set ending the current segment and its descriptor are loaded when
+  // the segment starts, off the critical path of the round that blocks
+  auto prefetch = [&]() {
+    next_start = sj + 1 < sj_end ? B.seg_start[sj + 1] : s_end;
+    nset = sj + 1 < sj_end ? B.seg_set[sj] : UNSET;
+    if (nset != UNSET && nset != full) {
+      nq = B.sets[nset];
+      nword = B.set_words[nq.word_off];
+    }
+  };
   if (t < T) {
     sj = B.seg_off[g];
     sj_end = B.seg_off[g + 1];
     s_end = B.thread_stmt[g + 1];
     cur_start = B.seg_start[sj];
-    next_start = sj + 1 < sj_end ? B.seg_start[sj + 1] : s_end;
+    prefetch();
     st = cur_start == s_end ? TS_RET : TS_RUN;
   }
   s_st[t] = st;
@@ -471,7 +518,7 @@ __global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
         st = TS_RET;
       } else {
         st = TS_BLOCK;
-        bset = B.seg_set[sj];
+        bset = nset;
         s_bs[t] = bset;
       }
       s_st[t] = st;
@@ -495,12 +542,12 @@ __global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
           ok = s_blkfull + ret_count == T;
           mn = 0;
         } else {
-          const veq_syncset q = B.sets[bset];
+          const veq_syncset q = nq;
           const uint32_t w0 = wid * 32;
           if (q.lo >= w0 && q.lo + q.n_bits <= w0 + 32) {
             // window inside this warp: one vote decides it (members beyond
             // the CTA are TS_NONE lanes, so they fail the test)
-            const uint64_t bits = B.set_words[q.word_off] & (q.n_bits >= 64 ? ~0ull : ((1ull << q.n_bits) - 1));
+            const uint64_t bits = nword & (q.n_bits >= 64 ? ~0ull : ((1ull << q.n_bits) - 1));
             const uint32_t M = (uint32_t)(bits << (q.lo - w0));
             ok = M != 0 && (M & ~(grp | retm)) == 0;
             mn = M ? w0 + __ffs(M) - 1 : q.lo;
@@ -538,7 +585,7 @@ __global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
       if (st == TS_BLOCK && bset == I) {
         sj++;
         cur_start = next_start;
-        next_start = sj + 1 < sj_end ? B.seg_start[sj + 1] : s_end;
+        prefetch();
         st = cur_start == s_end ? TS_RET : TS_RUN;
         s_st[t] = st;
       }
@@ -564,6 +611,190 @@ __global__ void __launch_bounds__(1024) k_schedule_lanes(Batch B) {
     B.prog_nrel[p] = nrel;
     B.prog_steps[p] = step;
     B.prog_dead[p] = ret_count != T;
+  }
+}
+
+// K0, one warp per CTA program (CTAs of at most 1024 threads whose sync
+// sets are all the full set or windows inside one aligned 32-thread chunk).
+// The round-robin loop (symexec.cpp:764-781) is emulated chunk by chunk:
+// after a release only the released chunk's threads change state, so a
+// round costs one chunk's scan plus a 32-way min over cached per-chunk
+// release candidates, with no block barrier. Each thread's next segment
+// end and set are prefetched when it blocks.
+constexpr uint32_t SW_WARPS = 4;
+struct SchedWarpSmem {
+  uint32_t bs[1024], sj[1024], so[1024], cs[1024], ns[1024], nset[1024];
+  uint8_t st[1024];
+  unsigned long long cand[32];
+};
+__global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
+  extern __shared__ __align__(16) char swsm[];
+  SchedWarpSmem &S = reinterpret_cast<SchedWarpSmem *>(swsm)[threadIdx.x >> 5];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t p = blockIdx.x * SW_WARPS + (threadIdx.x >> 5);
+  if (p >= B.n_progs) return;
+  const veq_program_meta pm = B.progs[p];
+  const uint32_t T = pm.n_threads, full = B.prog_full_set[p], nch = (T + 31) / 32;
+  const uint64_t seg0 = B.seg_off[pm.thread_off];
+  // next segment after segment j of thread g: its end and its ending set
+  auto seg_next = [&](uint32_t g, uint64_t j, uint32_t &end, uint32_t &set) {
+    set = B.seg_set[j];
+    end = set == UNSET ? (uint32_t)B.thread_stmt[g + 1] : (uint32_t)B.seg_start[j + 1];
+  };
+  uint32_t ret = 0, blkfull = 0, fullmin = UNSET;
+  for (uint32_t t = lane; t < nch * 32; t += 32) {
+    uint8_t st = TS_NONE;
+    if (t < T) {
+      const uint32_t g = pm.thread_off + t;
+      const uint64_t so = B.seg_off[g];
+      uint32_t end, set;
+      seg_next(g, so, end, set);
+      const uint32_t start = (uint32_t)B.seg_start[so];
+      S.so[t] = (uint32_t)(so - seg0);
+      S.sj[t] = 0;
+      S.cs[t] = start;
+      S.ns[t] = end;
+      S.nset[t] = set;
+      S.bs[t] = UNSET;
+      st = (set == UNSET && start == end) ? TS_RET : TS_RUN;
+    }
+    S.st[t] = st;
+    ret += __popc(__ballot_sync(kFull, st == TS_RET));
+  }
+  for (uint32_t c = lane; c < 32; c += 32) S.cand[c] = ~0ull;
+  __syncwarp();
+  uint32_t dirty = nch >= 32 ? ~0u : ((1u << nch) - 1);
+  unsigned long long step = 0;
+  uint32_t nrel = 0;
+  while (ret != T) {
+    // ---- run phase over the dirty chunks, in tid order
+    unsigned long long total = 0;
+    for (uint32_t dm = dirty; dm; dm &= dm - 1) {
+      const uint32_t c = __ffs(dm) - 1, t = c * 32 + lane;
+      const uint8_t st = S.st[t];
+      const bool run = st == TS_RUN;
+      const uint32_t len = run ? S.ns[t] - S.cs[t] : 0;
+      uint32_t tot;
+      const uint32_t ex = warp_excl_scan(len, tot);
+      if (run) {
+        const uint32_t g = pm.thread_off + t;
+        const uint32_t sj = S.sj[t];
+        const uint64_t j = seg0 + S.so[t] + sj;
+        B.seg_base[j] = (uint32_t)(step + total + ex);
+        const uint32_t set = S.nset[t];
+        if (set == UNSET) {
+          S.st[t] = TS_RET;
+        } else {
+          S.st[t] = TS_BLOCK;
+          S.bs[t] = set;
+          // prefetch the segment after the sync: it runs when I is released
+          uint32_t end, nset;
+          seg_next(g, j + 1, end, nset);
+          S.cs[t] = S.ns[t];
+          S.ns[t] = end;
+          S.nset[t] = nset;
+        }
+      }
+      const uint32_t nr = __ballot_sync(kFull, run && S.nset[t] == UNSET && S.st[t] == TS_RET);
+      ret += __popc(nr);
+      const uint32_t nf = __ballot_sync(kFull, run && S.st[t] == TS_BLOCK && S.bs[t] == full);
+      blkfull += __popc(nf);
+      if (nf) fullmin = min(fullmin, c * 32 + __ffs(nf) - 1);
+      total += tot;
+    }
+    step += total;
+    // ---- release candidates of the dirty chunks: a window set inside the
+    // chunk is releasable iff every member is blocked on it or returned
+    for (uint32_t dm = dirty; dm; dm &= dm - 1) {
+      const uint32_t c = __ffs(dm) - 1, t = c * 32 + lane;
+      const uint8_t st = S.st[t];
+      const uint32_t bs = S.bs[t];
+      const uint32_t retm = __ballot_sync(kFull, st == TS_RET);
+      const uint32_t blk = __ballot_sync(kFull, st == TS_BLOCK && bs != full);
+      unsigned long long key = ~0ull;
+      if ((blk >> lane) & 1u) {
+        const uint32_t grp = __match_any_sync(blk, bs);
+        if ((uint32_t)(__ffs(grp) - 1) == lane) {
+          const veq_syncset q = B.sets[bs];
+          const uint64_t bits = B.set_words[q.word_off] & (q.n_bits >= 64 ? ~0ull : ((1ull << q.n_bits) - 1));
+          const uint32_t M = (uint32_t)(bits << (q.lo - c * 32));
+          if (M != 0 && (M & ~(grp | retm)) == 0)
+            key = ((unsigned long long)(c * 32 + __ffs(M) - 1) << 32) | t;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(kFull, key, o);
+        key = y < key ? y : key;
+      }
+      if (lane == 0) S.cand[c] = key;
+    }
+    __syncwarp();
+    // ---- the release: smallest (min tid, first blocked member)
+    unsigned long long best = lane < nch ? S.cand[lane] : ~0ull;
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(kFull, best, o);
+      best = y < best ? y : best;
+    }
+    if (blkfull && blkfull + ret == T) {
+      const unsigned long long fk = (unsigned long long)fullmin;  // min tid 0
+      best = fk < best ? fk : best;
+    }
+    if (best == ~0ull) {
+      if (total == 0) break;  // nothing ran, nothing releasable: done or deadlock
+      dirty = 0;
+      continue;
+    }
+    const uint32_t I = S.bs[(uint32_t)(best & 0xffffffffu)];
+    dirty = 0;
+    if (I == full) {
+      for (uint32_t c = 0; c < nch; c++) {
+        const uint32_t t = c * 32 + lane;
+        const bool rel = S.st[t] == TS_BLOCK && S.bs[t] == full;
+        if (rel) {
+          S.sj[t] += 1;
+          const bool r = S.nset[t] == UNSET && S.cs[t] == S.ns[t];
+          S.st[t] = r ? TS_RET : TS_RUN;
+        }
+        const uint32_t rm = __ballot_sync(kFull, rel);
+        if (rm) dirty |= 1u << c;
+        ret += __popc(__ballot_sync(kFull, rel && S.st[t] == TS_RET));
+      }
+      blkfull = 0;
+      fullmin = UNSET;
+    } else {
+      const uint32_t c = (uint32_t)(best & 0xffffffffu) / 32, t = c * 32 + lane;
+      const bool rel = S.st[t] == TS_BLOCK && S.bs[t] == I;
+      if (rel) {
+        S.sj[t] += 1;
+        const bool r = S.nset[t] == UNSET && S.cs[t] == S.ns[t];
+        S.st[t] = r ? TS_RET : TS_RUN;
+      }
+      ret += __popc(__ballot_sync(kFull, rel && S.st[t] == TS_RET));
+      dirty = 1u << c;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t r = B.rel_off[p] + nrel;
+      if (r < B.rel_off[p + 1]) {
+        B.rel_step[r] = (uint32_t)step;
+        B.rel_set[r] = I;
+      }
+    }
+    nrel++;
+    step += 1;
+  }
+  __syncwarp();
+  for (uint32_t t = lane; t < T; t += 32) {
+    const uint32_t g = pm.thread_off + t;
+    const uint8_t st = S.st[t];
+    B.th_state[g] = st;
+    B.th_seg[g] = S.sj[t];
+    B.th_bset[g] = st == TS_BLOCK ? S.bs[t] : UNSET;
+  }
+  if (lane == 0) {
+    B.prog_nrel[p] = nrel;
+    B.prog_steps[p] = step;
+    B.prog_dead[p] = ret != T;
   }
 }
 
@@ -690,7 +921,7 @@ __global__ void k_exec(Batch B, Table T) {
         }
         if (!is_store) {
           if (!(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 && (uint32_t)off < arr.seeded) {
-            regs[st.dst] = REF_NODE | intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
+            regs[st.dst] = REF_NODE | B.canon[i];  // interned by k_pre_inputs
             break;
           }
           regs[st.dst] = (uint32_t)i;
@@ -701,7 +932,7 @@ __global__ void k_exec(Batch B, Table T) {
         B.st_step[i] = step;
         uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
         unsigned long long slot = agg_inc(B.n_tup);
-        B.tup_key[slot] = (cell << 32) | step;
+        B.tup_key[slot] = (cell << B.step_bits) | step;
         B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
         break;
       }
@@ -828,7 +1059,7 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
         case VEQ_ST_UNOP: val = (uint32_t)i; break;
         case VEQ_ST_LOAD:
           if (oob) val = REF_NODE | intern_undef(T, 1, ga, (uint64_t)(uint32_t)off);
-          else if (direct) val = REF_NODE | intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
+          else if (direct) val = REF_NODE | B.canon[i];  // interned by k_pre_inputs
           else val = (uint32_t)i;
           break;
         default: break;  // copy
@@ -877,7 +1108,7 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
           B.st_step[i] = step;
           uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
           unsigned long long slot = agg_inc(B.n_tup);
-          B.tup_key[slot] = (cell << 32) | step;
+          B.tup_key[slot] = (cell << B.step_bits) | step;
           B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
         } else if (st.kind == VEQ_ST_BINOP || st.kind == VEQ_ST_UNOP) {
           B.st_step[i] = step;
@@ -1001,9 +1232,9 @@ __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, con
   uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
   if (sidx >= n_segs) return;
   const uint64_t s = seg_starts[sidx];
-  const uint64_t cell = keys[s] >> 32;
+  const uint64_t cell = keys[s] >> B.step_bits;
   uint64_t e = s + 1;
-  while (e < n_tup && (keys[e] >> 32) == cell) e++;
+  while (e < n_tup && (keys[e] >> B.step_bits) == cell) e++;
   // identify the array of this cell via the first tuple's statement
   const uint32_t stmt0 = (uint32_t)(vals[s] >> 32);
   const uint32_t tid0 = (uint32_t)(vals[s] & 0xffffffffu);
@@ -1028,7 +1259,7 @@ __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, con
   Reader *rd = rscratch + s;
   uint32_t nrd = 0;
   for (uint64_t k = s; k < e; k++) {
-    const uint32_t step = (uint32_t)(keys[k] & 0xffffffffu);
+    const uint32_t step = (uint32_t)(keys[k] & ((1ull << B.step_bits) - 1));
     const uint32_t stmt = (uint32_t)(vals[k] >> 32);
     const uint32_t tid = (uint32_t)(vals[k] & 0xffffffffu);
     const bool is_store = B.stmts[stmt].kind == VEQ_ST_STORE;
@@ -1125,10 +1356,11 @@ __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, con
   B.final_val[cell] = has ? value : UNSET;
 }
 
-__global__ void k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t *starts, unsigned long long *n_starts) {
+__global__ void k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t *starts, unsigned long long *n_starts,
+                            uint32_t step_bits) {
   uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  if (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32)) {
+  if (k == 0 || (keys[k] >> step_bits) != (keys[k - 1] >> step_bits)) {
     unsigned long long i = agg_inc(n_starts);
     starts[i] = (uint32_t)k;
   }
@@ -1213,6 +1445,79 @@ __global__ void k_chain_scatter(Batch B, const uint32_t *base, uint32_t *log, ui
   }
 }
 
+// Input symbols read by direct loads (never-stored input arrays) are
+// interned in one parallel pass before execution; the executors read the
+// node from canon[i].
+__global__ void k_pre_inputs(Batch B, Table T) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  const veq_stmt st = B.stmts[i];
+  if (st.kind != VEQ_ST_LOAD) return;
+  const veq_program_meta pm = B.progs[prog_of_stmt(B, i)];
+  const veq_array arr = B.arrays[pm.array_off + st.arr];
+  const int32_t off = (int32_t)st.a;
+  if (off < 0 || (uint64_t)off >= arr.size) return;
+  if (!(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 && (uint32_t)off < arr.seeded)
+    B.canon[i] = intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
+}
+
+// One pass after the memory scan: operands resolved through loads, use
+// counts, and the chain-log size of every chain head.
+__global__ void k_resolve_all(Batch B, uint32_t *sz) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  uint32_t v = 0;
+  if (B.st_step[i] != UNSET) {
+    const veq_stmt st = B.stmts[i];
+    if (st.kind == VEQ_ST_BINOP) {
+      const uint32_t a = chase(B, B.ref_a[i]), b = chase(B, B.ref_b[i]);
+      B.ref_a[i] = a;
+      B.ref_b[i] = b;
+      if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
+      if (is_stmt_ref(b)) atomicAdd(B.uses + b, 1u);
+      if ((st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX) && B.chain_head[i] == (uint32_t)i) v = B.chain_len[i] + 1;
+    } else if (st.kind == VEQ_ST_UNOP) {
+      const uint32_t a = chase(B, B.ref_a[i]);
+      B.ref_a[i] = a;
+      if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
+    } else if (st.kind == VEQ_ST_STORE || st.kind == VEQ_ST_LOAD) {
+      B.ref_a[i] = chase(B, B.ref_a[i]);
+    }
+  }
+  sz[i] = v;
+}
+
+// One pass after the log scan: chain-log entries and the work list.
+__global__ void k_scatter_work(Batch B, const uint32_t *base, uint32_t *log, uint32_t *log_stmt,
+                               unsigned long long *wkey, uint32_t *wval, unsigned long long *n_work) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  if (B.st_step[i] == UNSET) return;
+  const veq_stmt st = B.stmts[i];
+  if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) return;
+  const bool chain = is_chain_op(st);
+  if (chain) {
+    const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
+    const uint32_t b = base[h];
+    if (pos == 0) {
+      log[b] = B.ref_a[i];
+      log[b + 1] = B.ref_b[i];
+      log_stmt[b] = (uint32_t)i;
+      log_stmt[b + 1] = (uint32_t)i;
+    } else {
+      log[b + pos + 1] = B.ref_b[i];
+      log_stmt[b + pos + 1] = (uint32_t)i;
+    }
+    if (B.continued[i] && B.uses[i] == 1) return;  // absorbed by its successor
+  }
+  const uint32_t p = prog_of_stmt(B, i);
+  unsigned long long slot = agg_inc(n_work);
+  // (step, program): every dependency of an item has a smaller step in the
+  // same program, hence a smaller key, and all CTAs advance together
+  wkey[slot] = ((unsigned long long)B.st_step[i] << B.prog_bits) | p;
+  wval[slot] = (uint32_t)i;
+}
+
 // work items: every executed BinOp/UnOp except chain links absorbed by
 // their successor (continued and used exactly once).
 __global__ void k_make_work(Batch B, unsigned long long *wkey, uint32_t *wval, unsigned long long *n_work) {
@@ -1233,7 +1538,7 @@ __global__ void k_make_work(Batch B, unsigned long long *wkey, uint32_t *wval, u
   unsigned long long slot = agg_inc(n_work);
   // (step, program): every dependency of an item has a smaller step in the
   // same program, hence a smaller key, and all CTAs advance together
-  wkey[slot] = ((unsigned long long)B.st_step[i] << 20) | p;
+  wkey[slot] = ((unsigned long long)B.st_step[i] << B.prog_bits) | p;
   wval[slot] = (uint32_t)i;
 }
 
