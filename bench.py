@@ -131,6 +131,7 @@ def main():
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     from paper_2511_12638_b200 import workloads
+    from paper_2511_12638_b200.dist import combine_verdicts, shard_blocks
     W = workloads.c2_reduce(n_blocks=args.blocks * world, block=1024)
     cfg_json = {"workload": "C2 warp-shuffle tree reduction vs sequential sum, N=2^20 per GPU as "
                             f"{args.blocks} CTA pairs x 1024 elements",
@@ -178,8 +179,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     t0 = time.time()
-    a, b, inputs = frontend.elaborate_pair(W.kernel_a, W.kernel_b, W.cfg, "B", args.blocks, want_names=False,
-                                           block_base=rank * args.blocks)
+    # weak scaling: each rank owns a contiguous share of a world-sized grid
+    base, nblk = shard_blocks(args.blocks * world, rank, world)
+    a, b, inputs = frontend.elaborate_pair(W.kernel_a, W.kernel_b, W.cfg, "B", nblk, want_names=False,
+                                           block_base=base)
     t_elab = time.time() - t0
     S = len(a.stmts) + len(b.stmts)
     sess = Session(local, max_nodes=max(1 << 22, 4 * S // 10), max_kid_words=(1 << 24) + 4 * S,
@@ -209,9 +212,11 @@ def main():
             dist.all_reduce(counters)
         return ra, rb, vc, launches
 
-    # correctness gate: every VC equal, no faults
+    # correctness gate: every VC equal, no faults, on every rank
     ra, rb, vc, _ = step()
-    ok = vc.n_equal == vc.n_vcs == args.blocks and ra.n_faults == 0 and rb.n_faults == 0
+    tot, first_fail = combine_verdicts([vc.n_equal, vc.n_vcs, ra.n_faults + rb.n_faults, vc.n_missing],
+                                       None if vc.n_equal == vc.n_vcs else base, device="cuda" if dist else None)
+    ok = tot["equal"] == tot["vcs"] == args.blocks * world and tot["faults"] == 0
     if not ok:
         print(f"[bench] rank {rank}: verification failed: {vc.n_equal}/{vc.n_vcs} equal, faults "
               f"{ra.n_faults}/{rb.n_faults}", file=sys.stderr)
