@@ -19,7 +19,34 @@ CASES = [
     ("wl_c2_reduce_b0", workloads.c2_reduce(n_blocks=2, block=128), 0),
     ("wl_c1_matmul_n8", workloads.c1_matmul(n=8, tk=2), None),
     ("wl_c1_matmul_n16", workloads.c1_matmul(n=16, tk=4), None),
+    # C3 conv at reduced shapes (CI, CO, H, W, tile)
+    ("wl_c3_conv_b1", workloads.c3_conv(2, 2, 4, 4, 2, 2), 1),
+    ("wl_c3_conv_b3", workloads.c3_conv(2, 2, 4, 4, 2, 2), 3),
+    ("wl_c3_conv_c3_b2", workloads.c3_conv(3, 2, 8, 8, 4, 4), 2),
+    # C4 attention at reduced shapes (L, D, rows, threads per row, key block)
+    ("wl_c4_attn_b1", workloads.c4_attention(8, 4, 2, 2, 4), 1),
+    ("wl_c4_attn_l16_b2", workloads.c4_attention(16, 4, 4, 2, 4), 2),
+    ("wl_c4_attn_l12_b0", workloads.c4_attention(12, 2, 2, 1, 4), 0),
 ]
+# C5: the first variant of every mutation kind of the seeded generator, N=4
+_seen = {}
+for _kind, _src, _cfg in workloads.c5_variants(400, 4):
+    _seen.setdefault(_kind, (_src, _cfg))
+C5 = [(f"wl_c5_{k}", _seen[k]) for k in workloads.C5_KINDS if k in _seen]
+
+
+def _write(name, ka, kb, cfg):
+    d = os.path.join(HERE, name)
+    os.makedirs(d, exist_ok=True)
+    for fn, text in (("a.mk", ka), ("b.mk", kb), ("cfg.cfg", cfg)):
+        with open(os.path.join(d, fn), "w") as f:
+            f.write(text)
+    subprocess.check_call([H, "pair", d, os.path.join(d, "a.mk"), os.path.join(d, "b.mk"), os.path.join(d, "cfg.cfg")])
+    print(name, "ok")
+
+
+for name, (src, cfg) in C5:
+    _write(name, workloads.c5_reference(4), src, cfg)
 
 for name, w, blk in CASES:
     d = os.path.join(HERE, name)
