@@ -66,8 +66,8 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
     for k in oa:
         sizes.append(int(a.arrays[o0 + k]["size"]))
     sc_nodes = [vc.sc_node[i] for i in range(vc.n_sc)]
-    sc_strs = dict(zip(sc_nodes, sess.to_strings(sorted(set(sc_nodes))))) if (render_side_conditions and sc_nodes) \
-        else {}
+    uniq = sorted(set(sc_nodes))
+    sc_strs = dict(zip(uniq, sess.to_strings(uniq))) if (render_side_conditions and uniq) else {}
     for p in range(a.n_progs):
         rep = PairReport(verdict="unknown")
         for side, rr in (("a", ra[p]), ("b", rb[p])):
