@@ -493,7 +493,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   }
   CK(cudaMemsetAsync(d_flags, 0, 4, s));
   PrepArgs PA{P, Tn, NS, d->n_arrays_total, S, B.progs, B.thread_stmt, B.thread_prog, B.stmts, B.sets, d_canon, d_pop,
-              d_cnt, ctx->error, B.set_words, d_flags};
+              d_cnt, ctx->error, B.set_words, d_flags, B.arrays};
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), s));
   CK(cudaMemsetAsync(d_cnt + S, 0, 8, s));
   CK(cudaMemsetAsync(d_nlong, 0, 8, s));
@@ -619,6 +619,10 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaMemsetAsync(B.canon, 0xff, S * 4, s));
   CK(cudaMemsetAsync(B.uses, 0, S * 4, s));
   CK(cudaMemsetAsync(B.continued, 0, S, s));
+  // the tuple buffer holds every checked access; slots of accesses that
+  // never execute (deadlock) keep key ~0 and sort last, so the sort needs no
+  // host read-back of the tuple count
+  if (bd->n_access_max) CK(cudaMemsetAsync(B.tup_key, 0xff, bd->n_access_max * 8, s));
   CK(cudaMemsetAsync(B.n_tup, 0, 8, s));
   CK(cudaMemsetAsync(B.n_faults, 0, 8, s));
   CK(cudaMemsetAsync(B.final_val, 0xff, std::max<uint64_t>(bd->n_cells, 1) * 4, s));
@@ -665,9 +669,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   if (B.n_long) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_long * 32, 128), 128, 0, s>>>(B, ctx->T));
   PH1(VEQ_PH_EXEC);
   CK(cudaGetLastError());
-  unsigned long long n_tup = 0;
-  CK(cudaMemcpyAsync(&n_tup, B.n_tup, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  const unsigned long long n_tup = bd->n_access_max;
   // K4: sort access tuples by (cell, step) and scan per cell
   PH0(VEQ_PH_SORT);
   if (n_tup) {
@@ -690,13 +692,13 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
     ctx->launches += (end_bit + 7) / 8 + 1;
     CK(cudaMemsetAsync(n_starts, 0, 8, s));
-    LAUNCH(k_seg_heads<<<blocks(n_tup, 256), 256, 0, s>>>(k2, n_tup, starts, n_starts, B.step_bits));
+    LAUNCH(k_seg_heads<<<blocks(n_tup, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(k2, n_tup, starts, n_starts, B.step_bits));
     PH1(VEQ_PH_SORT);
     unsigned long long nseg = 0;
     CK(cudaMemcpyAsync(&nseg, n_starts, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     PH0(VEQ_PH_MEMSCAN);
-    LAUNCH(k_mem_scan<<<blocks(nseg, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, (uint32_t)nseg, n_tup, rs));
+    if (nseg) LAUNCH(k_mem_scan<<<blocks(nseg, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, (uint32_t)nseg, n_tup, rs));
     PH1(VEQ_PH_MEMSCAN);
     CK(cudaGetLastError());
     CK(cudaFreeAsync(tmp, s));
@@ -752,7 +754,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMallocAsync(&wv2, S * 4, s));
     CK(cudaMallocAsync(&nw, 8, s));
     CK(cudaMemsetAsync(nw, 0, 8, s));
-    LAUNCH(k_scatter_work<<<blocks(S, 256), 256, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
+    LAUNCH(k_scatter_work<<<blocks(S, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
     CK(cudaMemcpyAsync(&n_work, nw, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     void *tmp2 = nullptr;

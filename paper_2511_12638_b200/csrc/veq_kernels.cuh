@@ -65,6 +65,7 @@ struct Batch {
   uint8_t *continued;
   unsigned long long *tup_key, *tup_val;
   unsigned long long *n_tup;
+
   uint32_t *final_val, *final_node;
   veq_fault *faults;
   unsigned long long *n_faults;
@@ -101,6 +102,40 @@ __device__ __forceinline__ unsigned long long agg_inc(unsigned long long *ctr) {
   return g.shfl(base, 0) + g.thread_rank();
 }
 
+// Block-wide append: every thread of the block calls it (no early exit) with
+// its item count and gets its first output slot; one atomic per block, so a
+// grid-wide stream compaction costs (items / block size) atomics instead of
+// one per warp on a single contended address.
+template <int NT>
+__device__ __forceinline__ unsigned long long block_append(unsigned long long *ctr, uint32_t cnt) {
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  __shared__ uint32_t s_w[NT / 32];
+  __shared__ unsigned long long s_base;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) s_w[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t v = lane < NT / 32 ? s_w[lane] : 0;
+    uint32_t z = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= (unsigned)o) z += y;
+    }
+    if (lane < NT / 32) s_w[lane] = z - v;
+    if (lane == 31) s_base = z ? atomicAdd(ctr, (unsigned long long)z) : 0;
+  }
+  __syncthreads();
+  return s_base + s_w[wid] + (x - cnt);
+}
+constexpr int APP_NT = 512, APP_ITEMS = 8;  // 4096 items per block
+
 __device__ __forceinline__ void emit_fault(const Batch &B, const veq_fault &f) {
   unsigned long long i = agg_inc(B.n_faults);
   if (i < B.fault_cap) B.faults[i] = f;
@@ -126,6 +161,7 @@ struct PrepArgs {
   int *error;
   const uint64_t *set_words;
   unsigned int *sched_flags;  // bit 0: some sync set does not suit k_schedule_warp
+  const veq_array *arrays;
 };
 
 __device__ __forceinline__ uint32_t thread_of_stmt(const uint64_t *thread_stmt, uint32_t n_threads, uint64_t i) {
@@ -153,9 +189,20 @@ __global__ void k_prep_stmts(PrepArgs A) {
   if (st.kind > VEQ_ST_SYNC) {
     atomicCAS(A.error, 0, 1);
   } else if (st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE) {
-    c = 1ull << 32;
     const uint32_t t = thread_of_stmt(A.thread_stmt, A.n_threads, i);
-    if (st.arr >= A.progs[A.thread_prog[t]].n_arrays) atomicCAS(A.error, 0, 2);
+    const veq_program_meta pm = A.progs[A.thread_prog[t]];
+    if (st.arr >= pm.n_arrays) {
+      atomicCAS(A.error, 0, 2);
+    } else {
+      // an access tuple is emitted by an in-bounds access to a checked
+      // array; direct loads of never-stored inputs cannot race
+      const veq_array ar = A.arrays[pm.array_off + st.arr];
+      const int32_t off = (int32_t)st.a;
+      const bool inb = off >= 0 && (uint64_t)off < ar.size;
+      const bool direct = st.kind == VEQ_ST_LOAD && !(ar.flags & VEQ_ARR_STORED) && ar.input >= 0 &&
+                          (uint32_t)off < ar.seeded;
+      if (inb && !direct) c = 1ull << 32;
+    }
   } else if (st.kind == VEQ_ST_SYNC) {
     c = 1;
     if (st.a >= A.n_syncsets) atomicCAS(A.error, 0, 3);
@@ -931,7 +978,8 @@ __global__ void k_exec(Batch B, Table T) {
         }
         B.st_step[i] = step;
         uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
-        unsigned long long slot = agg_inc(B.n_tup);
+        // warp-aggregated slot (coalesced writes); unfilled slots keep key ~0
+        const unsigned long long slot = agg_inc(B.n_tup);
         B.tup_key[slot] = (cell << B.step_bits) | step;
         B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
         break;
@@ -1107,7 +1155,7 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
           if (st.kind == VEQ_ST_STORE) B.ref_a[i] = va;
           B.st_step[i] = step;
           uint64_t cell = B.arr_cell_base[ga] + (uint64_t)off;
-          unsigned long long slot = agg_inc(B.n_tup);
+          const unsigned long long slot = agg_inc(B.n_tup);  // coalesced; unfilled slots keep key ~0
           B.tup_key[slot] = (cell << B.step_bits) | step;
           B.tup_val[slot] = ((unsigned long long)i << 32) | tid;
         } else if (st.kind == VEQ_ST_BINOP || st.kind == VEQ_ST_UNOP) {
@@ -1356,14 +1404,22 @@ __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, con
   B.final_val[cell] = has ? value : UNSET;
 }
 
-__global__ void k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t *starts, unsigned long long *n_starts,
-                            uint32_t step_bits) {
-  uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  if (k == 0 || (keys[k] >> step_bits) != (keys[k - 1] >> step_bits)) {
-    unsigned long long i = agg_inc(n_starts);
-    starts[i] = (uint32_t)k;
+__global__ void __launch_bounds__(APP_NT) k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t *starts,
+                                                     unsigned long long *n_starts, uint32_t step_bits) {
+  // a head starts every run of equal cells; unfilled slots (key ~0, from
+  // accesses that never executed) sort last and start nothing
+  const uint64_t b0 = (uint64_t)blockIdx.x * APP_NT * APP_ITEMS + threadIdx.x;
+  uint32_t mask = 0;
+#pragma unroll
+  for (int k = 0; k < APP_ITEMS; k++) {
+    const uint64_t i = b0 + (uint64_t)k * APP_NT;
+    if (i < n && keys[i] != ~0ull && (i == 0 || (keys[i] >> step_bits) != (keys[i - 1] >> step_bits)))
+      mask |= 1u << k;
   }
+  unsigned long long o = block_append<APP_NT>(n_starts, __popc(mask));
+#pragma unroll
+  for (int k = 0; k < APP_ITEMS; k++)
+    if ((mask >> k) & 1u) starts[o++] = (uint32_t)(b0 + (uint64_t)k * APP_NT);
 }
 
 // Follow load refs to the value they read (a load's ref_a holds the value
@@ -1487,35 +1543,46 @@ __global__ void k_resolve_all(Batch B, uint32_t *sz) {
   sz[i] = v;
 }
 
-// One pass after the log scan: chain-log entries and the work list.
-__global__ void k_scatter_work(Batch B, const uint32_t *base, uint32_t *log, uint32_t *log_stmt,
-                               unsigned long long *wkey, uint32_t *wval, unsigned long long *n_work) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  if (B.st_step[i] == UNSET) return;
-  const veq_stmt st = B.stmts[i];
-  if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) return;
-  const bool chain = is_chain_op(st);
-  if (chain) {
-    const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
-    const uint32_t b = base[h];
-    if (pos == 0) {
-      log[b] = B.ref_a[i];
-      log[b + 1] = B.ref_b[i];
-      log_stmt[b] = (uint32_t)i;
-      log_stmt[b + 1] = (uint32_t)i;
-    } else {
-      log[b + pos + 1] = B.ref_b[i];
-      log_stmt[b + pos + 1] = (uint32_t)i;
+// One pass after the log scan: chain-log entries and the work list (every
+// executed BinOp/UnOp except chain links absorbed by their successor).
+__global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t *base, uint32_t *log,
+                                                        uint32_t *log_stmt, unsigned long long *wkey, uint32_t *wval,
+                                                        unsigned long long *n_work) {
+  const uint64_t b0 = (uint64_t)blockIdx.x * APP_NT * APP_ITEMS + threadIdx.x;
+  uint32_t mask = 0;
+#pragma unroll
+  for (int k = 0; k < APP_ITEMS; k++) {
+    const uint64_t i = b0 + (uint64_t)k * APP_NT;
+    if (i >= B.n_stmts || B.st_step[i] == UNSET) continue;
+    const veq_stmt st = B.stmts[i];
+    if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) continue;
+    if (is_chain_op(st)) {
+      const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
+      const uint32_t b = base[h];
+      if (pos == 0) {
+        log[b] = B.ref_a[i];
+        log[b + 1] = B.ref_b[i];
+        log_stmt[b] = (uint32_t)i;
+        log_stmt[b + 1] = (uint32_t)i;
+      } else {
+        log[b + pos + 1] = B.ref_b[i];
+        log_stmt[b + pos + 1] = (uint32_t)i;
+      }
+      if (B.continued[i] && B.uses[i] == 1) continue;  // absorbed by its successor
     }
-    if (B.continued[i] && B.uses[i] == 1) return;  // absorbed by its successor
+    mask |= 1u << k;
   }
-  const uint32_t p = prog_of_stmt(B, i);
-  unsigned long long slot = agg_inc(n_work);
-  // (step, program): every dependency of an item has a smaller step in the
-  // same program, hence a smaller key, and all CTAs advance together
-  wkey[slot] = ((unsigned long long)B.st_step[i] << B.prog_bits) | p;
-  wval[slot] = (uint32_t)i;
+  unsigned long long o = block_append<APP_NT>(n_work, __popc(mask));
+#pragma unroll
+  for (int k = 0; k < APP_ITEMS; k++) {
+    if (!((mask >> k) & 1u)) continue;
+    const uint64_t i = b0 + (uint64_t)k * APP_NT;
+    // (step, program): every dependency of an item has a smaller step in the
+    // same program, hence a smaller key, and all CTAs advance together
+    wkey[o] = ((unsigned long long)B.st_step[i] << B.prog_bits) | prog_of_stmt(B, i);
+    wval[o] = (uint32_t)i;
+    o++;
+  }
 }
 
 // work items: every executed BinOp/UnOp except chain links absorbed by
