@@ -776,8 +776,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       static const bool prof_on = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
       unsigned long long *prof = nullptr;
       if (prof_on) {
-        CK(cudaMallocAsync(&prof, 16 * 8, s));
-        CK(cudaMemsetAsync(prof, 0, 16 * 8, s));
+        CK(cudaMallocAsync(&prof, 32 * 8, s));
+        CK(cudaMemsetAsync(prof, 0, 32 * 8, s));
       }
       EvalCtx E{log, log_stmt, base, prof};
       uint4 *desc = nullptr;
@@ -803,8 +803,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
                                                                                 ctx->pool_cap, chunk, grab));
       CK(cudaFreeAsync(desc, s));
       if (prof) {
-        unsigned long long hp[16];
-        CK(cudaMemcpyAsync(hp, prof, 16 * 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long hp[32];
+        CK(cudaMemcpyAsync(hp, prof, 32 * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         fprintf(stderr, "[veq prof] items %llu warps %llu grab %u | wait %.1f us/item |", (unsigned long long)n_work,
                 (unsigned long long)warps, grab, hp[0] / 1965.0 / std::max<double>(1, n_work));
@@ -814,6 +814,14 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
         if (hp[7])
           fprintf(stderr, " | lean phases: loads %.2f sort %.2f intern %.2f us", hp[11] / 1965.0 / hp[7],
                   hp[12] / 1965.0 / hp[7], hp[13] / 1965.0 / hp[7]);
+        if (hp[21] || hp[24] || hp[25] || hp[26] || hp[27] || hp[28])
+          fprintf(stderr, " | pairs: %llu items %.2f us per item; fallbacks skip %llu m>16 %llu coef %llu consts %llu ties %llu",
+                  hp[21], hp[20] / 1965.0 / std::max<unsigned long long>(1, hp[21]), hp[24], hp[25], hp[26], hp[27],
+                  hp[28]);
+        if (hp[8])
+          fprintf(stderr, " | smem: pool wait %.2f us/item, %.1f pages/item; runs %.2f gather %.2f merge %.2f intern %.2f us",
+                  hp[14] / 1965.0 / hp[8], (double)hp[15] / hp[8], hp[16] / 1965.0 / hp[8], hp[17] / 1965.0 / hp[8],
+                  hp[18] / 1965.0 / hp[8], hp[19] / 1965.0 / hp[8]);
         fprintf(stderr, "\n");
         CK(cudaFreeAsync(prof, s));
       }

@@ -1782,123 +1782,180 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
     d = w < n_work ? __ldg(desc + w) : make_uint4(0, 0, 0, 0xff);
     lg = (w < n_work && desc_is_add(d) && lane < d.z) ? __ldg(E.log + d.y + lane) : UNSET;
   };
-  unsigned long long prof_wait = 0, prof_work[5] = {0, 0, 0, 0, 0}, prof_n[5] = {0, 0, 0, 0, 0}, prof_lean[3] = {0, 0, 0};
+  unsigned long long prof_wait = 0, prof_work[6] = {0, 0, 0, 0, 0, 0}, prof_n[6] = {0, 0, 0, 0, 0, 0}, prof_lean[3] = {0, 0, 0}, prof_pool = 0, prof_pages = 0, prof_smem[4] = {0, 0, 0, 0};
   unsigned long long w = ((unsigned long long)wib * gridDim.x + blockIdx.x) * grab, w_end = w + grab;
   uint4 d;
   uint32_t lg;
   fetch(w, d, lg);
-  while (w < n_work) {
-    unsigned long long wn = w + 1;
-    if (wn == w_end) {
-      wn = claim();
-      w_end = wn + grab;
+  auto next_of = [&](unsigned long long x) -> unsigned long long {
+    unsigned long long y = x + 1;
+    if (y == w_end) {
+      y = claim();
+      w_end = y + grab;
     }
+    return y;
+  };
+  while (w < n_work) {
+    const unsigned long long wn = next_of(w);
     uint4 dn;
     uint32_t lgn;
     fetch(wn, dn, lgn);
+    // two consecutive small chains with no dependency between them run on
+    // the two halves of the warp (lean_pair16)
+    bool paired = wn < n_work && desc_is_add(d) && d.z <= 16 && desc_is_add(dn) && dn.z <= 16;
+    if (paired) paired = !__any_sync(kFull, lane < dn.z && lgn == d.x);
+    uint32_t rA = UNSET, rB = UNSET;
+    if (paired) {
+      const long long t0 = E.prof ? clock64() : 0;
+      const uint32_t sl = lane & 15;
+      const uint32_t lgp = __shfl_sync(kFull, lgn, sl);
+      const uint32_t my_lg = lane < 16 ? lg : lgp, my_n = lane < 16 ? d.z : dn.z;
+      const uint32_t leaf = sl < my_n ? wait_node(B, my_lg) : UNSET;
+      const uint32_t negm = __ballot_sync(kFull, leaf == T.id_neginf);
+      const bool skip = (negm & (0xffffu << (lane & 16))) != 0;  // -inf leaves: full path
+      bool created = false;
+      const uint32_t r = lean_pair16(T, leaf, my_n, skip, W, created, E.prof ? E.prof + 24 : nullptr);
+      rA = __shfl_sync(kFull, r, 0);
+      rB = __shfl_sync(kFull, r, 16);
+      if ((lane == 0 || lane == 16) && r != UNSET) {
+        if (!created) fence_acq_rel();
+        atomicExch(B.canon + (lane == 0 ? d.x : dn.x), r);
+      }
+      if (E.prof && lane == 0) {
+        prof_work[5] += clock64() - t0;
+        prof_n[5] += (rA != UNSET) + (rB != UNSET);
+      }
+    }
+    // items left for the full warp: the current one when unpaired, else the
+    // halves the pair path did not cover (in list order)
+    const bool needA = !paired || rA == UNSET, needB = paired && rB == UNSET;
+    for (int q = 0; q < 2; q++) {
+      if (q == 0 ? !needA : !needB) continue;
+      const uint4 dq = q == 0 ? d : dn;
+      const uint32_t lgq = q == 0 ? lg : lgn;
+      {
+        const uint4 &d = dq;
+        const uint32_t lg = lgq;
     const uint32_t i = d.x;
-    const uint64_t mark = A.used;
-    char *const mbase = A.base;
-    A.item = i;
-    uint32_t r = UNSET;
-    bool created = false;
-    int path = 0;  // 0 other, 1 lean, 2 smem, 3 small_reg, 4 global
-    long long t0 = E.prof ? clock64() : 0, t1 = 0;
-    if (desc_is_add(d)) {
-      const uint32_t b = d.y, n = d.z;
-      // operands ready, -inf check; sums of <= 32 terms finish in registers
-      uint32_t leaf0 = lane < n ? wait_node(B, lg) : UNSET, m = 0;
-      bool neg = leaf0 == T.id_neginf;
-      for (uint32_t k = lane + 32; k < n; k += 32) neg |= wait_node(B, E.log[b + k]) == T.id_neginf;
-      neg = __any_sync(kFull, neg);
-      if (E.prof) t1 = clock64();
-      if (!neg) {
-        bool counted = false;
-        if (n <= 32) {
-          r = warp_add_lean(T, leaf0, n, m, &W, &created, E.prof ? prof_lean : nullptr);
-          counted = true;
-          path = 1;
-        }
-        if (r == UNSET && (!counted || m > 32)) {
-          if (!counted) {
-            for (uint32_t k = lane; k < n; k += 32) m += n_terms_of(T, wait_node(B, E.log[b + k]));
-            m = __reduce_add_sync(kFull, m);
+      const uint64_t mark = A.used;
+      char *const mbase = A.base;
+      A.item = i;
+      uint32_t r = UNSET;
+      bool created = false;
+      int path = 0;  // 0 other, 1 lean, 2 smem, 3 small_reg, 4 global
+      long long t0 = E.prof ? clock64() : 0, t1 = 0;
+      if (desc_is_add(d)) {
+        const uint32_t b = d.y, n = d.z;
+        // operands ready, -inf check; sums of <= 32 terms finish in registers
+        uint32_t leaf0 = lane < n ? wait_node(B, lg) : UNSET, m = 0;
+        bool neg = leaf0 == T.id_neginf;
+        for (uint32_t k = lane + 32; k < n; k += 32) neg |= wait_node(B, E.log[b + k]) == T.id_neginf;
+        neg = __any_sync(kFull, neg);
+        if (E.prof) t1 = clock64();
+        if (!neg) {
+          bool counted = false;
+          if (n <= 32) {
+            r = warp_add_lean(T, leaf0, n, m, &W, &created, E.prof ? prof_lean : nullptr);
+            counted = true;
+            path = 1;
           }
-          const uint32_t pages = (uint32_t)((add_smem_bytes(n, m) + SPAGE - 1) / SPAGE);
-          const int first = pool_acquire(SP, pages);
-          if (first >= 0) {
-            char *buf = SP.base + (uint64_t)first * SPAGE;
-            uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
-            for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
-            __syncwarp();
-            r = warp_add_smem(T, buf, n, m, &W);
-            pool_release(SP, first, pages);
-            path = 2;
-          }
-        } else if (r == UNSET && n <= 32) {
-          r = warp_add_small_reg(T, leaf0, n);  // like terms / coefficients
-          path = 3;
-        }
-      }
-      if (r == UNSET) {
-        path = 4;
-        uint32_t *ids = warp_get<uint32_t>(A, n);
-        r = T.id_zero;
-        if (ids) {
-          for (uint32_t k = lane; k < n; k += 32) ids[k] = wait_node(B, E.log[b + k]);
-          __syncwarp();
-          uint32_t start = 0;
-          if (neg) {
-            // -inf operands: same restart rule as eval_stmt, sequentially
-            if (lane == 0) {
-              for (uint32_t k = 0; k < n; k++) {
-                if (ids[k] != T.id_neginf) continue;
-                uint32_t s = E.log_stmt[b + k];
-                arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
-                uint32_t rr = k < 1 ? 1 : k;
-                ids[rr] = intern_undef(T, 3, s >> 29, s);
-                start = rr;
-                if (k == 0) k = 1;
-              }
+          if (r == UNSET && (!counted || m > 32)) {
+            if (!counted) {
+              for (uint32_t k = lane; k < n; k += 32) m += n_terms_of(T, wait_node(B, E.log[b + k]));
+              m = __reduce_add_sync(kFull, m);
             }
-            start = __shfl_sync(kFull, start, 0);
-            __syncwarp();
+            const uint32_t pages = (uint32_t)((add_smem_bytes(n, m) + SPAGE - 1) / SPAGE);
+            const long long pa0 = E.prof ? clock64() : 0;
+            const int first = pool_acquire(SP, pages);
+            if (E.prof && lane == 0) {
+              prof_pool += clock64() - pa0;
+              prof_pages += pages;
+            }
+            if (first >= 0) {
+              char *buf = SP.base + (uint64_t)first * SPAGE;
+              uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
+              for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
+              __syncwarp();
+              r = warp_add_smem(T, buf, n, m, &W, E.prof ? prof_smem : nullptr);
+              pool_release(SP, first, pages);
+              path = 2;
+            }
+          } else if (r == UNSET && n <= 32) {
+            r = warp_add_small_reg(T, leaf0, n);  // like terms / coefficients
+            path = 3;
           }
-          r = warp_add_small(T, ids + start, n - start);
-          if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
+        }
+        if (r == UNSET) {
+          path = 4;
+          uint32_t *ids = warp_get<uint32_t>(A, n);
+          r = T.id_zero;
+          if (ids) {
+            for (uint32_t k = lane; k < n; k += 32) ids[k] = wait_node(B, E.log[b + k]);
+            __syncwarp();
+            uint32_t start = 0;
+            if (neg) {
+              // -inf operands: same restart rule as eval_stmt, sequentially
+              if (lane == 0) {
+                for (uint32_t k = 0; k < n; k++) {
+                  if (ids[k] != T.id_neginf) continue;
+                  uint32_t s = E.log_stmt[b + k];
+                  arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
+                  uint32_t rr = k < 1 ? 1 : k;
+                  ids[rr] = intern_undef(T, 3, s >> 29, s);
+                  start = rr;
+                  if (k == 0) k = 1;
+                }
+              }
+              start = __shfl_sync(kFull, start, 0);
+              __syncwarp();
+            }
+            r = warp_add_small(T, ids + start, n - start);
+            if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
+          }
+        }
+      } else {
+        if (lane == 0) r = eval_stmt(B, T, A, E, i);
+        r = __shfl_sync(kFull, r, 0);
+      }
+      if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
+      if (lane == 0) {
+        // a node this warp created was fenced before its slot was claimed;
+        // anything else needs the fence for cumulativity
+        if (!created) fence_acq_rel();
+        atomicExch(B.canon + i, r);
+        if (E.prof) {
+          long long t2 = clock64();
+          if (!t1) t1 = t0;
+          prof_wait += t1 - t0;
+          prof_work[path] += t2 - t1;
+          prof_n[path]++;
         }
       }
-    } else {
-      if (lane == 0) r = eval_stmt(B, T, A, E, i);
-      r = __shfl_sync(kFull, r, 0);
-    }
-    if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
-    if (lane == 0) {
-      // a node this warp created was fenced before its slot was claimed;
-      // anything else needs the fence for cumulativity
-      if (!created) fence_acq_rel();
-      atomicExch(B.canon + i, r);
-      if (E.prof) {
-        long long t2 = clock64();
-        if (!t1) t1 = t0;
-        prof_wait += t1 - t0;
-        prof_work[path] += t2 - t1;
-        prof_n[path]++;
       }
     }
-    w = wn;
-    d = dn;
-    lg = lgn;
+    if (paired) {
+      w = next_of(wn);
+      fetch(w, d, lg);
+    } else {
+      w = wn;
+      d = dn;
+      lg = lgn;
+    }
   }
+  if (lane == 0 || lane == 16) wa_flush(T, W);  // both halves allocate in lean_pair16
   if (lane == 0) {
-    wa_flush(T, W);
     if (E.prof) {
       atomicAdd(E.prof, prof_wait);
       for (int k = 0; k < 5; k++) {
         atomicAdd(E.prof + 1 + k, prof_work[k]);
         atomicAdd(E.prof + 6 + k, prof_n[k]);
       }
+      atomicAdd(E.prof + 20, prof_work[5]);
+      atomicAdd(E.prof + 21, prof_n[5]);
       for (int k = 0; k < 3; k++) atomicAdd(E.prof + 11 + k, prof_lean[k]);
+      atomicAdd(E.prof + 14, prof_pool);
+      atomicAdd(E.prof + 15, prof_pages);
+      for (int k = 0; k < 4; k++) atomicAdd(E.prof + 16 + k, prof_smem[k]);
     }
   }
 }
