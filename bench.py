@@ -273,12 +273,23 @@ def main():
     h2d = a.nbytes() + b.nbytes()
     d2h = elements_step // world * 24
 
+    e2e_prof = os.environ.get("VEQ_E2E_PROF") == "1"
+
     def e2e_step():
+        tt = [time.perf_counter()]
         sess.declare_inputs(inputs)
+        tt.append(time.perf_counter())
         xa, xb = sess.load(a), sess.load(b)
+        tt.append(time.perf_counter())
         ra = sess.run_raw(xa)
+        tt.append(time.perf_counter())
         rb = sess.run_raw(xb)
+        tt.append(time.perf_counter())
         vc = sess.compare_raw(xa, xb, oa, ob)
+        tt.append(time.perf_counter())
+        if e2e_prof:
+            print("[e2e] declare %.2f load %.2f run_a %.2f run_b %.2f compare %.2f ms" %
+                  tuple(1000 * (tt[k + 1] - tt[k]) for k in range(5)), file=sys.stderr)
         assert vc.n_equal == vc.n_vcs
         if dist is not None:
             counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)

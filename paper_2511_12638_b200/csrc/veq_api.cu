@@ -39,6 +39,8 @@ struct BatchDev {
   std::vector<uint64_t> arr_cell_base;
   std::vector<uint64_t> thread_stmt;
   uint64_t n_stmts = 0, n_cells = 0, n_segs = 0, n_rel_cap = 0, n_regs = 0, n_access_max = 0;
+  uint64_t n_arith = 0;  // BinOp/UnOp statements: bound of the work list and chain logs
+  unsigned long long n_work_last = 0;  // work items of the last run (read back with its results)
   uint32_t n_threads = 0;
   unsigned int sched_flags = 0;  // written by k_prep_syncs (valid after the load's final sync)
   // device arrays (owned)
@@ -487,13 +489,15 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   }
   B.long_threads = d_long;
   unsigned int *d_flags = nullptr;
-  if ((r = dalloc(ctx, nullptr, &d_flags, 1))) {
+  unsigned long long *d_narith = nullptr;
+  if ((r = dalloc(ctx, nullptr, &d_flags, 1)) || (r = dalloc(ctx, nullptr, &d_narith, 1))) {
     delete bd;
     return r;
   }
   CK(cudaMemsetAsync(d_flags, 0, 4, s));
+  CK(cudaMemsetAsync(d_narith, 0, 8, s));
   PrepArgs PA{P, Tn, NS, d->n_arrays_total, S, B.progs, B.thread_stmt, B.thread_prog, B.stmts, B.sets, d_canon, d_pop,
-              d_cnt, ctx->error, B.set_words, d_flags, B.arrays};
+              d_cnt, ctx->error, B.set_words, d_flags, B.arrays, d_narith};
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), s));
   CK(cudaMemsetAsync(d_cnt + S, 0, 8, s));
   CK(cudaMemsetAsync(d_nlong, 0, 8, s));
@@ -508,8 +512,9 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     CK(cudaFreeAsync(tmp, s));
   }
   if (Tn) k_prep_long<<<blocks(Tn, 256), 256, 0, s>>>(PA, d_long, d_nlong, EXEC_WARP_MIN);
-  unsigned long long tot = 0, nlong = 0;
+  unsigned long long tot = 0, nlong = 0, narith = 0;
   int perr = 0;
+  CK(cudaMemcpyAsync(&narith, d_narith, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&tot, d_cnt + S, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&nlong, d_nlong, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&perr, ctx->error, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -527,6 +532,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
                                                    : "sync set index out of range");
   }
   const uint64_t n_syncs = tot & 0xffffffffull, n_access = tot >> 32;
+  bd->n_arith = narith;
   B.n_long = (uint32_t)nlong;
   bd->n_segs = (uint64_t)Tn + n_syncs;
   bd->n_rel_cap = n_syncs;
@@ -553,6 +559,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&bd->sched_flags, d_flags, 4, cudaMemcpyDeviceToHost, s));
   CK(cudaFreeAsync(d_flags, s));
+  CK(cudaFreeAsync(d_narith, s));
   CK(cudaFreeAsync(d_canon, s));
   CK(cudaFreeAsync(d_pop, s));
   CK(cudaFreeAsync(d_cnt, s));
@@ -694,11 +701,9 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMemsetAsync(n_starts, 0, 8, s));
     LAUNCH(k_seg_heads<<<blocks(n_tup, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(k2, n_tup, starts, n_starts, B.step_bits));
     PH1(VEQ_PH_SORT);
-    unsigned long long nseg = 0;
-    CK(cudaMemcpyAsync(&nseg, n_starts, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
     PH0(VEQ_PH_MEMSCAN);
-    if (nseg) LAUNCH(k_mem_scan<<<blocks(nseg, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, (uint32_t)nseg, n_tup, rs));
+    // one thread per segment head; the head count stays on the device
+    LAUNCH(k_mem_scan<<<blocks(n_tup, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, n_starts, n_tup, rs));
     PH1(VEQ_PH_MEMSCAN);
     CK(cudaGetLastError());
     CK(cudaFreeAsync(tmp, s));
@@ -734,11 +739,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaMallocAsync(&tmp, tb, s));
     cub::DeviceScan::ExclusiveSum(tmp, tb, sz, base, (int64_t)S, s);
     ctx->launches += 2;
-    uint32_t last_sz = 0, last_base = 0;
-    CK(cudaMemcpyAsync(&last_sz, sz + S - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&last_base, base + S - 1, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    uint64_t nlog = (uint64_t)last_sz + last_base;
+    // log capacity bound: a chain of L links has L + 1 entries <= 2L
+    const uint64_t nlog = 2 * bd->n_arith + 2;
     CK(cudaMallocAsync(&log, std::max<uint64_t>(nlog, 1) * 4, s));
     CK(cudaMallocAsync(&log_stmt, std::max<uint64_t>(nlog, 1) * 4, s));
     CK(cudaFreeAsync(tmp, s));
@@ -748,23 +750,26 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     PH0(VEQ_PH_WORKLIST);
     unsigned long long *wk = nullptr, *wk2 = nullptr, *nw = nullptr;
     uint32_t *wv = nullptr, *wv2 = nullptr;
-    CK(cudaMallocAsync(&wk, S * 8, s));
-    CK(cudaMallocAsync(&wk2, S * 8, s));
-    CK(cudaMallocAsync(&wv, S * 4, s));
-    CK(cudaMallocAsync(&wv2, S * 4, s));
+    // capacity U = BinOp/UnOp statements (static bound); unused slots keep
+    // key ~0 and sort last; the true length stays on the device
+    const uint64_t U = std::max<uint64_t>(bd->n_arith, 1);
+    CK(cudaMallocAsync(&wk, U * 8, s));
+    CK(cudaMallocAsync(&wk2, U * 8, s));
+    CK(cudaMallocAsync(&wv, U * 4, s));
+    CK(cudaMallocAsync(&wv2, U * 4, s));
     CK(cudaMallocAsync(&nw, 8, s));
     CK(cudaMemsetAsync(nw, 0, 8, s));
+    CK(cudaMemsetAsync(wk, 0xff, U * 8, s));
     LAUNCH(k_scatter_work<<<blocks(S, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
-    CK(cudaMemcpyAsync(&n_work, nw, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
     void *tmp2 = nullptr;
+    n_work = bd->n_arith;
     if (n_work) {
       // key = step << prog_bits | program: sort only the bits in use
       const int end_bit = (int)(B.prog_bits + B.step_bits);
       size_t tb2 = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, end_bit, s);
+      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
       CK(cudaMallocAsync(&tmp2, tb2, s));
-      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)n_work, 0, end_bit, s);
+      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
       ctx->launches += (end_bit + 7) / 8 + 1;
     }
     PH1(VEQ_PH_WORKLIST);
@@ -782,7 +787,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       EvalCtx E{log, log_stmt, base, prof};
       uint4 *desc = nullptr;
       CK(cudaMallocAsync(&desc, n_work * sizeof(uint4), s));
-      LAUNCH(k_make_desc<<<blocks(n_work, 256), 256, 0, s>>>(B, E, wv2, n_work, desc));
+      LAUNCH(k_make_desc<<<blocks(n_work, 256), 256, 0, s>>>(B, E, wv2, nw, desc));
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
       // one warp per work item, persistent over the sorted work list;
@@ -793,38 +798,12 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_warp, EVAL_BLOCK, smem);
       if (per_sm < 1) per_sm = 1;
       // every resident slot is launched (warps spread over all SMs); the
-      // claim size keeps all warps busy when the work list is short
+      // kernel reads the work-list length and picks its claim size
       uint64_t threads = (uint64_t)nsm * per_sm * EVAL_BLOCK;
-      const uint64_t warps = threads / 32;
-      const uint32_t grab = n_work >= warps * 16 ? 4 : (n_work >= warps * 4 ? 2 : 1);
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
-      LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, desc, n_work, cursor,
+      LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, desc, nw, cursor,
                                                                                 ctx->pool, ctx->pool_used,
-                                                                                ctx->pool_cap, chunk, grab));
-      CK(cudaFreeAsync(desc, s));
-      if (prof) {
-        unsigned long long hp[32];
-        CK(cudaMemcpyAsync(hp, prof, 32 * 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        fprintf(stderr, "[veq prof] items %llu warps %llu grab %u | wait %.1f us/item |", (unsigned long long)n_work,
-                (unsigned long long)warps, grab, hp[0] / 1965.0 / std::max<double>(1, n_work));
-        const char *nm[5] = {"other", "lean", "smem", "small", "global"};
-        for (int k = 0; k < 5; k++)
-          if (hp[6 + k]) fprintf(stderr, " %s n=%llu %.2f us", nm[k], hp[6 + k], hp[1 + k] / 1965.0 / hp[6 + k]);
-        if (hp[7])
-          fprintf(stderr, " | lean phases: loads %.2f sort %.2f intern %.2f us", hp[11] / 1965.0 / hp[7],
-                  hp[12] / 1965.0 / hp[7], hp[13] / 1965.0 / hp[7]);
-        if (hp[21] || hp[24] || hp[25] || hp[26] || hp[27] || hp[28])
-          fprintf(stderr, " | pairs: %llu items %.2f us per item; fallbacks skip %llu m>16 %llu coef %llu consts %llu ties %llu",
-                  hp[21], hp[20] / 1965.0 / std::max<unsigned long long>(1, hp[21]), hp[24], hp[25], hp[26], hp[27],
-                  hp[28]);
-        if (hp[8])
-          fprintf(stderr, " | smem: pool wait %.2f us/item, %.1f pages/item; runs %.2f gather %.2f merge %.2f intern %.2f us",
-                  hp[14] / 1965.0 / hp[8], (double)hp[15] / hp[8], hp[16] / 1965.0 / hp[8], hp[17] / 1965.0 / hp[8],
-                  hp[18] / 1965.0 / hp[8], hp[19] / 1965.0 / hp[8]);
-        fprintf(stderr, "\n");
-        CK(cudaFreeAsync(prof, s));
-      }
+                                                                                ctx->pool_cap, chunk));
       CK(cudaGetLastError());
       CK(cudaFreeAsync(tmp2, s));
       CK(cudaFreeAsync(cursor, s));
@@ -834,6 +813,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     CK(cudaFreeAsync(wk2, s));
     CK(cudaFreeAsync(wv, s));
     CK(cudaFreeAsync(wv2, s));
+    CK(cudaMemcpyAsync(&bd->n_work_last, nw, 8, cudaMemcpyDeviceToHost, s));  // valid after the final sync
     CK(cudaFreeAsync(nw, s));
   }
   PH0(VEQ_PH_FINALS);
@@ -903,7 +883,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     out->thread_block_stmt = bd->th_bstmt.data();
     out->n_nodes = nn[0] - nn[4];
     out->n_kid_words = nn[1] - nn[5];
-    out->n_work = n_work;
+    out->n_work = bd->n_work_last;
     out->n_access = n_tup;
     uint64_t executed = 0;
     for (uint32_t p = 0; p < P; p++) executed += bd->res[p].steps - bd->res[p].releases;

@@ -162,6 +162,7 @@ struct PrepArgs {
   const uint64_t *set_words;
   unsigned int *sched_flags;  // bit 0: some sync set does not suit k_schedule_warp
   const veq_array *arrays;
+  unsigned long long *n_arith;  // BinOp/UnOp statements: bound of the work list
 };
 
 __device__ __forceinline__ uint32_t thread_of_stmt(const uint64_t *thread_stmt, uint32_t n_threads, uint64_t i) {
@@ -183,6 +184,9 @@ __global__ void k_prep_thread_prog(PrepArgs A, uint32_t *thread_prog) {
 // per statement: validation and the (sync, access) counts to scan
 __global__ void k_prep_stmts(PrepArgs A) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool arith = i < A.n_stmts && (A.stmts[i].kind == VEQ_ST_BINOP || A.stmts[i].kind == VEQ_ST_UNOP);
+  const int na = __syncthreads_count(arith);
+  if (threadIdx.x == 0 && na) atomicAdd(A.n_arith, (unsigned long long)na);
   if (i >= A.n_stmts) return;
   const veq_stmt st = A.stmts[i];
   unsigned long long c = 0;
@@ -1276,7 +1280,9 @@ struct Reader {
 
 // One thread per address segment [s, e) of the (cell, step)-sorted tuples.
 __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, const unsigned long long *vals,
-                           const uint32_t *seg_starts, uint32_t n_segs, uint64_t n_tup, Reader *rscratch) {
+                           const uint32_t *seg_starts, const unsigned long long *n_segs_dev, uint64_t n_tup,
+                           Reader *rscratch) {
+  const uint64_t n_segs = *n_segs_dev;  // device-side count: no host read-back
   uint32_t sidx = blockIdx.x * blockDim.x + threadIdx.x;
   if (sidx >= n_segs) return;
   const uint64_t s = seg_starts[sidx];
@@ -1727,9 +1733,10 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
 // Work descriptor per sorted item: statement, chain-log base and leaf count
 // (chain Adds), statement kind and op — one 16-byte load replaces the
 // stmts -> chain_head/pos -> log_base chain of dependent reads.
-__global__ void k_make_desc(Batch B, EvalCtx E, const uint32_t *work, uint64_t n_work, uint4 *desc) {
+__global__ void k_make_desc(Batch B, EvalCtx E, const uint32_t *work, const unsigned long long *n_work_dev,
+                            uint4 *desc) {
   uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= n_work) return;
+  if (w >= *n_work_dev) return;
   const uint32_t i = work[w];
   const veq_stmt st = B.stmts[i];
   uint4 d{i, 0u, 0u, (uint32_t)st.kind | ((uint32_t)st.op << 8)};
@@ -1754,9 +1761,15 @@ __device__ __forceinline__ bool desc_is_add(const uint4 &d) {
 // block with a 108 KB page pool).
 constexpr uint32_t EVAL_BLOCK = 512, EVAL_PAGES = 27;
 __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
-                                                             uint64_t n_work, unsigned long long *cursor, char *pool,
+                                                             const unsigned long long *n_work_dev,
+                                                             unsigned long long *cursor, char *pool,
                                                              unsigned long long *pool_used, uint64_t pool_cap,
-                                                             uint64_t chunk, uint32_t grab) {
+                                                             uint64_t chunk) {
+  // work-list length and claim size from the device (no host read-back):
+  // a short list is claimed one item at a time so it spreads over all warps
+  const uint64_t n_work = *n_work_dev;
+  const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t grab = n_work >= warps_total * 16 ? 4 : (n_work >= warps_total * 4 ? 2 : 1);
   extern __shared__ __align__(16) char eval_smem[];
   __shared__ uint32_t s_mask;
   if (threadIdx.x == 0) s_mask = 0;
