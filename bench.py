@@ -277,6 +277,8 @@ def main():
 
     def e2e_step():
         tt = [time.perf_counter()]
+        if e2e_prof:
+            L.veq_set_timing(sess.ctx, 1)
         sess.declare_inputs(inputs)
         tt.append(time.perf_counter())
         xa, xb = sess.load(a), sess.load(b)
@@ -289,7 +291,8 @@ def main():
         tt.append(time.perf_counter())
         if e2e_prof:
             print("[e2e] declare %.2f load %.2f run_a %.2f run_b %.2f compare %.2f ms" %
-                  tuple(1000 * (tt[k + 1] - tt[k]) for k in range(5)), file=sys.stderr)
+                  tuple(1000 * (tt[k + 1] - tt[k]) for k in range(5)), "| run_b phases",
+                  " ".join("%s=%.2f" % (nm, rb.phase_ms[i]) for i, nm in enumerate(N.PHASES)), file=sys.stderr)
         assert vc.n_equal == vc.n_vcs
         if dist is not None:
             counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)

@@ -61,6 +61,10 @@ struct BatchDev {
 
 struct veq_ctx {
   int device = 0;
+  // grow-only run workspace: one slot per veq_run/veq_compare temporary, so
+  // steady-state runs make no allocation at all (cudaMalloc only when a
+  // slot grows; runs on the ctx's single stream never overlap)
+  std::vector<std::pair<void *, size_t>> ws;
   cudaStream_t stream = nullptr;
   std::string last_error;
   Table T{};
@@ -107,6 +111,22 @@ int fail(veq_ctx *c, int code, const std::string &msg) {
     cudaError_t e_ = (call);                                                           \
     if (e_ != cudaSuccess) return fail(ctx, VEQ_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
   } while (0)
+
+int ws_get(veq_ctx *ctx, int slot, void **out, size_t bytes) {
+  if ((int)ctx->ws.size() <= slot) ctx->ws.resize(slot + 1, {nullptr, 0});
+  auto &w = ctx->ws[slot];
+  bytes = std::max<size_t>(bytes, 256);
+  if (w.second < bytes) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(w.first);
+    w = {nullptr, 0};
+    size_t cap = bytes + bytes / 8;
+    if (cudaMalloc(&w.first, cap) != cudaSuccess) return fail(ctx, VEQ_E_OOM, "run workspace");
+    w.second = cap;
+  }
+  *out = w.first;
+  return VEQ_OK;
+}
 
 template <class X> int dalloc(veq_ctx *ctx, BatchDev *bd, X **out, size_t n) {
   void *p = nullptr;
@@ -238,6 +258,7 @@ void veq_close(veq_ctx *ctx) {
   cudaFree(ctx->in_base);
   cudaFree(ctx->in_size);
   cudaFree(ctx->in_cache);
+  for (auto &w : ctx->ws) cudaFree(w.first);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -684,18 +705,18 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     uint32_t *starts = nullptr;
     unsigned long long *n_starts = nullptr;
     Reader *rs = nullptr;
-    CK(cudaMallocAsync(&k2, n_tup * 8, s));
-    CK(cudaMallocAsync(&v2, n_tup * 8, s));
-    CK(cudaMallocAsync(&starts, n_tup * 4, s));
-    CK(cudaMallocAsync(&n_starts, 8, s));
-    CK(cudaMallocAsync(&rs, n_tup * sizeof(Reader), s));
+    { int r_ = ws_get(ctx, 1, (void **)&k2, n_tup * 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 2, (void **)&v2, n_tup * 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 3, (void **)&starts, n_tup * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 4, (void **)&n_starts, 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 5, (void **)&rs, n_tup * sizeof(Reader)); if (r_) return r_; }
     int cb = 1;
     while ((1ull << cb) < bd->n_cells + 1) cb++;
     int end_bit = (int)B.step_bits + cb;
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
     void *tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, tmp_bytes, s));
+    { int r_ = ws_get(ctx, 6, (void **)&tmp, tmp_bytes); if (r_) return r_; }
     cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, B.tup_key, k2, B.tup_val, v2, (int64_t)n_tup, 0, end_bit, s);
     ctx->launches += (end_bit + 7) / 8 + 1;
     CK(cudaMemsetAsync(n_starts, 0, 8, s));
@@ -706,13 +727,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     LAUNCH(k_mem_scan<<<blocks(n_tup, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, n_starts, n_tup, rs));
     PH1(VEQ_PH_MEMSCAN);
     CK(cudaGetLastError());
-    CK(cudaFreeAsync(tmp, s));
-    CK(cudaFreeAsync(k2, s));
-    CK(cudaFreeAsync(v2, s));
-    CK(cudaFreeAsync(starts, s));
-    CK(cudaFreeAsync(n_starts, s));
-    CK(cudaFreeAsync(rs, s));
-  } else {
+                          } else {
     PH1(VEQ_PH_SORT);
     PH0(VEQ_PH_MEMSCAN);
     PH1(VEQ_PH_MEMSCAN);
@@ -723,8 +738,8 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   unsigned long long n_work = 0;
   PH0(VEQ_PH_RESOLVE);
   if (S) {
-    CK(cudaMallocAsync(&sz, S * 4, s));
-    CK(cudaMallocAsync(&base, S * 4, s));
+    { int r_ = ws_get(ctx, 7, (void **)&sz, S * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 8, (void **)&base, S * 4); if (r_) return r_; }
     LAUNCH(k_resolve_all<<<blocks(S, 256), 256, 0, s>>>(B, sz));
   }
   if (bd->n_cells) LAUNCH(k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
@@ -736,15 +751,14 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, base, (int64_t)S, s);
     void *tmp = nullptr;
-    CK(cudaMallocAsync(&tmp, tb, s));
+    { int r_ = ws_get(ctx, 9, (void **)&tmp, tb); if (r_) return r_; }
     cub::DeviceScan::ExclusiveSum(tmp, tb, sz, base, (int64_t)S, s);
     ctx->launches += 2;
     // log capacity bound: a chain of L links has L + 1 entries <= 2L
     const uint64_t nlog = 2 * bd->n_arith + 2;
-    CK(cudaMallocAsync(&log, std::max<uint64_t>(nlog, 1) * 4, s));
-    CK(cudaMallocAsync(&log_stmt, std::max<uint64_t>(nlog, 1) * 4, s));
-    CK(cudaFreeAsync(tmp, s));
-    PH1(VEQ_PH_CHAINS);
+    { int r_ = ws_get(ctx, 10, (void **)&log, std::max<uint64_t>(nlog, 1) * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 11, (void **)&log_stmt, std::max<uint64_t>(nlog, 1) * 4); if (r_) return r_; }
+        PH1(VEQ_PH_CHAINS);
     // chain-log entries and the work list, one pass; work sorted by
     // (step, program)
     PH0(VEQ_PH_WORKLIST);
@@ -753,11 +767,11 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     // capacity U = BinOp/UnOp statements (static bound); unused slots keep
     // key ~0 and sort last; the true length stays on the device
     const uint64_t U = std::max<uint64_t>(bd->n_arith, 1);
-    CK(cudaMallocAsync(&wk, U * 8, s));
-    CK(cudaMallocAsync(&wk2, U * 8, s));
-    CK(cudaMallocAsync(&wv, U * 4, s));
-    CK(cudaMallocAsync(&wv2, U * 4, s));
-    CK(cudaMallocAsync(&nw, 8, s));
+    { int r_ = ws_get(ctx, 12, (void **)&wk, U * 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 13, (void **)&wk2, U * 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 14, (void **)&wv, U * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 15, (void **)&wv2, U * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 16, (void **)&nw, 8); if (r_) return r_; }
     CK(cudaMemsetAsync(nw, 0, 8, s));
     CK(cudaMemsetAsync(wk, 0xff, U * 8, s));
     LAUNCH(k_scatter_work<<<blocks(S, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
@@ -768,7 +782,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       const int end_bit = (int)(B.prog_bits + B.step_bits);
       size_t tb2 = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
-      CK(cudaMallocAsync(&tmp2, tb2, s));
+      { int r_ = ws_get(ctx, 17, (void **)&tmp2, tb2); if (r_) return r_; }
       cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
       ctx->launches += (end_bit + 7) / 8 + 1;
     }
@@ -776,17 +790,17 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     PH0(VEQ_PH_EVAL);
     if (n_work) {
       unsigned long long *cursor = nullptr;
-      CK(cudaMallocAsync(&cursor, 8, s));
+      { int r_ = ws_get(ctx, 18, (void **)&cursor, 8); if (r_) return r_; }
       CK(cudaMemsetAsync(cursor, 0, 8, s));
       static const bool prof_on = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
       unsigned long long *prof = nullptr;
       if (prof_on) {
-        CK(cudaMallocAsync(&prof, 32 * 8, s));
+        { int r_ = ws_get(ctx, 19, (void **)&prof, 32 * 8); if (r_) return r_; }
         CK(cudaMemsetAsync(prof, 0, 32 * 8, s));
       }
       EvalCtx E{log, log_stmt, base, prof};
       uint4 *desc = nullptr;
-      CK(cudaMallocAsync(&desc, n_work * sizeof(uint4), s));
+      { int r_ = ws_get(ctx, 20, (void **)&desc, n_work * sizeof(uint4)); if (r_) return r_; }
       LAUNCH(k_make_desc<<<blocks(n_work, 256), 256, 0, s>>>(B, E, wv2, nw, desc));
       int nsm = 148;
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -805,27 +819,16 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
                                                                                 ctx->pool, ctx->pool_used,
                                                                                 ctx->pool_cap, chunk));
       CK(cudaGetLastError());
-      CK(cudaFreeAsync(tmp2, s));
-      CK(cudaFreeAsync(cursor, s));
-    }
+                }
     PH1(VEQ_PH_EVAL);
-    CK(cudaFreeAsync(wk, s));
-    CK(cudaFreeAsync(wk2, s));
-    CK(cudaFreeAsync(wv, s));
-    CK(cudaFreeAsync(wv2, s));
-    CK(cudaMemcpyAsync(&bd->n_work_last, nw, 8, cudaMemcpyDeviceToHost, s));  // valid after the final sync
-    CK(cudaFreeAsync(nw, s));
-  }
+                    CK(cudaMemcpyAsync(&bd->n_work_last, nw, 8, cudaMemcpyDeviceToHost, s));  // valid after the final sync
+      }
   PH0(VEQ_PH_FINALS);
   if (bd->n_cells) LAUNCH(k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
   PH1(VEQ_PH_FINALS);
   CK(cudaGetLastError());
   if (sz) {
-    CK(cudaFreeAsync(sz, s));
-    CK(cudaFreeAsync(base, s));
-    CK(cudaFreeAsync(log, s));
-    CK(cudaFreeAsync(log_stmt, s));
-  }
+                  }
   // ---- results to host
   const uint32_t P = B.n_progs;
   std::vector<uint32_t> nrel(P);
@@ -929,12 +932,12 @@ int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, c
   veq_vc *dv = nullptr;
   unsigned long long *cnt = nullptr;
   uint64_t sc_cap = std::max<uint64_t>(nv * 2, 1024);
-  CK(cudaMallocAsync(&dca, std::max<uint64_t>(nv, 1) * 4, s));
-  CK(cudaMallocAsync(&dcb, std::max<uint64_t>(nv, 1) * 4, s));
-  CK(cudaMallocAsync(&dv, std::max<uint64_t>(nv, 1) * sizeof(veq_vc), s));
-  CK(cudaMallocAsync(&scn, sc_cap * 4, s));
-  CK(cudaMallocAsync(&scd, sc_cap, s));
-  CK(cudaMallocAsync(&cnt, 3 * 8, s));
+  { int r_ = ws_get(ctx, 21, (void **)&dca, std::max<uint64_t>(nv, 1) * 4); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 22, (void **)&dcb, std::max<uint64_t>(nv, 1) * 4); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 23, (void **)&dv, std::max<uint64_t>(nv, 1) * sizeof(veq_vc)); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 24, (void **)&scn, sc_cap * 4); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 25, (void **)&scd, sc_cap); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 26, (void **)&cnt, 3 * 8); if (r_) return r_; }
   CK(cudaMemsetAsync(cnt, 0, 24, s));
   CK(cudaMemsetAsync(ctx->pool_used, 0, 8, s));
   if (nv) {
@@ -958,13 +961,7 @@ int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, c
     CK(cudaMemcpyAsync(ctx->sc_node.data(), scn, nsc * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(ctx->sc_dis.data(), scd, nsc, cudaMemcpyDeviceToHost, s));
   }
-  CK(cudaFreeAsync(dca, s));
-  CK(cudaFreeAsync(dcb, s));
-  CK(cudaFreeAsync(dv, s));
-  CK(cudaFreeAsync(scn, s));
-  CK(cudaFreeAsync(scd, s));
-  CK(cudaFreeAsync(cnt, s));
-  CK(cudaStreamSynchronize(s));
+              CK(cudaStreamSynchronize(s));
   int er = check_error_flag(ctx);
   if (er) return er;
   if (h[0] > sc_cap) return fail(ctx, VEQ_E_BUDGET, "side-condition buffer overflow");
