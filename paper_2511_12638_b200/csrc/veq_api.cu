@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -360,8 +361,18 @@ int veq_set_timing(veq_ctx *ctx, int on) {
   return VEQ_OK;
 }
 
+// Frees a batch's device buffers (stream-ordered) and the batch itself.
+void drop_batch(veq_ctx *ctx, BatchDev *bd) {
+  for (void *p : bd->owned) cudaFreeAsync(p, ctx->stream);
+  delete bd;
+}
+
 int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   if (!ctx || !d || !out) return VEQ_E_ARG;
+  static const bool lprof = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto lt0 = now();
   CK(cudaSetDevice(ctx->device));
   const uint32_t P = d->n_progs, Tn = d->n_threads_total;
   const uint64_t S = d->n_stmts;
@@ -370,9 +381,33 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   BatchDev *bd = new BatchDev();
   bd->progs.assign(d->progs, d->progs + P);
   bd->arrays.assign(d->arrays, d->arrays + d->n_arrays_total);
-  bd->thread_stmt.assign(d->thread_stmt, d->thread_stmt + Tn + 1);
   bd->n_stmts = S;
   bd->n_threads = Tn;
+  Batch &B = bd->B;
+  B.n_progs = P;
+  B.n_threads = Tn;
+  B.n_stmts = S;
+  int r = 0;
+  cudaStream_t s = ctx->stream;
+#define UP(field, src, n, T_)                                                            \
+  do {                                                                                   \
+    T_ *p_ = nullptr;                                                                    \
+    if ((r = dupload(ctx, bd, &p_, (const T_ *)(src), (n)))) { drop_batch(ctx, bd); return r; }   \
+    B.field = p_;                                                                        \
+  } while (0)
+#define AL(field, n, T_)                                                  \
+  do {                                                                    \
+    T_ *p_ = nullptr;                                                     \
+    if ((r = dalloc(ctx, bd, &p_, (n)))) { drop_batch(ctx, bd); return r; }        \
+    B.field = p_;                                                         \
+  } while (0)
+  // the caller's big buffers go first: their DMA overlaps the host
+  // preparation below (async when the caller's memory is pinned)
+  UP(stmts, d->stmts, S, veq_stmt);
+  UP(thread_stmt, d->thread_stmt, Tn + 1, uint64_t);
+  UP(progs, d->progs, P, veq_program_meta);
+  UP(arrays, d->arrays, d->n_arrays_total, veq_array);
+  UP(set_words, d->set_words, d->n_set_words, uint64_t);
   // ---- host preparation (per program / array / pool entry only): program
   // ranges, register offsets, sync-set pool canonicalisation, cell bases.
   // Everything per statement runs on the device (k_prep_*).
@@ -380,13 +415,13 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   for (uint32_t p = 0; p < P; p++) {
     const veq_program_meta &m = d->progs[p];
     if ((uint64_t)m.thread_off + m.n_threads > Tn || (uint64_t)m.array_off + m.n_arrays > d->n_arrays_total) {
-      delete bd;
+      drop_batch(ctx, bd);
       return fail(ctx, VEQ_E_INVALID_IR, "program " + std::to_string(p) + " out of range");
     }
   }
   for (uint32_t t = 0; t < Tn; t++) {
     if (d->thread_stmt[t + 1] < d->thread_stmt[t] || d->thread_stmt[t + 1] > S) {
-      delete bd;
+      drop_batch(ctx, bd);
       return fail(ctx, VEQ_E_INVALID_IR, "thread statement ranges are not monotone");
     }
     reg_off[t + 1] = reg_off[t] + d->thread_nregs[t];
@@ -406,7 +441,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
       key.assign(reinterpret_cast<const char *>(&q.full), 4);
       if (!q.full) {
         if ((uint64_t)q.word_off + (q.n_bits + 63) / 64 > d->n_set_words) {
-          delete bd;
+          drop_batch(ctx, bd);
           return fail(ctx, VEQ_E_INVALID_IR, "sync set words out of range");
         }
         key.append(reinterpret_cast<const char *>(&q.lo), 8);
@@ -427,7 +462,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     const veq_array &ar = d->arrays[a];
     bool direct = !(ar.flags & VEQ_ARR_STORED) && ar.input >= 0 && ar.seeded >= ar.size;
     if (ar.input >= (int32_t)ctx->input_names.size()) {
-      delete bd;
+      drop_batch(ctx, bd);
       return fail(ctx, VEQ_E_INVALID_IR, "array refers to an undeclared input");
     }
     if (!direct) {
@@ -436,7 +471,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     }
   }
   if (cells >= (1ull << 32)) {
-    delete bd;
+    drop_batch(ctx, bd);
     return fail(ctx, VEQ_E_UNSUPPORTED, "more than 2^32 checked memory cells in one batch");
   }
   bd->arr_cell_base = cell_base;
@@ -466,38 +501,17 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     bd->B.step_bits = sb;
     bd->B.prog_bits = pb;
   }
+  const auto lt1 = now();
   // ---- upload
-  Batch &B = bd->B;
-  B.n_progs = P;
-  B.n_threads = Tn;
-  B.n_stmts = S;
-  B.n_cells = cells;
-  int r = 0;
-  cudaStream_t s = ctx->stream;
-#define UP(field, src, n, T_)                                                            \
-  do {                                                                                   \
-    T_ *p_ = nullptr;                                                                    \
-    if ((r = dupload(ctx, bd, &p_, (const T_ *)(src), (n)))) { delete bd; return r; }   \
-    B.field = p_;                                                                        \
-  } while (0)
-#define AL(field, n, T_)                                                  \
-  do {                                                                    \
-    T_ *p_ = nullptr;                                                     \
-    if ((r = dalloc(ctx, bd, &p_, (n)))) { delete bd; return r; }        \
-    B.field = p_;                                                         \
-  } while (0)
-  UP(progs, d->progs, P, veq_program_meta);
-  UP(thread_stmt, d->thread_stmt, Tn + 1, uint64_t);
-  UP(stmts, d->stmts, S, veq_stmt);
-  UP(arrays, d->arrays, d->n_arrays_total, veq_array);
   UP(arr_cell_base, cell_base.data(), cell_base.size(), uint64_t);
+  B.n_cells = cells;
   UP(sets, sets.data(), sets.size(), veq_syncset);
-  UP(set_words, d->set_words, d->n_set_words, uint64_t);
   UP(reg_off, reg_off.data(), Tn + 1, uint64_t);
   if (in_order && P) UP(prog_stmt, prog_stmt.data(), P + 1, uint64_t);
   else B.prog_stmt = nullptr;
   AL(thread_prog, Tn, uint32_t);
   AL(prog_full_set, P, uint32_t);
+  const auto lt2 = now();
   // ---- device preparation
   uint32_t *d_canon = nullptr, *d_pop = nullptr, *d_long = nullptr;
   unsigned long long *d_cnt = nullptr, *d_nlong = nullptr;
@@ -505,14 +519,14 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   if ((r = dupload(ctx, nullptr, &d_canon, set_canon.data(), NS)) || (r = dupload(ctx, nullptr, &d_pop, set_pop.data(), NS)) ||
       (r = dalloc(ctx, nullptr, &d_cnt, S + 1)) || (r = dalloc(ctx, nullptr, &d_nlong, 1)) ||
       (r = dalloc(ctx, nullptr, &d_psync, P + 1)) || (r = dalloc(ctx, bd, &d_long, Tn))) {
-    delete bd;
+    drop_batch(ctx, bd);
     return r;
   }
   B.long_threads = d_long;
   unsigned int *d_flags = nullptr;
   unsigned long long *d_narith = nullptr;
   if ((r = dalloc(ctx, nullptr, &d_flags, 1)) || (r = dalloc(ctx, nullptr, &d_narith, 1))) {
-    delete bd;
+    drop_batch(ctx, bd);
     return r;
   }
   CK(cudaMemsetAsync(d_flags, 0, 4, s));
@@ -547,11 +561,12 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
     cudaFreeAsync(d_nlong, s);
     cudaFreeAsync(d_psync, s);
     cudaMemsetAsync(ctx->error, 0, sizeof(int), s);
-    delete bd;
+    drop_batch(ctx, bd);
     return fail(ctx, VEQ_E_INVALID_IR, perr == 1 ? "bad statement kind"
                                        : perr == 2 ? "array index out of range"
                                                    : "sync set index out of range");
   }
+  const auto lt3 = now();
   const uint64_t n_syncs = tot & 0xffffffffull, n_access = tot >> 32;
   bd->n_arith = narith;
   B.n_long = (uint32_t)nlong;
@@ -589,7 +604,7 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   uint32_t *cn = nullptr;
   veq_rat *dconsts = nullptr;
   if ((r = dalloc(ctx, bd, &cn, d->n_consts)) || (r = dupload(ctx, bd, &dconsts, d->consts, d->n_consts))) {
-    delete bd;
+    drop_batch(ctx, bd);
     return r;
   }
   B.const_node = cn;
@@ -628,7 +643,11 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
 #undef UP
   ctx->batches.push_back(bd);
   *out = (uint32_t)(ctx->batches.size() - 1);
-  return check_error_flag(ctx);
+  const int rc = check_error_flag(ctx);
+  if (lprof)
+    fprintf(stderr, "[veq load] S=%llu host prep %.2f upload-issue %.2f device prep+sync %.2f rest %.2f ms\n",
+            (unsigned long long)S, ms(lt0, lt1), ms(lt1, lt2), ms(lt2, lt3), ms(lt3, now()));
+  return rc;
 }
 
 int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
