@@ -1435,25 +1435,6 @@ __device__ __forceinline__ uint32_t chase(const Batch &B, uint32_t r) {
   return r;
 }
 
-__global__ void k_resolve(Batch B) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  if (B.st_step[i] == UNSET) return;
-  veq_stmt st = B.stmts[i];
-  if (st.kind == VEQ_ST_BINOP) {
-    uint32_t a = chase(B, B.ref_a[i]), b = chase(B, B.ref_b[i]);
-    B.ref_a[i] = a;
-    B.ref_b[i] = b;
-  } else if (st.kind == VEQ_ST_UNOP || st.kind == VEQ_ST_STORE) {
-    B.ref_a[i] = chase(B, B.ref_a[i]);
-  }
-}
-__global__ void k_resolve_loads(Batch B) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  if (B.st_step[i] == UNSET) return;
-  if (B.stmts[i].kind == VEQ_ST_LOAD) B.ref_a[i] = chase(B, B.ref_a[i]);
-}
 __global__ void k_resolve_finals(Batch B) {
   uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= B.n_cells) return;
@@ -1462,49 +1443,6 @@ __global__ void k_resolve_finals(Batch B) {
   v = chase(B, v);
   B.final_val[c] = v;
   if (is_stmt_ref(v)) atomicAdd(B.uses + v, 1u);
-}
-
-__global__ void k_count_uses(Batch B) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  if (B.st_step[i] == UNSET) return;
-  veq_stmt st = B.stmts[i];
-  if (st.kind == VEQ_ST_BINOP) {
-    uint32_t a = B.ref_a[i], b = B.ref_b[i];
-    if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
-    if (is_stmt_ref(b)) atomicAdd(B.uses + b, 1u);
-  } else if (st.kind == VEQ_ST_UNOP) {
-    uint32_t a = B.ref_a[i];
-    if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
-  }
-}
-
-__device__ __forceinline__ bool is_chain_op(const veq_stmt &st) {
-  return st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX);
-}
-// chain leaf count of the head (for the log scan); 0 elsewhere
-__global__ void k_chain_sizes(Batch B, uint32_t *sz) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  uint32_t v = 0;
-  if (B.st_step[i] != UNSET && is_chain_op(B.stmts[i]) && B.chain_head[i] == (uint32_t)i) v = B.chain_len[i] + 1;
-  sz[i] = v;
-}
-__global__ void k_chain_scatter(Batch B, const uint32_t *base, uint32_t *log, uint32_t *log_stmt) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  if (B.st_step[i] == UNSET || !is_chain_op(B.stmts[i])) return;
-  uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
-  uint32_t b = base[h];
-  if (pos == 0) {
-    log[b] = B.ref_a[i];
-    log[b + 1] = B.ref_b[i];
-    log_stmt[b] = (uint32_t)i;
-    log_stmt[b + 1] = (uint32_t)i;
-  } else {
-    log[b + pos + 1] = B.ref_b[i];
-    log_stmt[b + pos + 1] = (uint32_t)i;
-  }
 }
 
 // Input symbols read by direct loads (never-stored input arrays) are
@@ -1521,6 +1459,10 @@ __global__ void k_pre_inputs(Batch B, Table T) {
   if (off < 0 || (uint64_t)off >= arr.size) return;
   if (!(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 && (uint32_t)off < arr.seeded)
     B.canon[i] = intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
+}
+
+__device__ __forceinline__ bool is_chain_op(const veq_stmt &st) {
+  return st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX);
 }
 
 // One pass after the memory scan: operands resolved through loads, use
@@ -1589,30 +1531,6 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
     wval[o] = (uint32_t)i;
     o++;
   }
-}
-
-// work items: every executed BinOp/UnOp except chain links absorbed by
-// their successor (continued and used exactly once).
-__global__ void k_make_work(Batch B, unsigned long long *wkey, uint32_t *wval, unsigned long long *n_work) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts) return;
-  if (B.st_step[i] == UNSET) return;
-  veq_stmt st = B.stmts[i];
-  if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) return;
-  if (is_chain_op(st) && B.continued[i] && B.uses[i] == 1) return;
-  // program of statement: binary search on thread_stmt
-  uint32_t lo = 0, hi = B.n_threads;
-  while (hi - lo > 1) {
-    uint32_t mid = (lo + hi) / 2;
-    if (B.thread_stmt[mid] <= i) lo = mid;
-    else hi = mid;
-  }
-  uint32_t p = B.thread_prog[lo];
-  unsigned long long slot = agg_inc(n_work);
-  // (step, program): every dependency of an item has a smaller step in the
-  // same program, hence a smaller key, and all CTAs advance together
-  wkey[slot] = ((unsigned long long)B.st_step[i] << B.prog_bits) | p;
-  wval[slot] = (uint32_t)i;
 }
 
 // ---------------------------------------------------------------------------
