@@ -580,6 +580,9 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   k_prep_threads<<<blocks((uint64_t)Tn + 1, 256), 256, 0, s>>>(PA, (uint64_t *)B.seg_off, (uint64_t *)B.seg_start,
                                                                (uint32_t *)B.seg_set);
   if (S) k_prep_syncs<<<blocks(S, 256), 256, 0, s>>>(PA, (uint64_t *)B.seg_start, (uint32_t *)B.seg_set);
+  AL(set_chunk, (uint64_t)NS + 1, unsigned long long);
+  k_prep_set_chunks<<<blocks((uint64_t)NS + 1, 256), 256, 0, s>>>(B.sets, B.set_words, NS,
+                                                                   (unsigned long long *)B.set_chunk);
   if (P) {
     k_prep_progs<<<blocks(P, 256), 256, 0, s>>>(PA, d_psync, (uint32_t *)B.prog_full_set);
     CK(cudaMemsetAsync(d_psync + P, 0, 8, s));

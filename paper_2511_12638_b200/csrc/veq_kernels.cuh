@@ -51,6 +51,7 @@ struct Batch {
   uint32_t n_long;
   const uint64_t *prog_stmt;  // [P+1] first statement of each program when programs are laid out in order, else null
   uint32_t step_bits, prog_bits;  // widths of step / program fields in the sort keys
+  const unsigned long long *set_chunk;  // per set: (32-thread chunk << 32) | member mask in it; ~0: not one chunk
   // run state
   uint32_t *seg_base;
   uint32_t *rel_step, *rel_set;
@@ -250,6 +251,21 @@ __global__ void k_prep_syncs(PrepArgs A, uint64_t *seg_start, uint32_t *seg_set)
     const bool chunk = q.n_bits == 0 || q.lo / 32 == (q.lo + q.n_bits - 1) / 32;
     if (!member || !chunk) atomicOr(A.sched_flags, 1u);
   }
+}
+
+// per sync set: the aligned 32-thread chunk holding its window and the
+// member mask inside it (k_schedule_warp decides releases from it)
+__global__ void k_prep_set_chunks(const veq_syncset *sets, const uint64_t *set_words, uint32_t n,
+                                  unsigned long long *set_chunk) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const veq_syncset q = sets[i];
+  unsigned long long v = ~0ull;
+  if (!q.full && q.n_bits && q.lo / 32 == (q.lo + q.n_bits - 1) / 32) {
+    const uint64_t bits = set_words[q.word_off] & (q.n_bits >= 64 ? ~0ull : ((1ull << q.n_bits) - 1));
+    v = ((unsigned long long)(q.lo / 32) << 32) | (uint32_t)(bits << (q.lo % 32));
+  }
+  set_chunk[i] = v;
 }
 
 // per program: sync count (release capacity) for the rel_off scan
@@ -674,7 +690,10 @@ __global__ void __launch_bounds__(1024, 2) k_schedule_lanes(Batch B) {
 // end and set are prefetched when it blocks.
 constexpr uint32_t SW_WARPS = 4;
 struct SchedWarpSmem {
-  uint32_t bs[1024], sj[1024], so[1024], cs[1024], ns[1024], nset[1024];
+  // per thread: blocked set and its member mask (in the thread's chunk); the
+  // segment to run next (index relative to the CTA's first segment), its
+  // length, the set ending it and that set's mask
+  uint32_t bs[1024], bm[1024], cj[1024], len[1024], nset[1024], nm[1024];
   uint8_t st[1024];
   unsigned long long cand[32];
 };
@@ -687,10 +706,13 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
   const veq_program_meta pm = B.progs[p];
   const uint32_t T = pm.n_threads, full = B.prog_full_set[p], nch = (T + 31) / 32;
   const uint64_t seg0 = B.seg_off[pm.thread_off];
-  // next segment after segment j of thread g: its end and its ending set
-  auto seg_next = [&](uint32_t g, uint64_t j, uint32_t &end, uint32_t &set) {
+  // segment j (absolute) of thread g: length, ending set and its chunk mask
+  auto seg_info = [&](uint32_t g, uint64_t j, uint32_t &ln, uint32_t &set, uint32_t &msk) {
     set = B.seg_set[j];
-    end = set == UNSET ? (uint32_t)B.thread_stmt[g + 1] : (uint32_t)B.seg_start[j + 1];
+    const uint64_t start = B.seg_start[j];
+    const uint64_t end = set == UNSET ? B.thread_stmt[g + 1] : B.seg_start[j + 1];
+    ln = (uint32_t)(end - start);
+    msk = (set != UNSET && set != full) ? (uint32_t)B.set_chunk[set] : 0u;
   };
   uint32_t ret = 0, blkfull = 0, fullmin = UNSET;
   for (uint32_t t = lane; t < nch * 32; t += 32) {
@@ -698,16 +720,15 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
     if (t < T) {
       const uint32_t g = pm.thread_off + t;
       const uint64_t so = B.seg_off[g];
-      uint32_t end, set;
-      seg_next(g, so, end, set);
-      const uint32_t start = (uint32_t)B.seg_start[so];
-      S.so[t] = (uint32_t)(so - seg0);
-      S.sj[t] = 0;
-      S.cs[t] = start;
-      S.ns[t] = end;
+      uint32_t ln, set, msk;
+      seg_info(g, so, ln, set, msk);
+      S.cj[t] = (uint32_t)(so - seg0);
+      S.len[t] = ln;
       S.nset[t] = set;
+      S.nm[t] = msk;
       S.bs[t] = UNSET;
-      st = (set == UNSET && start == end) ? TS_RET : TS_RUN;
+      S.bm[t] = 0;
+      st = (set == UNSET && ln == 0) ? TS_RET : TS_RUN;
     }
     S.st[t] = st;
     ret += __popc(__ballot_sync(kFull, st == TS_RET));
@@ -717,38 +738,62 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
   uint32_t dirty = nch >= 32 ? ~0u : ((1u << nch) - 1);
   unsigned long long step = 0;
   uint32_t nrel = 0;
+  // next-segment loads of threads that block stay in registers and are
+  // written to shared memory at the start of the next round, so the warp
+  // does not wait for them inside the round that issued them (a released
+  // thread is marked runnable; an empty last segment returns when it "runs")
+  bool p_has = false;
+  uint32_t p_t = 0, p_len = 0, p_set = 0, p_msk = 0;
   while (ret != T) {
+    if (p_has) {
+      S.len[p_t] = p_len;
+      S.nset[p_t] = p_set;
+      S.nm[p_t] = p_msk;
+      p_has = false;
+    }
+    __syncwarp();
+    const bool single = __popc(dirty) == 1;
     // ---- run phase over the dirty chunks, in tid order
     unsigned long long total = 0;
     for (uint32_t dm = dirty; dm; dm &= dm - 1) {
       const uint32_t c = __ffs(dm) - 1, t = c * 32 + lane;
-      const uint8_t st = S.st[t];
-      const bool run = st == TS_RUN;
-      const uint32_t len = run ? S.ns[t] - S.cs[t] : 0;
+      const bool run = S.st[t] == TS_RUN;
+      const uint32_t ln = run ? S.len[t] : 0;
       uint32_t tot;
-      const uint32_t ex = warp_excl_scan(len, tot);
+      const uint32_t ex = warp_excl_scan(ln, tot);
+      bool newret = false, newfull = false;
       if (run) {
-        const uint32_t g = pm.thread_off + t;
-        const uint32_t sj = S.sj[t];
-        const uint64_t j = seg0 + S.so[t] + sj;
-        B.seg_base[j] = (uint32_t)(step + total + ex);
+        const uint32_t cj = S.cj[t];
+        B.seg_base[seg0 + cj] = (uint32_t)(step + total + ex);
         const uint32_t set = S.nset[t];
         if (set == UNSET) {
           S.st[t] = TS_RET;
+          newret = true;
         } else {
           S.st[t] = TS_BLOCK;
           S.bs[t] = set;
-          // prefetch the segment after the sync: it runs when I is released
-          uint32_t end, nset;
-          seg_next(g, j + 1, end, nset);
-          S.cs[t] = S.ns[t];
-          S.ns[t] = end;
-          S.nset[t] = nset;
+          S.bm[t] = S.nm[t];
+          newfull = set == full;
+          // prefetch the segment after the sync: it runs when the set is
+          // released, so these loads are off the critical path
+          uint32_t ln2, set2, msk2;
+          seg_info(pm.thread_off + t, seg0 + cj + 1, ln2, set2, msk2);
+          S.cj[t] = cj + 1;
+          if (single) {
+            p_has = true;
+            p_t = t;
+            p_len = ln2;
+            p_set = set2;
+            p_msk = msk2;
+          } else {
+            S.len[t] = ln2;
+            S.nset[t] = set2;
+            S.nm[t] = msk2;
+          }
         }
       }
-      const uint32_t nr = __ballot_sync(kFull, run && S.nset[t] == UNSET && S.st[t] == TS_RET);
-      ret += __popc(nr);
-      const uint32_t nf = __ballot_sync(kFull, run && S.st[t] == TS_BLOCK && S.bs[t] == full);
+      ret += __popc(__ballot_sync(kFull, newret));
+      const uint32_t nf = __ballot_sync(kFull, newfull);
       blkfull += __popc(nf);
       if (nf) fullmin = min(fullmin, c * 32 + __ffs(nf) - 1);
       total += tot;
@@ -766,13 +811,11 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
       if ((blk >> lane) & 1u) {
         const uint32_t grp = __match_any_sync(blk, bs);
         if ((uint32_t)(__ffs(grp) - 1) == lane) {
-          const veq_syncset q = B.sets[bs];
-          const uint64_t bits = B.set_words[q.word_off] & (q.n_bits >= 64 ? ~0ull : ((1ull << q.n_bits) - 1));
-          const uint32_t M = (uint32_t)(bits << (q.lo - c * 32));
-          if (M != 0 && (M & ~(grp | retm)) == 0)
-            key = ((unsigned long long)(c * 32 + __ffs(M) - 1) << 32) | t;
+          const uint32_t M = S.bm[t];
+          if (M != 0 && (M & ~(grp | retm)) == 0) key = ((unsigned long long)(c * 32 + __ffs(M) - 1) << 32) | t;
         }
       }
+#pragma unroll
       for (int o = 16; o; o >>= 1) {
         const unsigned long long y = __shfl_xor_sync(kFull, key, o);
         key = y < key ? y : key;
@@ -782,6 +825,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
     __syncwarp();
     // ---- the release: smallest (min tid, first blocked member)
     unsigned long long best = lane < nch ? S.cand[lane] : ~0ull;
+#pragma unroll
     for (int o = 16; o; o >>= 1) {
       const unsigned long long y = __shfl_xor_sync(kFull, best, o);
       best = y < best ? y : best;
@@ -801,26 +845,15 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
       for (uint32_t c = 0; c < nch; c++) {
         const uint32_t t = c * 32 + lane;
         const bool rel = S.st[t] == TS_BLOCK && S.bs[t] == full;
-        if (rel) {
-          S.sj[t] += 1;
-          const bool r = S.nset[t] == UNSET && S.cs[t] == S.ns[t];
-          S.st[t] = r ? TS_RET : TS_RUN;
-        }
-        const uint32_t rm = __ballot_sync(kFull, rel);
-        if (rm) dirty |= 1u << c;
-        ret += __popc(__ballot_sync(kFull, rel && S.st[t] == TS_RET));
+        if (rel) S.st[t] = TS_RUN;
+        if (__ballot_sync(kFull, rel)) dirty |= 1u << c;
       }
       blkfull = 0;
       fullmin = UNSET;
     } else {
       const uint32_t c = (uint32_t)(best & 0xffffffffu) / 32, t = c * 32 + lane;
       const bool rel = S.st[t] == TS_BLOCK && S.bs[t] == I;
-      if (rel) {
-        S.sj[t] += 1;
-        const bool r = S.nset[t] == UNSET && S.cs[t] == S.ns[t];
-        S.st[t] = r ? TS_RET : TS_RUN;
-      }
-      ret += __popc(__ballot_sync(kFull, rel && S.st[t] == TS_RET));
+      if (rel) S.st[t] = TS_RUN;
       dirty = 1u << c;
     }
     __syncwarp();
@@ -834,12 +867,18 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
     nrel++;
     step += 1;
   }
+  if (p_has) {
+    S.len[p_t] = p_len;
+    S.nset[p_t] = p_set;
+    S.nm[p_t] = p_msk;
+  }
   __syncwarp();
   for (uint32_t t = lane; t < T; t += 32) {
     const uint32_t g = pm.thread_off + t;
     const uint8_t st = S.st[t];
     B.th_state[g] = st;
-    B.th_seg[g] = S.sj[t];
+    // blocked threads: the segment that ended at their sync
+    B.th_seg[g] = S.cj[t] - (uint32_t)(B.seg_off[g] - seg0) - (st == TS_BLOCK ? 1u : 0u);
     B.th_bset[g] = st == TS_BLOCK ? S.bs[t] : UNSET;
   }
   if (lane == 0) {
