@@ -841,10 +841,33 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
                                                                                 ctx->pool, ctx->pool_used,
                                                                                 ctx->pool_cap, chunk));
       CK(cudaGetLastError());
-                }
-    PH1(VEQ_PH_EVAL);
-                    CK(cudaMemcpyAsync(&bd->n_work_last, nw, 8, cudaMemcpyDeviceToHost, s));  // valid after the final sync
+      if (prof) {
+        unsigned long long hp[32], nwh = 0;
+        CK(cudaMemcpyAsync(hp, prof, 32 * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&nwh, nw, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "[veq prof] items %llu warps %llu | wait %.1f us/item |", nwh, (unsigned long long)(threads / 32),
+                hp[0] / 1965.0 / std::max<double>(1, nwh));
+        const char *nm[5] = {"other", "lean", "smem", "small", "global"};
+        for (int k = 0; k < 5; k++)
+          if (hp[6 + k]) fprintf(stderr, " %s n=%llu %.2f us", nm[k], hp[6 + k], hp[1 + k] / 1965.0 / hp[6 + k]);
+        if (hp[7])
+          fprintf(stderr, " | lean phases: loads %.2f sort %.2f intern %.2f us", hp[11] / 1965.0 / hp[7],
+                  hp[12] / 1965.0 / hp[7], hp[13] / 1965.0 / hp[7]);
+        if (hp[21] || hp[24] || hp[25] || hp[26] || hp[27] || hp[28])
+          fprintf(stderr, " | pairs: %llu items %.2f us per item; fallbacks skip %llu m>16 %llu coef %llu consts %llu ties %llu",
+                  hp[21], hp[20] / 1965.0 / std::max<unsigned long long>(1, hp[21]), hp[24], hp[25], hp[26], hp[27],
+                  hp[28]);
+        if (hp[8])
+          fprintf(stderr, " | smem: pool wait %.2f us/item, %.1f pages/item; runs %.2f gather %.2f merge %.2f intern %.2f us",
+                  hp[14] / 1965.0 / hp[8], (double)hp[15] / hp[8], hp[16] / 1965.0 / hp[8], hp[17] / 1965.0 / hp[8],
+                  hp[18] / 1965.0 / hp[8], hp[19] / 1965.0 / hp[8]);
+        fprintf(stderr, "\n");
       }
+    }
+    PH1(VEQ_PH_EVAL);
+    CK(cudaMemcpyAsync(&bd->n_work_last, nw, 8, cudaMemcpyDeviceToHost, s));  // valid after the final sync
+  }
   PH0(VEQ_PH_FINALS);
   if (bd->n_cells) LAUNCH(k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
   PH1(VEQ_PH_FINALS);

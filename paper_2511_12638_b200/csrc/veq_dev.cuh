@@ -19,7 +19,9 @@ enum Kind : uint8_t { K_CONST = 0, K_NEGINF, K_VAR, K_EXP, K_MAX, K_DIV, K_NEG, 
 // F_COEF: a Mul whose first kid is a Const (a term with coefficient != 1).
 // Terms without it are determined by their factor vector, so two like terms
 // of a sum without F_COEF terms are the same interned id.
-enum : uint8_t { F_HASDIV = 1, F_POSDEF = 2, F_COEF = 4 };
+// F_ANYCOEF: an Add with at least one F_COEF kid (tells a sum's consumer,
+// before it gathers the terms, whether like terms may differ in id).
+enum : uint8_t { F_HASDIV = 1, F_POSDEF = 2, F_COEF = 4, F_ANYCOEF = 8 };
 
 // 32-byte node. Const: p0 = num, p1 = den. Var: p0 = order key, p1 =
 // identity (input << 40 | cell, or the undef key). Composite: p0 = offset of
@@ -233,8 +235,9 @@ __device__ __forceinline__ uint64_t composite_prefix(uint8_t kind, uint32_t nk, 
 }
 // positive_definite (proj/src/decide.cpp:306-333) from kid flags
 __device__ __forceinline__ uint8_t composite_flags(uint8_t kind, bool any_pd, bool all_pd, bool any_div,
-                                                  bool kid0_const = false) {
+                                                  bool kid0_const = false, bool any_coef = false) {
   uint8_t flags = (kind == K_MUL && kid0_const) ? F_COEF : 0;
+  if (kind == K_ADD && any_coef) flags |= F_ANYCOEF;
   if (any_div || kind == K_DIV) flags |= F_HASDIV;
   if (kind == K_EXP) flags |= F_POSDEF;
   else if (kind == K_MAX && any_pd) flags |= F_POSDEF;
@@ -255,7 +258,7 @@ __device__ inline uint32_t intern(const Table &T, uint8_t kind, uint64_t p0, uin
   } else if (kind == K_VAR) {
     h = hcomb(h, p0);
   } else if (kind != K_NEGINF) {
-    bool any_pd = false, all_pd = true, any_div = false, k0c = false;
+    bool any_pd = false, all_pd = true, any_div = false, k0c = false, any_cf = false;
     uint64_t sum = 0;
     for (uint32_t i = 0; i < nk; i++) {
       Node kn = ld_node(T, kids[i]);
@@ -264,13 +267,14 @@ __device__ inline uint32_t intern(const Table &T, uint8_t kind, uint64_t p0, uin
       any_pd |= pd;
       all_pd &= pd;
       any_div |= (kn.flags & F_HASDIV) != 0;
+      any_cf |= (kn.flags & F_COEF) != 0;
       if (i == 0) {
         p1 = composite_prefix(kind, nk, prefix_of(kn));
         k0c = kn.kind == K_CONST;
       }
     }
     h = composite_hash(kind, nk, sum);
-    flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
+    flags = composite_flags(kind, any_pd, all_pd, any_div, k0c, any_cf);
   }
   return intern_meta(T, kind, p0, p1, kids, nk, h, flags);
 }

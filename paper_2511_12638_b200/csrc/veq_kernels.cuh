@@ -1714,10 +1714,10 @@ __device__ __forceinline__ bool desc_is_add(const uint4 &d) {
 // memory pool (warp_add_smem); like terms, -inf leaves or an exhausted pool
 // use the global-scratch path (warp_add_nary). The next item's descriptor
 // and first 32 chain-log entries are loaded while the current one runs.
-// 64 registers/thread: 32 resident warps per SM (2 blocks of 16 warps, each
-// block with a 108 KB page pool).
-constexpr uint32_t EVAL_BLOCK = 512, EVAL_PAGES = 27;
-__global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
+// 64 registers/thread: 32 resident warps per SM in one block sharing one
+// 216 KB page pool.
+constexpr uint32_t EVAL_BLOCK = 1024, EVAL_PAGES = 54;
+__global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
                                                              const unsigned long long *n_work_dev,
                                                              unsigned long long *cursor, char *pool,
                                                              unsigned long long *pool_used, uint64_t pool_cap,
@@ -1728,7 +1728,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
   const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t grab = n_work >= warps_total * 16 ? 4 : (n_work >= warps_total * 4 ? 2 : 1);
   extern __shared__ __align__(16) char eval_smem[];
-  __shared__ uint32_t s_mask;
+  __shared__ unsigned long long s_mask;
   if (threadIdx.x == 0) s_mask = 0;
   __syncthreads();
   const SmemPool SP{&s_mask, eval_smem, EVAL_PAGES};
@@ -1834,7 +1834,14 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
               for (uint32_t k = lane; k < n; k += 32) m += n_terms_of(T, wait_node(B, E.log[b + k]));
               m = __reduce_add_sync(kFull, m);
             }
-            const uint32_t pages = (uint32_t)((add_smem_bytes(n, m) + SPAGE - 1) / SPAGE);
+            // leaves with coefficient terms need the grouping region
+          bool cleaf = false;
+          for (uint32_t k = lane; k < n; k += 32) {
+            const uint32_t fl = ld_node(T, wait_node(B, E.log[b + k])).flags;
+            cleaf |= (fl & (F_COEF | F_ANYCOEF)) != 0;
+          }
+          cleaf = __any_sync(kFull, cleaf);
+          const uint32_t pages = (uint32_t)((add_smem_bytes(n, m, cleaf) + SPAGE - 1) / SPAGE);
             const long long pa0 = E.prof ? clock64() : 0;
             const int first = pool_acquire(SP, pages);
             if (E.prof && lane == 0) {
@@ -1846,7 +1853,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 2) k_eval_warp(Batch B, Table T, E
               uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
               for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
               __syncwarp();
-              r = warp_add_smem(T, buf, n, m, &W, E.prof ? prof_smem : nullptr);
+              r = warp_add_smem(T, buf, n, m, &W, E.prof ? prof_smem : nullptr, cleaf);
               pool_release(SP, first, pages);
               path = 2;
             }

@@ -118,7 +118,7 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
                                        WarpAlloc *W = nullptr) {
   const uint32_t lane = lane_id();
   uint64_t sum = 0, p1 = 0;
-  bool any_pd = false, all_pd = true, any_div = false, k0c = false;
+  bool any_pd = false, all_pd = true, any_div = false, k0c = false, any_cf = false;
 #pragma unroll 4
   for (uint32_t i = lane; i < nk; i += 32) {
     Node kn = ld_node(T, kids[i]);
@@ -127,6 +127,7 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
     any_pd |= pd;
     all_pd &= pd;
     any_div |= (kn.flags & F_HASDIV) != 0;
+    any_cf |= (kn.flags & F_COEF) != 0;
     if (i == 0) {
       p1 = composite_prefix(kind, nk, prefix_of(kn));
       k0c = kn.kind == K_CONST;
@@ -138,8 +139,9 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
   any_pd = __any_sync(kFull, any_pd);
   all_pd = __all_sync(kFull, all_pd);
   any_div = __any_sync(kFull, any_div);
+  any_cf = __any_sync(kFull, any_cf);
   const uint64_t h = composite_hash(kind, nk, sum);
-  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
+  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c, any_cf);
   uint64_t slot = h & T.slot_mask;
   uint32_t mine = EMPTY;
   for (uint64_t probes = 0;; probes++) {
@@ -252,31 +254,33 @@ __device__ __forceinline__ void reg_bitonic(uint64_t &key, uint32_t &val, Less l
 
 __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
                                               bool pd, bool dv, uint64_t p1, bool k0c, WarpAlloc *W = nullptr,
-                                              bool *created = nullptr);
+                                              bool *created = nullptr, bool cf = false);
 
 // Interns a composite whose kid i is held by lane i (m <= 32 kids).
 __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32_t kid, uint32_t m) {
   const uint32_t lane = lane_id();
   uint64_t term = 0, p1 = 0;
-  bool pd = true, dv = false, k0c = false;
+  bool pd = true, dv = false, k0c = false, cf = false;
   if (lane < m) {
     Node kn = ld_node(T, kid);
     term = kid_term(lane, kn.hash);
     pd = kn.flags & F_POSDEF;
     dv = (kn.flags & F_HASDIV) != 0;
+    cf = (kn.flags & F_COEF) != 0;
     if (lane == 0) {
       p1 = composite_prefix(kind, m, prefix_of(kn));
       k0c = kn.kind == K_CONST;
     }
   }
-  return warp_intern_regs_h(T, kind, kid, m, term, pd, dv, __shfl_sync(kFull, p1, 0), __shfl_sync(kFull, k0c, 0));
+  return warp_intern_regs_h(T, kind, kid, m, term, pd, dv, __shfl_sync(kFull, p1, 0), __shfl_sync(kFull, k0c, 0),
+                            nullptr, nullptr, cf);
 }
 
 // Same, with each lane's kid term hash (kid_term(lane, hash)) and flags
 // already known; p1 = composite prefix, k0c = kid 0 is a Const.
 __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
                                               bool pd, bool dv, uint64_t p1, bool k0c, WarpAlloc *W,
-                                              bool *created) {
+                                              bool *created, bool cf) {
   const uint32_t lane = lane_id();
   if (lane >= m) {
     term = 0;
@@ -286,8 +290,9 @@ __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint
   const uint64_t sum = warp_sum_u64(term);
   const bool any_pd = __any_sync(kFull, lane < m && pd), all_pd = __all_sync(kFull, pd);
   const bool any_div = __any_sync(kFull, dv);
+  const bool any_cf = __any_sync(kFull, lane < m && cf);
   const uint64_t h = composite_hash(kind, m, sum);
-  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c);
+  const uint8_t flags = composite_flags(kind, any_pd, all_pd, any_div, k0c, any_cf);
   uint64_t slot = h & T.slot_mask;
   uint32_t mine = EMPTY;
   if (W) {
@@ -819,7 +824,7 @@ __device__ inline uint32_t lean_pair16(const Table &T, uint32_t leaf, uint32_t n
 // uses the global-scratch path instead).
 constexpr uint32_t SPAGE = 4096;
 struct SmemPool {
-  uint32_t *mask;  // bit i: page i taken
+  unsigned long long *mask;  // bit i: page i taken (up to 64 pages)
   char *base;
   uint32_t npages;
 };
@@ -827,17 +832,18 @@ struct SmemPool {
 __device__ inline int pool_acquire(const SmemPool &P, uint32_t k) {
   int got = -1;
   if (lane_id() == 0 && k <= P.npages) {
-    const uint32_t all = P.npages >= 32 ? ~0u : ((1u << P.npages) - 1);
+    const unsigned long long all = P.npages >= 64 ? ~0ull : ((1ull << P.npages) - 1);
     for (int tries = 0; tries < 4096 && got < 0; tries++) {
-      uint32_t m = *(volatile uint32_t *)P.mask;
-      uint32_t fr = ~m & all, x = fr;
+      const unsigned long long m = *(volatile unsigned long long *)P.mask;
+      const unsigned long long fr = ~m & all;
+      unsigned long long x = fr;
       for (uint32_t j = 1; j < k; j++) x &= fr >> j;
       if (!x) {
         __nanosleep(256);
         continue;
       }
-      int i = __ffs(x) - 1;
-      uint32_t bits = (k >= 32 ? ~0u : ((1u << k) - 1)) << i;
+      const int i = __ffsll((long long)x) - 1;
+      const unsigned long long bits = (k >= 64 ? ~0ull : ((1ull << k) - 1)) << i;
       if (atomicCAS(P.mask, m, m | bits) == m) got = i;
     }
   }
@@ -845,7 +851,7 @@ __device__ inline int pool_acquire(const SmemPool &P, uint32_t k) {
 }
 __device__ inline void pool_release(const SmemPool &P, int first, uint32_t k) {
   __syncwarp();
-  if (lane_id() == 0) atomicAnd(P.mask, ~((k >= 32 ? ~0u : ((1u << k) - 1)) << first));
+  if (lane_id() == 0) atomicAnd(P.mask, ~((k >= 64 ? ~0ull : ((1ull << k) - 1)) << first));
 }
 
 // Working-set bytes of warp_add_smem for n leaves and m terms.
@@ -854,10 +860,10 @@ __device__ __forceinline__ uint32_t hash_slots(uint32_t m) {
   while (H < m + m / 2 + 1) H <<= 1;
   return H;
 }
-__device__ __forceinline__ uint64_t add_smem_bytes(uint32_t n, uint32_t m) {
+__device__ __forceinline__ uint64_t add_smem_bytes(uint32_t n, uint32_t m, bool coef) {
   uint64_t a = ((uint64_t)(2 * n + 1 + m) * 4 + 7) & ~7ull;
-  uint64_t y = 8ull * m + (uint64_t)hash_slots(m) * 4;  // coefficient grouping
-  if (y < 12ull * m) y = 12ull * m;                      // merge ping-pong
+  uint64_t y = coef ? 8ull * m + (uint64_t)hash_slots(m) * 4 : 0;  // coefficient grouping
+  if (y < 12ull * m) y = 12ull * m;                                 // merge ping-pong
   return a + 8ull * m + y;
 }
 
@@ -875,7 +881,7 @@ __device__ __forceinline__ bool pref_less(const Table &T, uint64_t pa, uint32_t 
 // and canonical order (Expr::compare) is produced by merging the leaves'
 // already-sorted kid runs with warp-parallel merge-path passes.
 __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint32_t m, WarpAlloc *W,
-                                       unsigned long long *ph = nullptr) {
+                                       unsigned long long *ph = nullptr, bool coef_room = true) {
   const uint32_t lane = lane_id();
   const long long c0 = ph ? clock64() : 0;
   long long c1 = 0, c2 = 0, c3 = 0;
@@ -936,6 +942,7 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   nconst = __reduce_add_sync(kFull, nconst);
   coef = __any_sync(kFull, coef);
   __syncwarp();
+  if (coef && !coef_room) return UNSET;  // sized without the grouping region
   if (coef) {
     // like terms may differ in id: exact grouping key = factor-vector hash
     // in a shared-memory table; any hit (true or a hash collision) defers to
