@@ -902,7 +902,17 @@ __global__ void k_exec(Batch B, Table T) {
   const uint32_t p = B.thread_prog[g];
   const veq_program_meta pm = B.progs[p];
   const uint32_t tid = g - pm.thread_off;
+  // a short thread's register file lives in local memory (per-thread
+  // interleaved, L1-resident) when it is small, else in the global file
+  constexpr uint32_t LREG = 32;
+  uint32_t lregs[LREG];
+  const uint32_t nregs = (uint32_t)(B.reg_off[g + 1] - B.reg_off[g]);
   uint32_t *regs = B.regfile + B.reg_off[g];
+  if (nregs <= LREG) {
+#pragma unroll
+    for (uint32_t k = 0; k < LREG; k++) lregs[k] = UNSET;
+    regs = lregs;
+  }
   const uint64_t s0 = B.thread_stmt[g], s1 = B.thread_stmt[g + 1];
   const uint64_t j0 = B.seg_off[g], j1 = B.seg_off[g + 1];
   for (uint64_t j = j0; j < j1; j++) {
