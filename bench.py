@@ -203,8 +203,7 @@ def main():
     def step():
         st = L.veq_clear_terms(sess.ctx)
         assert st == 0
-        ra = sess.run_raw(ba)
-        rb = sess.run_raw(bb)
+        ra, rb = sess.run_pair_raw(ba, bb)
         vc = sess.compare_raw(ba, bb, oa, ob)
         launches = ra.n_launches + rb.n_launches + 2
         if dist is not None:
@@ -221,9 +220,12 @@ def main():
         print(f"[bench] rank {rank}: verification failed: {vc.n_equal}/{vc.n_vcs} equal, faults "
               f"{ra.n_faults}/{rb.n_faults}", file=sys.stderr)
         sys.exit(1)
-    # instrumented pass: per-phase device time (CUDA events on the ctx stream)
+    # instrumented pass: per-phase device time (CUDA events on the ctx stream;
+    # one run at a time so each run's phase events are its own)
     L.veq_set_timing(sess.ctx, 1)
-    ra_t, rb_t, _, _ = step()
+    assert L.veq_clear_terms(sess.ctx) == 0
+    ra_t = sess.run_raw(ba)
+    rb_t = sess.run_raw(bb)
     L.veq_set_timing(sess.ctx, 0)
     phases = {}
     for i, name in enumerate(N.PHASES):
@@ -283,9 +285,8 @@ def main():
         tt.append(time.perf_counter())
         xa, xb = sess.load(a), sess.load(b)
         tt.append(time.perf_counter())
-        ra = sess.run_raw(xa)
+        ra, rb = sess.run_pair_raw(xa, xb)
         tt.append(time.perf_counter())
-        rb = sess.run_raw(xb)
         tt.append(time.perf_counter())
         vc = sess.compare_raw(xa, xb, oa, ob)
         tt.append(time.perf_counter())

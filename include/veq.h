@@ -226,6 +226,14 @@ typedef struct veq_run_out {
 
 int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out);
 
+/* veq_run in two halves: _start enqueues the whole run on the ctx stream and
+ * returns without waiting; _finish waits for it and fills `out` (same
+ * contents as veq_run). Several batches may be started before the first is
+ * finished (they execute in start order), so the device never idles between
+ * them. A batch cannot be started again before it is finished. */
+int veq_run_start(veq_ctx *ctx, uint32_t batch);
+int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out);
+
 /* Final shared-memory contents after veq_run (the Final payload of
  * ctaeq::Outcome, symexec.hpp:155): canonical term node of each cell of
  * program `prog`'s array `array` (program-local index), or 0xFFFFFFFF when

@@ -41,6 +41,10 @@ struct BatchDev {
   std::vector<uint64_t> thread_stmt;
   uint64_t n_stmts = 0, n_cells = 0, n_segs = 0, n_rel_cap = 0, n_regs = 0, n_access_max = 0;
   uint64_t n_arith = 0;  // BinOp/UnOp statements: bound of the work list and chain logs
+  unsigned long long *d_stats = nullptr;  // [0..7] table counters at run start, [8] work items
+  bool started = false;                   // veq_run_start enqueued, veq_run_finish pending
+  bool timing_run = false;                // phase events recorded by this run
+  uint32_t run_launches = 0;
   unsigned long long n_work_last = 0;  // work items of the last run (read back with its results)
   uint32_t n_threads = 0;
   unsigned int sched_flags = 0;  // written by k_prep_syncs (valid after the load's final sync)
@@ -66,6 +70,10 @@ struct veq_ctx {
   // steady-state runs make no allocation at all (cudaMalloc only when a
   // slot grows; runs on the ctx's single stream never overlap)
   std::vector<std::pair<void *, size_t>> ws;
+  // all-returned thread states handed out by runs without a deadlock
+  std::vector<uint8_t> ret_state;
+  std::vector<uint32_t> unset_set;
+  std::vector<uint64_t> unset_stmt;
   cudaStream_t stream = nullptr;
   std::string last_error;
   Table T{};
@@ -644,6 +652,10 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   B.fault_cap = fcap;
 #undef AL
 #undef UP
+  if ((r = dalloc(ctx, bd, &bd->d_stats, 16))) {
+    drop_batch(ctx, bd);
+    return r;
+  }
   ctx->batches.push_back(bd);
   *out = (uint32_t)(ctx->batches.size() - 1);
   const int rc = check_error_flag(ctx);
@@ -654,15 +666,21 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
 }
 
 int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
+  int r = veq_run_start(ctx, batch);
+  if (r) return r;
+  return veq_run_finish(ctx, batch, out);
+}
+
+int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   if (!ctx || batch >= ctx->batches.size()) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   BatchDev *bd = ctx->batches[batch];
+  if (bd->started) return fail(ctx, VEQ_E_ARG, "veq_run_start: previous run of this batch not finished");
   Batch &B = bd->B;
   cudaStream_t s = ctx->stream;
   const uint64_t S = bd->n_stmts;
-  // reset run state
-  unsigned long long cnt0[8] = {0};
-  CK(cudaMemcpyAsync(cnt0, ctx->counters, 64, cudaMemcpyDeviceToHost, s));
+  // reset run state; the table counters are snapshot on the device (stats)
+  CK(cudaMemcpyAsync(bd->d_stats, ctx->counters, 64, cudaMemcpyDeviceToDevice, s));
   CK(cudaMemsetAsync(B.seg_base, 0xff, bd->n_segs * 4, s));
   CK(cudaMemsetAsync(B.regfile, 0xff, std::max<uint64_t>(bd->n_regs, 1) * 4, s));
   CK(cudaMemsetAsync(B.st_step, 0xff, S * 4, s));
@@ -866,7 +884,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
       }
     }
     PH1(VEQ_PH_EVAL);
-    CK(cudaMemcpyAsync(&bd->n_work_last, nw, 8, cudaMemcpyDeviceToHost, s));  // valid after the final sync
+    CK(cudaMemcpyAsync(bd->d_stats + 8, nw, 8, cudaMemcpyDeviceToDevice, s));
   }
   PH0(VEQ_PH_FINALS);
   if (bd->n_cells) LAUNCH(k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
@@ -874,7 +892,25 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   CK(cudaGetLastError());
   if (sz) {
                   }
-  // ---- results to host
+  bd->started = true;
+  bd->timing_run = ctx->timing;
+  bd->run_launches = ctx->launches - launches0;
+  return VEQ_OK;
+}
+
+int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
+  if (!ctx || batch >= ctx->batches.size()) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  if (!bd->started) return fail(ctx, VEQ_E_ARG, "veq_run_finish: no run started on this batch");
+  bd->started = false;
+  Batch &B = bd->B;
+  cudaStream_t s = ctx->stream;
+  // ---- results to host (the first read-back waits for the run)
+  unsigned long long st16[16] = {0};
+  CK(cudaMemcpyAsync(st16, bd->d_stats, 128, cudaMemcpyDeviceToHost, s));
+  const unsigned long long *cnt0 = st16;
+  bd->n_work_last = st16[8];
   const uint32_t P = B.n_progs;
   std::vector<uint32_t> nrel(P);
   std::vector<unsigned long long> steps(P);
@@ -894,11 +930,21 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   if (nf) CK(cudaMemcpyAsync(bd->faults.data(), B.faults, nf * sizeof(veq_fault), cudaMemcpyDeviceToHost, s));
   bool any_dead = false;
   for (uint32_t p = 0; p < P; p++) any_dead |= dead[p] != 0;
-  bd->th_state.assign(B.n_threads, TS_RET);
-  bd->th_bset.assign(B.n_threads, UNSET);
-  bd->th_bstmt.assign(B.n_threads, ~0ull);
+  // final thread states are per-thread only after a deadlock; otherwise every
+  // thread returned and the ctx's shared all-returned arrays are handed out
+  bd->th_state.clear();
+  bd->th_bset.clear();
+  bd->th_bstmt.clear();
+  if (ctx->ret_state.size() < B.n_threads) {
+    ctx->ret_state.assign(B.n_threads, TS_RET);
+    ctx->unset_set.assign(B.n_threads, UNSET);
+    ctx->unset_stmt.assign(B.n_threads, ~0ull);
+  }
   if (any_dead) {
     // final thread states only matter for deadlock reports (symexec.cpp:335-365)
+    bd->th_state.assign(B.n_threads, TS_RET);
+    bd->th_bset.assign(B.n_threads, UNSET);
+    bd->th_bstmt.assign(B.n_threads, ~0ull);
     std::vector<uint32_t> th_seg(B.n_threads);
     CK(cudaMemcpyAsync(bd->th_state.data(), B.th_state, B.n_threads, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(bd->th_bset.data(), B.th_bset, B.n_threads * 4, cudaMemcpyDeviceToHost, s));
@@ -926,24 +972,25 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     out->n_faults = nf;
     out->faults = bd->faults.data();
     out->n_threads_total = B.n_threads;
-    out->thread_state = bd->th_state.data();
-    out->thread_block_set = bd->th_bset.data();
-    out->thread_block_stmt = bd->th_bstmt.data();
+    const bool own = !bd->th_state.empty();
+    out->thread_state = own ? bd->th_state.data() : ctx->ret_state.data();
+    out->thread_block_set = own ? bd->th_bset.data() : ctx->unset_set.data();
+    out->thread_block_stmt = own ? bd->th_bstmt.data() : ctx->unset_stmt.data();
     out->n_nodes = nn[0] - nn[4];
     out->n_kid_words = nn[1] - nn[5];
     out->n_work = bd->n_work_last;
-    out->n_access = n_tup;
+    out->n_access = bd->n_access_max;
     uint64_t executed = 0;
     for (uint32_t p = 0; p < P; p++) executed += bd->res[p].steps - bd->res[p].releases;
     out->n_stmts_executed = executed;
     // allocation chunks leave holes (counters[4], [5]); stats count real nodes
     out->n_new_nodes = (nn[0] - nn[4]) - (cnt0[0] - cnt0[4]);
     out->n_new_kid_words = (nn[1] - nn[5]) - (cnt0[1] - cnt0[5]);
-    out->n_launches = ctx->launches - launches0;
+    out->n_launches = bd->run_launches;
     out->n_phases = VEQ_MAX_PHASES;
     for (int i = 0; i < VEQ_MAX_PHASES; i++) {
       float ms = 0;
-      if (ctx->timing) cudaEventElapsedTime(&ms, ctx->ev0[i], ctx->ev1[i]);
+      if (bd->timing_run) cudaEventElapsedTime(&ms, ctx->ev0[i], ctx->ev1[i]);
       out->phase_ms[i] = ms;
     }
   }

@@ -137,6 +137,21 @@ class Session:
         _check(self.ctx, N.lib().veq_run(self.ctx, bid, C.byref(out)))
         return out
 
+    def run_pair_raw(self, ba: int, bb: int) -> Tuple[N.veq_run_out, N.veq_run_out]:
+        """Both runs of a check enqueued back to back (veq_run_start ×2, then
+        veq_run_finish ×2): the device runs kernel B's batch right after
+        kernel A's with no host round trip in between."""
+        L = N.lib()
+        oa, ob = N.veq_run_out(), N.veq_run_out()
+        _check(self.ctx, L.veq_run_start(self.ctx, ba))
+        st = L.veq_run_start(self.ctx, bb)
+        ra = L.veq_run_finish(self.ctx, ba, C.byref(oa))
+        if st == 0:
+            _check(self.ctx, L.veq_run_finish(self.ctx, bb, C.byref(ob)))
+        _check(self.ctx, ra)
+        _check(self.ctx, st)
+        return oa, ob
+
     def compare_raw(self, ba: int, bb: int, out_a: Sequence[int], out_b: Sequence[int]) -> N.veq_vc_out:
         n = len(out_a)
         A = (C.c_uint32 * max(1, n))(*out_a)

@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
     L.veq_declare_inputs.argtypes = [vp, P(veq_input_desc), u32]
     L.veq_load_batch.argtypes = [vp, P(veq_batch_desc), P(u32)]
     L.veq_run.argtypes = [vp, u32, P(veq_run_out)]
+    L.veq_run_start.argtypes = [vp, u32]
+    L.veq_run_finish.argtypes = [vp, u32, P(veq_run_out)]
     L.veq_fetch_cells.argtypes = [vp, u32, u32, u32, P(u32), u64]
     L.veq_compare.argtypes = [vp, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
     L.veq_export_dag.argtypes = [vp, P(u32), C.c_size_t, P(veq_dag_buf)]
@@ -137,7 +139,8 @@ def lib() -> C.CDLL:
     L.veq_stream.argtypes = [vp]
     L.veq_stream.restype = vp
     L.veq_clear_terms.argtypes = [vp]
-    for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_fetch_cells", "veq_compare",
+    for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_run_start", "veq_run_finish",
+              "veq_fetch_cells", "veq_compare",
               "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -145,6 +148,6 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_declare_inputs", "veq_load_batch",
-            "veq_run", "veq_fetch_cells", "veq_compare", "veq_export_dag", "veq_verdict_counters",
+            "veq_run", "veq_run_start", "veq_run_finish", "veq_fetch_cells", "veq_compare", "veq_export_dag", "veq_verdict_counters",
             "veq_set_timing", "veq_clear_terms", "veq_stream"]
 PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]

@@ -52,9 +52,8 @@ def _failed(rr: RunResult) -> bool:
 def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: bool = True) -> List[PairReport]:
     ba = sess.load(a)
     bb = sess.load(b)
-    out_a = sess.run_raw(ba)
+    out_a, out_b = sess.run_pair_raw(ba, bb)
     ra = build_results(sess, ba, a, out_a, with_shared=False)
-    out_b = sess.run_raw(bb)
     rb = build_results(sess, bb, b, out_b, with_shared=False)
     reports: List[PairReport] = []
     # programs share Out array layout across the batch (same kernel pair)
