@@ -226,6 +226,7 @@ def main():
     assert L.veq_clear_terms(sess.ctx) == 0
     ra_t = sess.run_raw(ba)
     rb_t = sess.run_raw(bb)
+    sess.compare_raw(ba, bb, oa, ob)  # each bench step ends with a compare (profile step boundaries)
     L.veq_set_timing(sess.ctx, 0)
     phases = {}
     for i, name in enumerate(N.PHASES):
