@@ -19,6 +19,8 @@ CASES = [
     ("wl_c2_reduce_b0", workloads.c2_reduce(n_blocks=2, block=128), 0),
     ("wl_c1_matmul_n8", workloads.c1_matmul(n=8, tk=2), None),
     ("wl_c1_matmul_n16", workloads.c1_matmul(n=16, tk=4), None),
+    # 1600 threads: exercises the block scheduler for CTAs above 1024 threads
+    ("wl_c1_matmul_n33", workloads.c1_matmul(n=33, tk=11), None),
     # C3 conv at reduced shapes (CI, CO, H, W, tile)
     ("wl_c3_conv_b1", workloads.c3_conv(2, 2, 4, 4, 2, 2), 1),
     ("wl_c3_conv_b3", workloads.c3_conv(2, 2, 4, 4, 2, 2), 3),
