@@ -127,6 +127,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=1024, help="CTA pairs per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--separate", action="store_true",
+                    help="load/run kernel A's and kernel B's CTAs as two batches (default: one merged batch)")
     args = ap.parse_args()
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
@@ -169,7 +171,7 @@ def main():
 
     import numpy as np
     import torch
-    from paper_2511_12638_b200 import frontend, native as N
+    from paper_2511_12638_b200 import frontend, ir, native as N
     from paper_2511_12638_b200.engine import Session
 
     torch.cuda.set_device(local)
@@ -189,7 +191,6 @@ def main():
                    scratch_bytes=8 << 30)
     L = N.lib()
     sess.declare_inputs(inputs)
-    ba, bb = sess.load(a), sess.load(b)
     oa, ob = [0], [0]  # y is the only Out array (array-name order)
     for k, name in enumerate(a.array_names[:int(a.progs[0]["n_arrays"])]):
         if int(a.arrays[k]["role"]) == N.ROLE_OUT:
@@ -197,40 +198,62 @@ def main():
     for k, name in enumerate(b.array_names[:int(b.progs[0]["n_arrays"])]):
         if int(b.arrays[k]["role"]) == N.ROLE_OUT:
             ob = [k]
+    P = a.n_progs
+    # default: both kernels' CTAs in ONE batch (programs 0..P-1 = kernel A,
+    # P..2P-1 = kernel B): one run carries both, and program i of A is
+    # compared with program P+i (veq_compare_progs)
+    merged = None if args.separate else ir.concat([a, b])
+
+    def load_all():
+        if merged is not None:
+            return (sess.load(merged),)
+        return (sess.load(a), sess.load(b))
+
+    def run_all(hs):
+        if len(hs) == 1:
+            return [sess.run_raw(hs[0])]
+        return list(sess.run_pair_raw(hs[0], hs[1]))
+
+    def compare_all(hs):
+        if len(hs) == 1:
+            return sess.compare_progs_raw(hs[0], 0, hs[0], P, P, oa, ob)
+        return sess.compare_raw(hs[0], hs[1], oa, ob)
+
+    hs = load_all()
     stream = torch.cuda.ExternalStream(L.veq_stream(sess.ctx))
     counters = torch.zeros(4, dtype=torch.float64, device="cuda")
 
     def step():
         st = L.veq_clear_terms(sess.ctx)
         assert st == 0
-        ra, rb = sess.run_pair_raw(ba, bb)
-        vc = sess.compare_raw(ba, bb, oa, ob)
-        launches = ra.n_launches + rb.n_launches + 2
+        rs = run_all(hs)
+        vc = compare_all(hs)
+        launches = sum(r.n_launches for r in rs) + 2
         if dist is not None:
             counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)
             dist.all_reduce(counters)
-        return ra, rb, vc, launches
+        return rs, vc, launches
 
     # correctness gate: every VC equal, no faults, on every rank
-    ra, rb, vc, _ = step()
-    tot, first_fail = combine_verdicts([vc.n_equal, vc.n_vcs, ra.n_faults + rb.n_faults, vc.n_missing],
+    rs, vc, _ = step()
+    nfaults = sum(r.n_faults for r in rs)
+    tot, first_fail = combine_verdicts([vc.n_equal, vc.n_vcs, nfaults, vc.n_missing],
                                        None if vc.n_equal == vc.n_vcs else base, device="cuda" if dist else None)
     ok = tot["equal"] == tot["vcs"] == args.blocks * world and tot["faults"] == 0
     if not ok:
-        print(f"[bench] rank {rank}: verification failed: {vc.n_equal}/{vc.n_vcs} equal, faults "
-              f"{ra.n_faults}/{rb.n_faults}", file=sys.stderr)
+        print(f"[bench] rank {rank}: verification failed: {vc.n_equal}/{vc.n_vcs} equal, {nfaults} faults",
+              file=sys.stderr)
         sys.exit(1)
     # instrumented pass: per-phase device time (CUDA events on the ctx stream;
     # one run at a time so each run's phase events are its own)
     L.veq_set_timing(sess.ctx, 1)
     assert L.veq_clear_terms(sess.ctx) == 0
-    ra_t = sess.run_raw(ba)
-    rb_t = sess.run_raw(bb)
-    sess.compare_raw(ba, bb, oa, ob)  # each bench step ends with a compare (profile step boundaries)
+    rs_t = [sess.run_raw(h) for h in hs]
+    compare_all(hs)  # each bench step ends with a compare (profile step boundaries)
     L.veq_set_timing(sess.ctx, 0)
     phases = {}
     for i, name in enumerate(N.PHASES):
-        phases[name] = float(ra_t.phase_ms[i]) + float(rb_t.phase_ms[i])
+        phases[name] = sum(float(r.phase_ms[i]) for r in rs_t)
 
     for _ in range(args.warmup):
         step()
@@ -256,7 +279,7 @@ def main():
         return ms, launches
 
     with ClockSampler(local) as clk:
-        ms, launches = timed(lambda: step()[3], args.steps)
+        ms, launches = timed(lambda: step()[2], args.steps)
     ms_step = ms / args.steps
     elements_step = args.blocks * world
     value = elements_step / (ms_step / 1000.0)
@@ -272,7 +295,7 @@ def main():
             setattr(batch, f, t.numpy().view(arr.dtype))
         return keep
 
-    keep = pin(a) + pin(b)
+    keep = pin(merged) if merged is not None else pin(a) + pin(b)
     h2d = a.nbytes() + b.nbytes()
     d2h = elements_step // world * 24
 
@@ -284,22 +307,21 @@ def main():
             L.veq_set_timing(sess.ctx, 1)
         sess.declare_inputs(inputs)
         tt.append(time.perf_counter())
-        xa, xb = sess.load(a), sess.load(b)
+        xs = load_all()
         tt.append(time.perf_counter())
-        ra, rb = sess.run_pair_raw(xa, xb)
+        rs = run_all(xs)
         tt.append(time.perf_counter())
-        tt.append(time.perf_counter())
-        vc = sess.compare_raw(xa, xb, oa, ob)
+        vc = compare_all(xs)
         tt.append(time.perf_counter())
         if e2e_prof:
-            print("[e2e] declare %.2f load %.2f run_a %.2f run_b %.2f compare %.2f ms" %
-                  tuple(1000 * (tt[k + 1] - tt[k]) for k in range(5)), "| run_b phases",
-                  " ".join("%s=%.2f" % (nm, rb.phase_ms[i]) for i, nm in enumerate(N.PHASES)), file=sys.stderr)
+            print("[e2e] declare %.2f load %.2f run %.2f compare %.2f ms" %
+                  tuple(1000 * (tt[k + 1] - tt[k]) for k in range(4)), "| phases",
+                  " ".join("%s=%.2f" % (nm, rs[-1].phase_ms[i]) for i, nm in enumerate(N.PHASES)), file=sys.stderr)
         assert vc.n_equal == vc.n_vcs
         if dist is not None:
             counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)
             dist.all_reduce(counters)
-        return ra.n_launches + rb.n_launches + 2
+        return sum(r.n_launches for r in rs) + 2
 
     e2e_step()
     e2e_k = max(1, min(args.steps, 5))
@@ -310,9 +332,9 @@ def main():
     #   exec 16 B per executed statement; sort+memscan 32 B per access tuple;
     #   eval 2 x (16 + 4k) per created node (written once, read once)
     peak, peak_kind = peaks()
-    S_exec = ra.n_stmts_executed + rb.n_stmts_executed
-    R = ra.n_access + rb.n_access
-    U_bytes = 16 * (ra.n_new_nodes + rb.n_new_nodes) + 4 * (ra.n_new_kid_words + rb.n_new_kid_words)
+    S_exec = sum(r.n_stmts_executed for r in rs_t)
+    R = sum(r.n_access for r in rs_t)
+    U_bytes = 16 * sum(r.n_new_nodes for r in rs_t) + 4 * sum(r.n_new_kid_words for r in rs_t)
     alg = {"exec": 16 * S_exec, "sort": 16 * R, "memscan": 16 * R, "eval": 2 * U_bytes}
     dom = max(phases, key=lambda k: phases[k])
     dom_bytes = alg.get(dom, 0)
@@ -336,8 +358,9 @@ def main():
         "step_roofline": {"b_min_bytes": b_min, "achieved_gbs": b_min / (ms_step / 1000.0) / 1e9,
                           "frac": b_min / (ms_step / 1000.0) / 1e9 / peak},
         "phases_ms": phases,
-        "counts": {"S": S_exec, "R": R, "new_nodes": ra.n_new_nodes + rb.n_new_nodes,
-                   "work_items": ra.n_work + rb.n_work, "t_elab_s": t_elab},
+        "counts": {"S": S_exec, "R": R, "new_nodes": sum(r.n_new_nodes for r in rs_t),
+                   "work_items": sum(r.n_work for r in rs_t), "t_elab_s": t_elab,
+                   "batches": "merged (A and B CTAs in one batch)" if merged is not None else "separate"},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

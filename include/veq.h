@@ -275,6 +275,14 @@ int veq_compare(veq_ctx *ctx, uint32_t batch_a, uint32_t batch_b,
                 const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
                 uint32_t n_out_per_pair, veq_vc_out *out);
 
+/* The same over program ranges: program prog_a0 + i of batch_a against
+ * program prog_b0 + i of batch_b, i < n_pairs. The two ranges may lie in ONE
+ * batch: loading and running both kernels' CTAs as a single batch lets one
+ * set of launches carry both runs. */
+int veq_compare_progs(veq_ctx *ctx, uint32_t batch_a, uint32_t prog_a0, uint32_t batch_b, uint32_t prog_b0,
+                      uint32_t n_pairs, const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
+                      uint32_t n_out_per_pair, veq_vc_out *out);
+
 /* ---- DAG export (host to_string / slow path / reports) -----------------
  * Exports the sub-DAG reachable from roots in canonical kid order. Nodes are
  * renumbered densely 0..n-1 in post-order (kids first); root_index maps each

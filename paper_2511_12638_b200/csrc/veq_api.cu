@@ -75,6 +75,8 @@ struct veq_ctx {
   std::vector<uint32_t> unset_set;
   std::vector<uint64_t> unset_stmt;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // side stream: long-thread executor alongside the short-thread one
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string last_error;
   Table T{};
   veq_limits lim{};
@@ -210,6 +212,10 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(VEQ_E_CUDA, "cudaSetDevice");
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(VEQ_E_CUDA, "stream");
+  if (cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return bail(VEQ_E_CUDA, "side stream");
   {
     // keep freed stream-ordered allocations in the pool across syncs: the
     // per-run work buffers are re-allocated every run
@@ -269,6 +275,9 @@ void veq_close(veq_ctx *ctx) {
   cudaFree(ctx->in_cache);
   for (auto &w : ctx->ws) cudaFree(w.first);
   cudaStreamDestroy(ctx->stream);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -733,8 +742,20 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   PH0(VEQ_PH_EXEC);
   if (S) LAUNCH(k_pre_inputs<<<blocks(S, 256), 256, 0, s>>>(B, ctx->T));
   // short threads: one CUDA thread each; long threads: one warp each
-  if (B.n_threads) LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
-  if (B.n_long) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_long * 32, 128), 128, 0, s>>>(B, ctx->T));
+  // long threads (warp executor) run on the side stream alongside the short
+  // ones: a batch mixing both kinds of CTA (e.g. kernel A's 1-thread CTAs
+  // and kernel B's 1024-thread CTAs) keeps the GPU busy with both
+  if (B.n_long && B.n_threads > B.n_long) {
+    CK(cudaEventRecord(ctx->ev_fork, s));
+    CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_fork, 0));
+    LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_long * 32, 128), 128, 0, ctx->stream2>>>(B, ctx->T));
+    CK(cudaEventRecord(ctx->ev_join, ctx->stream2));
+    LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
+    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  } else {
+    if (B.n_threads) LAUNCH(k_exec<<<blocks(B.n_threads, 128), 128, 0, s>>>(B, ctx->T));
+    if (B.n_long) LAUNCH(k_exec_warp<<<blocks((uint64_t)B.n_long * 32, 128), 128, 0, s>>>(B, ctx->T));
+  }
   PH1(VEQ_PH_EXEC);
   CK(cudaGetLastError());
   const unsigned long long n_tup = bd->n_access_max;
@@ -1000,15 +1021,25 @@ int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
 int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, const uint32_t *out_b,
                 uint32_t n_out, veq_vc_out *out) {
   if (!ctx || ba >= ctx->batches.size() || bb >= ctx->batches.size()) return VEQ_E_ARG;
+  BatchDev *A = ctx->batches[ba], *Bd = ctx->batches[bb];
+  if (A->progs.size() != Bd->progs.size()) return fail(ctx, VEQ_E_ARG, "batches differ in program count");
+  return veq_compare_progs(ctx, ba, 0, bb, 0, (uint32_t)A->progs.size(), out_a, out_b, n_out, out);
+}
+
+int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint32_t pb0, uint32_t n_pairs,
+                      const uint32_t *out_a, const uint32_t *out_b, uint32_t n_out, veq_vc_out *out) {
+  if (!ctx || ba >= ctx->batches.size() || bb >= ctx->batches.size()) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   BatchDev *A = ctx->batches[ba], *Bd = ctx->batches[bb];
   if (!A->ran || !Bd->ran) return fail(ctx, VEQ_E_ARG, "compare before run");
-  if (A->progs.size() != Bd->progs.size()) return fail(ctx, VEQ_E_ARG, "batches differ in program count");
+  if ((uint64_t)pa0 + n_pairs > A->progs.size() || (uint64_t)pb0 + n_pairs > Bd->progs.size())
+    return fail(ctx, VEQ_E_ARG, "program range out of the batch");
   std::vector<uint32_t> ca, cb;
-  for (size_t p = 0; p < A->progs.size(); p++)
+  for (size_t q = 0; q < n_pairs; q++)
     for (uint32_t k = 0; k < n_out; k++) {
-      uint32_t ga = A->progs[p].array_off + out_a[k], gb = Bd->progs[p].array_off + out_b[k];
-      if (out_a[k] >= A->progs[p].n_arrays || out_b[k] >= Bd->progs[p].n_arrays)
+      const size_t p = pa0 + q, pb = pb0 + q;
+      uint32_t ga = A->progs[p].array_off + out_a[k], gb = Bd->progs[pb].array_off + out_b[k];
+      if (out_a[k] >= A->progs[p].n_arrays || out_b[k] >= Bd->progs[pb].n_arrays)
         return fail(ctx, VEQ_E_ARG, "out array index out of range");
       uint64_t n = A->arrays[ga].size;
       uint64_t cba = A->arr_cell_base[ga], cbb = Bd->arr_cell_base[gb];

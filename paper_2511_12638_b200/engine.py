@@ -152,6 +152,15 @@ class Session:
         _check(self.ctx, st)
         return oa, ob
 
+    def compare_progs_raw(self, ba: int, pa0: int, bb: int, pb0: int, n_pairs: int, out_a: Sequence[int],
+                          out_b: Sequence[int]) -> N.veq_vc_out:
+        n = len(out_a)
+        A = (C.c_uint32 * max(1, n))(*out_a)
+        B = (C.c_uint32 * max(1, n))(*out_b)
+        out = N.veq_vc_out()
+        _check(self.ctx, N.lib().veq_compare_progs(self.ctx, ba, pa0, bb, pb0, n_pairs, A, B, n, C.byref(out)))
+        return out
+
     def compare_raw(self, ba: int, bb: int, out_a: Sequence[int], out_b: Sequence[int]) -> N.veq_vc_out:
         n = len(out_a)
         A = (C.c_uint32 * max(1, n))(*out_a)

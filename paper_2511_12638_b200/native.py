@@ -133,6 +133,7 @@ def lib() -> C.CDLL:
     L.veq_run_finish.argtypes = [vp, u32, P(veq_run_out)]
     L.veq_fetch_cells.argtypes = [vp, u32, u32, u32, P(u32), u64]
     L.veq_compare.argtypes = [vp, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
+    L.veq_compare_progs.argtypes = [vp, u32, u32, u32, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
     L.veq_export_dag.argtypes = [vp, P(u32), C.c_size_t, P(veq_dag_buf)]
     L.veq_verdict_counters.argtypes = [vp, P(u64)]
     L.veq_set_timing.argtypes = [vp, C.c_int]
@@ -140,7 +141,7 @@ def lib() -> C.CDLL:
     L.veq_stream.restype = vp
     L.veq_clear_terms.argtypes = [vp]
     for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_run_start", "veq_run_finish",
-              "veq_fetch_cells", "veq_compare",
+              "veq_fetch_cells", "veq_compare", "veq_compare_progs",
               "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -148,6 +149,6 @@ def lib() -> C.CDLL:
 
 
 EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_declare_inputs", "veq_load_batch",
-            "veq_run", "veq_run_start", "veq_run_finish", "veq_fetch_cells", "veq_compare", "veq_export_dag", "veq_verdict_counters",
+            "veq_run", "veq_run_start", "veq_run_finish", "veq_fetch_cells", "veq_compare", "veq_compare_progs", "veq_export_dag", "veq_verdict_counters",
             "veq_set_timing", "veq_clear_terms", "veq_stream"]
 PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]
