@@ -860,11 +860,14 @@ __device__ __forceinline__ uint32_t hash_slots(uint32_t m) {
   while (H < m + m / 2 + 1) H <<= 1;
   return H;
 }
+__device__ __forceinline__ uint32_t pz(uint32_t x) { return x + (x >> 5); }
+__device__ __forceinline__ uint32_t smem_pad_len(uint32_t m) { return m + (m >> 5) + 1; }
 __device__ __forceinline__ uint64_t add_smem_bytes(uint32_t n, uint32_t m, bool coef) {
-  uint64_t a = ((uint64_t)(2 * n + 1 + m) * 4 + 7) & ~7ull;
+  const uint64_t mp = smem_pad_len(m);
+  uint64_t a = ((uint64_t)(2 * n + 1 + mp) * 4 + 7) & ~7ull;
   uint64_t y = coef ? 8ull * m + (uint64_t)hash_slots(m) * 4 : 0;  // coefficient grouping
-  if (y < 12ull * m) y = 12ull * m;                                 // merge ping-pong
-  return a + 8ull * m + y;
+  if (y < 12ull * mp) y = 12ull * mp;                               // merge ping-pong
+  return a + 8ull * mp + y;
 }
 
 __device__ __forceinline__ bool pref_less(const Table &T, uint64_t pa, uint32_t a, uint64_t pb, uint32_t b) {
@@ -887,12 +890,15 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   long long c1 = 0, c2 = 0, c3 = 0;
   uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
   uint32_t *rs = lv + n;  // run starts = leaf term offsets, n + 1 entries
+  // term arrays are padded one slot per 32 (index pz(x)): lanes working on
+  // neighbouring 32-element chunks then fall in different banks
+  const uint32_t mp = smem_pad_len(m);
   uint32_t *idA = rs + n + 1;
-  uint64_t *preA = reinterpret_cast<uint64_t *>(buf + (((uint64_t)(2 * n + 1 + m) * 4 + 7) & ~7ull));
-  char *Y = reinterpret_cast<char *>(preA + m);
+  uint64_t *preA = reinterpret_cast<uint64_t *>(buf + (((uint64_t)(2 * n + 1 + mp) * 4 + 7) & ~7ull));
+  char *Y = reinterpret_cast<char *>(preA + mp);
   const uint32_t H = hash_slots(m);
   uint64_t *preB = reinterpret_cast<uint64_t *>(Y);
-  uint32_t *idB = reinterpret_cast<uint32_t *>(preB + m);
+  uint32_t *idB = reinterpret_cast<uint32_t *>(preB + mp);
   // 1. term offsets per leaf
   // (an Add leaf's slot in lv is replaced by its kid-arena offset: the
   // gather below then reads kid words without reloading the node)
@@ -929,13 +935,13 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
     // a leaf with several terms is an Add (lv holds its kid offset); a
     // canonical Add has at least two kids, so a one-term leaf is the term
     const uint32_t nl = rs[lo + 1] - rs[lo];
-    idA[t] = nl > 1 ? ld_kid(T, (uint64_t)lv[lo] + (t - rs[lo])) : lv[lo];
+    idA[pz(t)] = nl > 1 ? ld_kid(T, (uint64_t)lv[lo] + (t - rs[lo])) : lv[lo];
   }
   __syncwarp();
 #pragma unroll 4
   for (uint32_t t = lane; t < m; t += 32) {
-    const Node tn = ld_node(T, idA[t]);
-    preA[t] = prefix_of(tn);
+    const Node tn = ld_node(T, idA[pz(t)]);
+    preA[pz(t)] = prefix_of(tn);
     nconst += tn.kind == K_CONST;
     coef |= tn.kind == K_MUL && (tn.flags & F_COEF);
   }
@@ -953,7 +959,7 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
     for (uint32_t i = lane; i < H; i += 32) hs2[i] = EMPTY;
     __syncwarp();
     for (uint32_t t = lane; t < m; t += 32) {
-      Term tm = decompose_one(T, idA[t]);
+      Term tm = decompose_one(T, idA[pz(t)]);
       if (tm.nf == 0) continue;
       const uint64_t h = tm.fh;
       fh[t] = h;
@@ -997,25 +1003,22 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
       while (ilo < ihi) {
         uint32_t mid = (ilo + ihi) / 2;
         uint32_t bj = a1 + (d - mid - 1);
-        if (pref_less(T, ps[a0 + mid], is[a0 + mid], ps[bj], is[bj])) ilo = mid + 1;
+        if (pref_less(T, ps[pz(a0 + mid)], is[pz(a0 + mid)], ps[pz(bj)], is[pz(bj)])) ilo = mid + 1;
         else ihi = mid;
       }
       uint32_t i = a0 + ilo, j = a1 + (d - ilo);
       const uint32_t stop = min(end, b1);
       for (; pos < stop; pos++) {
+        const uint32_t pi = pz(i), pj = pz(j);
         bool takeA;
         if (i >= a1) takeA = false;
         else if (j >= b1) takeA = true;
-        else takeA = pref_less(T, ps[i], is[i], ps[j], is[j]);
-        if (takeA) {
-          pd[pos] = ps[i];
-          id_[pos] = is[i];
-          i++;
-        } else {
-          pd[pos] = ps[j];
-          id_[pos] = is[j];
-          j++;
-        }
+        else takeA = pref_less(T, ps[pi], is[pi], ps[pj], is[pj]);
+        const uint32_t src = takeA ? pi : pj;
+        pd[pz(pos)] = ps[src];
+        id_[pz(pos)] = is[src];
+        if (takeA) i++;
+        else j++;
       }
     }
     __syncwarp();
@@ -1039,7 +1042,7 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   // like terms without coefficients are equal interned ids: adjacent now
   {
     bool dup = false;
-    for (uint32_t t = lane + 1; t < m; t += 32) dup |= is[t] == is[t - 1];
+    for (uint32_t t = lane + 1; t < m; t += 32) dup |= is[pz(t)] == is[pz(t - 1)];
     if (__any_sync(kFull, dup)) return UNSET;
   }
   // 5. fold the leading Const terms into one (dropped when zero)
@@ -1048,9 +1051,9 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
     uint32_t cid = 0;
     if (lane == 0) {
       Rat c{0, 1};
-      for (uint32_t k = 0; k < nconst; k++) c = rat_add(T, c, const_val(ld_node(T, is[k])));
+      for (uint32_t k = 0; k < nconst; k++) c = rat_add(T, c, const_val(ld_node(T, is[pz(k)])));
       cid = rat_is(c, 0) ? UNSET : intern_const(T, c);
-      if (cid != UNSET) is[nconst - 1] = cid;
+      if (cid != UNSET) is[pz(nconst - 1)] = cid;
     }
     cid = __shfl_sync(kFull, cid, 0);
     first = cid == UNSET ? nconst : nconst - 1;
@@ -1058,8 +1061,11 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   }
   const uint32_t nout = m - first;
   if (nout == 0) return T.id_zero;
-  if (nout == 1) return is[first];
-  const uint32_t res = warp_intern(T, K_ADD, is + first, nout, W);
+  if (nout == 1) return is[pz(first)];
+  // the kids, contiguous (unpadded) in the other id buffer
+  for (uint32_t t = lane; t < nout; t += 32) id_[t] = is[pz(first + t)];
+  __syncwarp();
+  const uint32_t res = warp_intern(T, K_ADD, id_, nout, W);
   if (ph && lane == 0) {
     const long long c4 = clock64();
     ph[0] += c1 - c0;
