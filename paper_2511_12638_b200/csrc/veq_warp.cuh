@@ -119,7 +119,7 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
   const uint32_t lane = lane_id();
   uint64_t sum = 0, p1 = 0;
   bool any_pd = false, all_pd = true, any_div = false, k0c = false, any_cf = false;
-#pragma unroll 8
+#pragma unroll 4
   for (uint32_t i = lane; i < nk; i += 32) {
     Node kn = ld_node(T, kids[i]);
     sum += kid_term(i, kn.hash);
@@ -924,7 +924,7 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
   // term ids (kid words of Add leaves), then the term nodes.
   bool coef = false;
   uint32_t nconst = 0;
-#pragma unroll 8
+#pragma unroll 4
   for (uint32_t t = lane; t < m; t += 32) {
     uint32_t lo = 0, hi = n;
     while (hi - lo > 1) {
@@ -938,7 +938,7 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
     idA[pz(t)] = nl > 1 ? ld_kid(T, (uint64_t)lv[lo] + (t - rs[lo])) : lv[lo];
   }
   __syncwarp();
-#pragma unroll 8
+#pragma unroll 4
   for (uint32_t t = lane; t < m; t += 32) {
     const Node tn = ld_node(T, idA[pz(t)]);
     preA[pz(t)] = prefix_of(tn);
