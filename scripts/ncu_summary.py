@@ -83,8 +83,8 @@ def main():
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "launch__block_size", "l1tex__t_sector_hit_rate.pct",
             "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
-    lines = [f"# {tag}: ncu --set full of the dominant kernel ({phase}), {len(ms)} launch(es) "
-             "(kernel A's batch, then kernel B's, of one step)", "",
+    lines = [f"# {tag}: ncu --set full of the dominant kernel ({phase}), {len(ms)} launch(es); "
+             f"each launch is one bench step's {phase} (kernel A's and kernel B's CTAs in one merged batch)", "",
              "| metric | unit | " + " | ".join(f"launch {i}" for i in range(len(ms))) + " |",
              "|---|---|" + "---|" * len(ms)]
     for k in keys:
@@ -100,13 +100,13 @@ def main():
         u, v = m.get(k, ("", "0"))
         v = float(v.replace(",", "") or 0)
         return v * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}.get(u, 1.0)
-    # per step: summed over the captured launches (A and B batches)
-    traffic = sum(num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum") for m in ms)
+    # per launch (= per step with merged batches): mean over the captured launches
+    traffic = sum(num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum") for m in ms) / max(1, len(ms))
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     t = json.load(open(tp)) if os.path.exists(tp) else {}
     t[phase] = traffic
     t[f"{phase}_source"] = (f"profiles/{tag}_{phase}_ncu.md (dram__bytes_read.sum + dram__bytes_write.sum, "
-                            f"summed over {len(ms)} launch(es) of one step)")
+                            f"per launch, mean of {len(ms)} launches)")
     json.dump(t, open(tp, "w"), indent=1)
     print(open(os.path.join(ROOT, "profiles", f"{tag}_launches.md")).read())
     print(open(os.path.join(ROOT, "profiles", f"{tag}_{phase}_ncu.md")).read())
