@@ -1657,6 +1657,19 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
         arith_fault(B, i, VEQ_DETAIL_NEGINF_MUL);
         return undef_of(i);
       }
+      // product of two atoms (Var/Exp/Max/Div, at most one Exp): no
+      // coefficient, no distribution, no exp merge, so canon_mul_kids
+      // (expr.cpp:426-481) reduces to the two factors in canonical order
+      const Node na = ld_node(T, a), nc = ld_node(T, c);
+      auto atom = [](uint8_t k) { return k == K_VAR || k == K_EXP || k == K_MAX || k == K_DIV; };
+      if (atom(na.kind) && atom(nc.kind) && !(na.kind == K_EXP && nc.kind == K_EXP)) {
+        uint32_t f[2] = {a, c};
+        if (cmp_pref(T, prefix_of(nc), c, prefix_of(na), a) < 0) {
+          f[0] = c;
+          f[1] = a;
+        }
+        return intern(T, K_MUL, 0, 0, f, 2);
+      }
       uint32_t ops[2] = {a, c};
       return mul_canon(T, A, ops, 2);
     }
