@@ -875,6 +875,13 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
       // every resident slot is launched (warps spread over all SMs); the
       // kernel reads the work-list length and picks its claim size
       uint64_t threads = (uint64_t)nsm * per_sm * EVAL_BLOCK;
+      // per-warp allocation chunks: at most 1/16 of the table's capacity is
+      // held in chunk tails when every warp holds one
+      {
+        const uint64_t warps = threads / 32;
+        ctx->T.wa_ids = (uint32_t)std::min<uint64_t>(WA_IDS, std::max<uint64_t>(1, ctx->lim.max_nodes / (16 * warps)));
+        ctx->T.wa_kids = (uint32_t)std::min<uint64_t>(WA_KIDS, std::max<uint64_t>(32, ctx->lim.max_kid_words / (16 * warps)));
+      }
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
       LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, desc, nw, cursor,
                                                                                 ctx->pool, ctx->pool_used,

@@ -56,6 +56,7 @@ struct Table {
   const uint64_t *in_size;
   uint32_t n_inputs;
   uint32_t *in_cache;       // node id per input symbol (dense rank), UNSET = not yet interned
+  uint32_t wa_ids, wa_kids; // per-warp allocation chunk sizes (set per launch from capacity and grid)
 };
 
 __device__ __forceinline__ void set_error(const Table &T, int code) { atomicCAS(T.error, 0, code); }

@@ -48,13 +48,14 @@ constexpr uint64_t WA_IDS = 32, WA_KIDS = 2048;
 
 // Lane 0 only. False when the table is full (E_BUDGET set).
 __device__ inline bool wa_alloc(const Table &T, WarpAlloc &W, uint32_t nk, uint64_t &id, uint64_t &off) {
+  const uint64_t ids_chunk = T.wa_ids ? T.wa_ids : WA_IDS, kids_chunk = T.wa_kids ? T.wa_kids : WA_KIDS;
   if (W.id_next == W.id_end) {
-    unsigned long long b = atomicAdd(&T.counters[0], (unsigned long long)WA_IDS);
+    unsigned long long b = atomicAdd(&T.counters[0], (unsigned long long)ids_chunk);
     W.id_next = b;
-    W.id_end = b + WA_IDS;
+    W.id_end = b + ids_chunk;
   }
   if (W.kid_next + nk > W.kid_end) {
-    const uint64_t want = nk > WA_KIDS ? nk : WA_KIDS;
+    const uint64_t want = nk > kids_chunk ? nk : kids_chunk;
     if (W.kid_end > W.kid_next) atomicAdd(&T.counters[5], (unsigned long long)(W.kid_end - W.kid_next));
     unsigned long long b = atomicAdd(&T.counters[1], (unsigned long long)want);
     W.kid_next = b;
