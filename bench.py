@@ -4,10 +4,11 @@
 Workload (BASELINE.json configs[1], the metric's config): warp-shuffle tree
 reduction vs sequential sum over N = 2^20 inputs, as 1024 independent CTA
 pairs of 1024 elements (each CTA pair is one reference
-check_equivalence). A step = execute kernel A's batch, kernel B's batch and
-the per-VC canonical compare on the GPU (the reference's t_exec_a + t_exec_b
-+ t_decide), starting from an empty term DAG, plus the cross-rank verdict
-all-reduce when N > 1. Packed IR is resident in HBM for `value`; `e2e`
+check_equivalence). A step = execute both kernels' CTAs (by default as one
+merged batch: programs 0..P-1 are kernel A's, P..2P-1 kernel B's; --separate
+runs two batches) and the per-VC canonical compare on the GPU (the
+reference's t_exec_a + t_exec_b + t_decide), starting from an empty term
+DAG, plus the cross-rank verdict all-reduce when N > 1. Packed IR is resident in HBM for `value`; `e2e`
 re-uploads it from pinned host memory every step through the C-ABI and reads
 the verdicts back.
 
