@@ -95,6 +95,16 @@ __device__ __forceinline__ uint32_t prog_of_stmt(const Batch &B, uint64_t i) {
   return B.thread_prog[lo];
 }
 
+// Program of statement i, starting from a program p0 known to hold a
+// statement <= i (the block's first statement): a short forward walk over
+// the program boundaries instead of a full search.
+__device__ __forceinline__ uint32_t prog_walk(const Batch &B, uint32_t p0, uint64_t i) {
+  if (!B.prog_stmt) return prog_of_stmt(B, i);
+  uint32_t p = p0;
+  while (p + 1 < B.n_progs && __ldg(B.prog_stmt + p + 1) <= i) p++;
+  return p;
+}
+
 // Warp-aggregated slot allocation: one atomic per group of converged lanes.
 __device__ __forceinline__ unsigned long long agg_inc(unsigned long long *ctr) {
   cg::coalesced_group g = cg::coalesced_threads();
@@ -1498,11 +1508,15 @@ __global__ void k_resolve_finals(Batch B) {
 // interned in one parallel pass before execution; the executors read the
 // node from canon[i].
 __global__ void k_pre_inputs(Batch B, Table T) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ uint32_t s_p0;
+  const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x;
+  if (threadIdx.x == 0) s_p0 = prog_of_stmt(B, i0 < B.n_stmts ? i0 : B.n_stmts - 1);
+  __syncthreads();
+  const uint64_t i = i0 + threadIdx.x;
   if (i >= B.n_stmts) return;
   const veq_stmt st = B.stmts[i];
   if (st.kind != VEQ_ST_LOAD) return;
-  const veq_program_meta pm = B.progs[prog_of_stmt(B, i)];
+  const veq_program_meta pm = B.progs[prog_walk(B, s_p0, i)];
   const veq_array arr = B.arrays[pm.array_off + st.arr];
   const int32_t off = (int32_t)st.a;
   if (off < 0 || (uint64_t)off >= arr.size) return;
@@ -1545,7 +1559,10 @@ __global__ void k_resolve_all(Batch B, uint32_t *sz) {
 __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t *base, uint32_t *log,
                                                         uint32_t *log_stmt, unsigned long long *wkey, uint32_t *wval,
                                                         unsigned long long *n_work) {
-  const uint64_t b0 = (uint64_t)blockIdx.x * APP_NT * APP_ITEMS + threadIdx.x;
+  __shared__ uint32_t s_p0;
+  const uint64_t blk0 = (uint64_t)blockIdx.x * APP_NT * APP_ITEMS;
+  if (threadIdx.x == 0) s_p0 = prog_of_stmt(B, blk0 < B.n_stmts ? blk0 : B.n_stmts - 1);
+  const uint64_t b0 = blk0 + threadIdx.x;
   uint32_t mask = 0;
 #pragma unroll
   for (int k = 0; k < APP_ITEMS; k++) {
@@ -1576,7 +1593,7 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
     const uint64_t i = b0 + (uint64_t)k * APP_NT;
     // (step, program): every dependency of an item has a smaller step in the
     // same program, hence a smaller key, and all CTAs advance together
-    wkey[o] = ((unsigned long long)B.st_step[i] << B.prog_bits) | prog_of_stmt(B, i);
+    wkey[o] = ((unsigned long long)B.st_step[i] << B.prog_bits) | prog_walk(B, s_p0, i);
     wval[o] = (uint32_t)i;
     o++;
   }
