@@ -856,8 +856,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
       static const bool prof_on = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
       unsigned long long *prof = nullptr;
       if (prof_on) {
-        { int r_ = ws_get(ctx, 19, (void **)&prof, 32 * 8); if (r_) return r_; }
-        CK(cudaMemsetAsync(prof, 0, 32 * 8, s));
+        { int r_ = ws_get(ctx, 19, (void **)&prof, 128 * 8); if (r_) return r_; }
+        CK(cudaMemsetAsync(prof, 0, 128 * 8, s));
       }
       EvalCtx E{log, log_stmt, base, prof};
       uint4 *desc = nullptr;
@@ -888,8 +888,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
                                                                                 ctx->pool_cap, chunk));
       CK(cudaGetLastError());
       if (prof) {
-        unsigned long long hp[32], nwh = 0;
-        CK(cudaMemcpyAsync(hp, prof, 32 * 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long hp[128], nwh = 0;
+        CK(cudaMemcpyAsync(hp, prof, 128 * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&nwh, nw, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         fprintf(stderr, "[veq prof] items %llu warps %llu | wait %.1f us/item |", nwh, (unsigned long long)(threads / 32),
@@ -908,6 +908,9 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
           fprintf(stderr, " | smem: pool wait %.2f us/item, %.1f pages/item; runs %.2f gather %.2f merge %.2f intern %.2f us",
                   hp[14] / 1965.0 / hp[8], (double)hp[15] / hp[8], hp[16] / 1965.0 / hp[8], hp[17] / 1965.0 / hp[8],
                   hp[18] / 1965.0 / hp[8], hp[19] / 1965.0 / hp[8]);
+        fprintf(stderr, "\n[veq prof] timeline (per 400 us: items, smem items, warps done):");
+        for (int k = 0; k < 32; k++)
+          if (hp[32 + k] || hp[96 + k]) fprintf(stderr, " %d:%llu/%llu/%llu", k, hp[32 + k], hp[64 + k], hp[96 + k]);
         fprintf(stderr, "\n");
       }
     }

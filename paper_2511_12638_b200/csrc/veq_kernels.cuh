@@ -1793,6 +1793,16 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
     lg = (w < n_work && desc_is_add(d) && lane < d.z) ? __ldg(E.log + d.y + lane) : UNSET;
   };
   unsigned long long prof_wait = 0, prof_work[6] = {0, 0, 0, 0, 0, 0}, prof_n[6] = {0, 0, 0, 0, 0, 0}, prof_lean[3] = {0, 0, 0}, prof_pool = 0, prof_pages = 0, prof_smem[4] = {0, 0, 0, 0};
+  unsigned long long t_k0 = 0;
+  if (E.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_k0));
+  // VEQ_PROF timeline: items finished / smem items finished / warps done per
+  // 100 us bucket since the block started (slots 32..127)
+  auto tbucket = [&]() -> uint32_t {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long b = (t - t_k0) / 400000;
+    return (uint32_t)(b < 31 ? b : 31);
+  };
   unsigned long long w = ((unsigned long long)wib * gridDim.x + blockIdx.x) * grab, w_end = w + grab;
   uint4 d;
   uint32_t lg;
@@ -1834,6 +1844,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
       if (E.prof && lane == 0) {
         prof_work[5] += clock64() - t0;
         prof_n[5] += (rA != UNSET) + (rB != UNSET);
+        atomicAdd(E.prof + 32 + tbucket(), (unsigned long long)((rA != UNSET) + (rB != UNSET)));
       }
     }
     // items left for the full warp: the current one when unpaired, else the
@@ -1946,6 +1957,9 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
           prof_wait += t1 - t0;
           prof_work[path] += t2 - t1;
           prof_n[path]++;
+          const uint32_t tb = tbucket();
+          atomicAdd(E.prof + 32 + tb, 1ull);
+          if (path == 2) atomicAdd(E.prof + 64 + tb, 1ull);
         }
       }
       }
@@ -1962,6 +1976,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
   if (lane == 0 || lane == 16) wa_flush(T, W);  // both halves allocate in lean_pair16
   if (lane == 0) {
     if (E.prof) {
+      atomicAdd(E.prof + 96 + tbucket(), 1ull);
       atomicAdd(E.prof, prof_wait);
       for (int k = 0; k < 5; k++) {
         atomicAdd(E.prof + 1 + k, prof_work[k]);
