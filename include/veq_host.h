@@ -38,6 +38,14 @@ int veqh_elaborate_grid(const char *kernel_a, const char *kernel_b, const char *
 
 void veqh_free(veqh_pair *p);
 
+/* ctaeq::parse_config (proj/include/ctaeq/frontend.hpp:120,
+ * proj/src/frontend.cpp:1017-1110): on success writes the parsed launch
+ * configuration as "key=value" lines (threads, threads_a, threads_b,
+ * warp_size, params.<name> in name order, inputs, outputs) and returns
+ * VEQH_OK; on error returns VEQH_E_CONFIG with the reference's ParseError
+ * text ("<line>:1: <message>"). */
+int veqh_parse_config(const char *cfg, char *out, size_t outlen);
+
 #ifdef __cplusplus
 }
 #endif

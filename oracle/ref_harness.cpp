@@ -446,9 +446,34 @@ int cmd_bench(const std::string &pa_path, const std::string &pb_path, const std:
 
 } // namespace
 
+// parse_config of one config file, printed in veqh_parse_config's format
+// (or the exception text): pins the product config reader.
+int cmd_config(const char *path) {
+  std::ifstream f(path);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  try {
+    LaunchConfig c = parse_config(ss.str());
+    std::cout << "threads=" << c.threads << "\nthreads_a=" << c.threads_a << "\nthreads_b=" << c.threads_b
+              << "\nwarp_size=" << c.warp_size;
+    for (auto &[k, v] : c.params) std::cout << "\nparams." << k << "=" << v;
+    auto join = [](const std::vector<std::string> &v) {
+      std::string r;
+      for (size_t i = 0; i < v.size(); i++) r += (i ? "," : "") + v[i];
+      return r;
+    };
+    std::cout << "\ninputs=" << join(c.inputs) << "\noutputs=" << join(c.outputs) << "\n";
+    return 0;
+  } catch (const std::exception &e) {
+    std::cout << e.what();
+    return 3;
+  }
+}
+
 int main(int argc, char **argv) {
   try {
     std::string cmd = argc > 1 ? argv[1] : "";
+    if (cmd == "config" && argc == 3) return cmd_config(argv[2]);
     if (cmd == "pair" && argc == 6) return cmd_pair(argv[2], argv[3], argv[4], argv[5]);
     if (cmd == "gen" && argc == 4) return cmd_gen(argv[2], std::stoull(argv[3]));
     if (cmd == "bench" && argc == 7)

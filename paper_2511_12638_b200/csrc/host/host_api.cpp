@@ -30,6 +30,27 @@ uint8_t *to_image(const veq::HostBatch &b, size_t *len) {
 
 }  // namespace
 
+extern "C" int veqh_parse_config(const char *cfg_src, char *out, size_t outlen) {
+  if (!cfg_src) return VEQH_E_ARG;
+  try {
+    const veqh::LaunchConfig c = veqh::parse_config(cfg_src);
+    std::string s = "threads=" + std::to_string(c.threads) + "\nthreads_a=" + std::to_string(c.threads_a) +
+                    "\nthreads_b=" + std::to_string(c.threads_b) + "\nwarp_size=" + std::to_string(c.warp_size);
+    for (const auto &[k, v] : c.params) s += "\nparams." + k + "=" + std::to_string(v);
+    auto join = [](const std::vector<std::string> &v) {
+      std::string r;
+      for (size_t i = 0; i < v.size(); i++) r += (i ? "," : "") + v[i];
+      return r;
+    };
+    s += "\ninputs=" + join(c.inputs) + "\noutputs=" + join(c.outputs) + "\n";
+    put_err(out, outlen, s);
+    return VEQH_OK;
+  } catch (const std::exception &e) {
+    put_err(out, outlen, e.what());
+    return VEQH_E_CONFIG;
+  }
+}
+
 extern "C" int veqh_elaborate_grid(const char *kernel_a, const char *kernel_b, const char *cfg_src,
                                    const char *block_param, uint32_t block_base, uint32_t n_blocks,
                                    uint32_t n_workers, int want_names, veqh_pair *out, char *err, size_t errlen) {

@@ -788,7 +788,7 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     LAUNCH(k_mem_scan<<<blocks(n_tup, 128), 128, 0, s>>>(B, ctx->T, k2, v2, starts, n_starts, n_tup, rs));
     PH1(VEQ_PH_MEMSCAN);
     CK(cudaGetLastError());
-                          } else {
+  } else {
     PH1(VEQ_PH_SORT);
     PH0(VEQ_PH_MEMSCAN);
     PH1(VEQ_PH_MEMSCAN);
@@ -819,7 +819,7 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     const uint64_t nlog = 2 * bd->n_arith + 2;
     { int r_ = ws_get(ctx, 10, (void **)&log, std::max<uint64_t>(nlog, 1) * 4); if (r_) return r_; }
     { int r_ = ws_get(ctx, 11, (void **)&log_stmt, std::max<uint64_t>(nlog, 1) * 4); if (r_) return r_; }
-        PH1(VEQ_PH_CHAINS);
+    PH1(VEQ_PH_CHAINS);
     // chain-log entries and the work list, one pass; work sorted by
     // (step, program)
     PH0(VEQ_PH_WORKLIST);
@@ -921,8 +921,6 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   if (bd->n_cells) LAUNCH(k_final_nodes<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
   PH1(VEQ_PH_FINALS);
   CK(cudaGetLastError());
-  if (sz) {
-                  }
   bd->started = true;
   bd->timing_run = ctx->timing;
   bd->run_launches = ctx->launches - launches0;
@@ -1094,7 +1092,7 @@ int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint
     CK(cudaMemcpyAsync(ctx->sc_node.data(), scn, nsc * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(ctx->sc_dis.data(), scd, nsc, cudaMemcpyDeviceToHost, s));
   }
-              CK(cudaStreamSynchronize(s));
+  CK(cudaStreamSynchronize(s));
   int er = check_error_flag(ctx);
   if (er) return er;
   if (h[0] > sc_cap) return fail(ctx, VEQ_E_BUDGET, "side-condition buffer overflow");

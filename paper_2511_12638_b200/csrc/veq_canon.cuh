@@ -325,8 +325,6 @@ __device__ inline uint32_t mul_canon(const Table &T, Arena &A, const uint32_t *o
     uint64_t rem = t;
     Rat c = coeff;
     uint32_t cnt = f;
-    Term parts_dummy;
-    (void)parts_dummy;
     // first pass: count factors
     uint64_t r2 = rem;
     for (int q = (int)s - 1; q >= 0; q--) {
@@ -423,15 +421,12 @@ __device__ inline uint32_t split_coeff(const Table &T, Arena &A, uint32_t e, Rat
     Rat inv = rat_div(T, Rat{1, 1}, cont);
     uint32_t *sc = A.get<uint32_t>(n.nkids);
     if (!sc) return T.id_zero;
-    uint32_t nconst = 0;
     for (uint32_t i = 0; i < n.nkids; i++) {
       Rat c = rat_mul(T, ts[i].c, inv);
       Term t = ts[i];
       t.src = UNSET;
       sc[i] = finish_term(T, A, c, t);  // scale_term (expr.cpp:484-490)
-      nconst += ts[i].nf == 0;
     }
-    (void)nconst;
     // add(scaled): terms stay distinct; at most one Const
     sort_canonical(T, A, sc, n.nkids);
     return intern(T, K_ADD, 0, 0, sc, n.nkids);

@@ -2028,10 +2028,11 @@ struct CmpArgs {
   unsigned long long *n_equal, *n_missing;
 };
 
-__device__ inline void collect_sc(const Table &T, Arena &A, uint32_t root, uint32_t *seen_den, uint32_t &nseen,
-                                  uint32_t cap, uint32_t *visited, uint32_t &nvis, uint32_t vcap) {
-  uint32_t *stack = A.get<uint32_t>(vcap);
-  if (!stack) return;
+// Overflowing any of the fixed per-VC sets is an error (E_SCRATCH), never a
+// silent truncation: a dropped undischarged denominator would turn the
+// reference's "unknown" into "equivalent".
+__device__ inline void collect_sc(const Table &T, uint32_t root, uint32_t *seen_den, uint32_t &nseen,
+                                  uint32_t cap, uint32_t *visited, uint32_t &nvis, uint32_t vcap, uint32_t *stack) {
   uint32_t sp = 0;
   stack[sp++] = root;
   while (sp) {
@@ -2055,7 +2056,13 @@ __device__ inline void collect_sc(const Table &T, Arena &A, uint32_t root, uint3
       bool dup = false;
       for (uint32_t q = 0; q < nseen; q++)
         if (seen_den[q] == den) dup = true;
-      if (!dup && nseen < cap) seen_den[nseen++] = den;
+      if (!dup) {
+        if (nseen >= cap) {
+          set_error(T, E_SCRATCH);
+          return;
+        }
+        seen_den[nseen++] = den;
+      }
     }
     for (int k = (int)n.nkids - 1; k >= 0; k--) {
       if (sp >= vcap) {
@@ -2089,10 +2096,11 @@ __global__ void k_compare(Table T, const uint32_t *final_node_a, const uint32_t 
       const uint32_t cap = 1024, vcap = 1u << 13;
       uint32_t *seen = A.get<uint32_t>(cap);
       uint32_t *visited = A.get<uint32_t>(vcap);
-      if (seen && visited) {
+      uint32_t *stack = A.get<uint32_t>(vcap);  // shared by both roots
+      if (seen && visited && stack) {
         uint32_t nseen = 0, nvis = 0;
-        collect_sc(T, A, na, seen, nseen, cap, visited, nvis, vcap);
-        collect_sc(T, A, nb, seen, nseen, cap, visited, nvis, vcap);
+        collect_sc(T, na, seen, nseen, cap, visited, nvis, vcap, stack);
+        collect_sc(T, nb, seen, nseen, cap, visited, nvis, vcap, stack);
         unsigned long long off = atomicAdd(C.n_sc, (unsigned long long)nseen);
         if (off + nseen <= C.sc_cap) {
           for (uint32_t q = 0; q < nseen; q++) {

@@ -27,6 +27,7 @@ class PairReport:
     verdict: str
     vcs: List[dict] = field(default_factory=list)
     error_kernel: str = ""
+    error_detail: str = ""
     races: list = field(default_factory=list)
     safeties: list = field(default_factory=list)
     deadlock: Optional[object] = None
@@ -45,6 +46,43 @@ def out_array_pairs(a: Batch, b: Batch, p: int) -> Tuple[List[int], List[int], L
     return [oa[n] for n in names], [ob.get(n, 0) for n in names], names
 
 
+def signature_mismatch(a: Batch, b: Batch, p: int) -> Optional[str]:
+    """In/Out declarations of program p must agree between the kernels
+    (proj/src/pipeline.cpp:39-60): same count per role, then name and size of
+    each array in ascending name order. Scratch layout is private."""
+    def decls(bt: Batch, role: int):
+        pm = bt.progs[p]
+        o = int(pm["array_off"])
+        return sorted((bt.array_names[o + k], int(bt.arrays[o + k]["size"])) for k in range(int(pm["n_arrays"]))
+                      if int(bt.arrays[o + k]["role"]) == role)
+    for role, rs in ((N.ROLE_IN, "in"), (N.ROLE_OUT, "out")):
+        xs, ys = decls(a, role), decls(b, role)
+        if len(xs) != len(ys):
+            return f"kernels declare a different number of {rs} arrays"
+        for (na, sa), (nb, sb) in zip(xs, ys):
+            if na != nb:
+                return f"{rs} array name mismatch: {na} vs {nb}"
+            if sa != sb:
+                return f"{rs} array {na} size mismatch: {sa} vs {sb}"
+    return None
+
+
+class _VcSnap:
+    """Host copy of one veq_vc_out (its buffers are ctx-owned and reused by
+    the next compare call)."""
+
+    def __init__(self, v):
+        n = int(v.n_vcs)
+        self.n_vcs = n
+        self.vcs = []
+        for i in range(n):
+            x = v.vcs[i]
+            self.vcs.append(N.veq_vc(x.node_a, x.node_b, x.equal, x.sc_off, x.sc_n, 0))
+        self.n_sc = int(v.n_sc)
+        self.sc_node = [int(v.sc_node[i]) for i in range(self.n_sc)]
+        self.sc_discharged = [int(v.sc_discharged[i]) for i in range(self.n_sc)]
+
+
 def _failed(rr: RunResult) -> bool:
     return not (rr.outcome == "final" and not rr.races and not rr.safeties)
 
@@ -56,19 +94,40 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
     ra = build_results(sess, ba, a, out_a, with_shared=False)
     rb = build_results(sess, bb, b, out_b, with_shared=False)
     reports: List[PairReport] = []
-    # programs share Out array layout across the batch (same kernel pair)
-    oa, ob, names = out_array_pairs(a, b, 0)
-    vc = sess.compare_raw(ba, bb, oa, ob)
-    n_per = vc.n_vcs // max(1, a.n_progs) if a.n_progs else 0
-    sizes = []
-    o0 = int(a.progs[0]["array_off"]) if a.n_progs else 0
-    for k in oa:
-        sizes.append(int(a.arrays[o0 + k]["size"]))
-    sc_nodes = [vc.sc_node[i] for i in range(vc.n_sc)]
-    uniq = sorted(set(sc_nodes))
-    sc_strs = dict(zip(uniq, sess.to_strings(uniq))) if (render_side_conditions and uniq) else {}
+    mism = [signature_mismatch(a, b, p) for p in range(a.n_progs)]
+    # Out layout (array-name order) per program pair; signatures agree for
+    # every pair that is compared, so A's names index B's arrays
+    layouts = [out_array_pairs(a, b, p) if mism[p] is None else None for p in range(a.n_progs)]
+    ref = next((l for l in layouts if l is not None), None)
+    vc_of: Dict[int, Tuple[object, int]] = {}  # program -> (vc_out, first VC index of the pair)
+    if ref is not None and all(l is None or l == ref for l in layouts):
+        vc = _VcSnap(sess.compare_raw(ba, bb, ref[0], ref[1]))
+        n_per = vc.n_vcs // max(1, a.n_progs)
+        outs = [vc] * a.n_progs
+        for p in range(a.n_progs):
+            vc_of[p] = (vc, p * n_per)
+    else:
+        outs = []
+        for p in range(a.n_progs):
+            if layouts[p] is not None:
+                # per-pair compare when Out layouts differ between pairs
+                v = _VcSnap(sess.compare_progs_raw(ba, p, bb, p, 1, layouts[p][0], layouts[p][1]))
+                outs.append(v)
+                vc_of[p] = (v, 0)
+    sc_nodes = sorted({v.sc_node[i] for v in {id(x): x for x in outs}.values() for i in range(v.n_sc)}) \
+        if outs else []
+    sc_strs = dict(zip(sc_nodes, sess.to_strings(sc_nodes))) if (render_side_conditions and sc_nodes) else {}
     for p in range(a.n_progs):
         rep = PairReport(verdict="unknown")
+        if mism[p] is not None:
+            # signature_mismatch is checked before either run (pipeline.cpp:170-176)
+            rep.verdict, rep.error_kernel, rep.error_detail = "kernel-B-error", "b", mism[p]
+            reports.append(rep)
+            continue
+        oa, ob, names = layouts[p]
+        o0 = int(a.progs[p]["array_off"])
+        sizes = [int(a.arrays[o0 + k]["size"]) for k in oa]
+        vc, base = vc_of[p]
         for side, rr in (("a", ra[p]), ("b", rb[p])):
             if _failed(rr):
                 rep.verdict = f"kernel-{side.upper()}-error"
@@ -76,7 +135,6 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
                 rep.races, rep.safeties, rep.deadlock = rr.races, rr.safeties, rr.deadlock
                 break
             # missing_output (pipeline.cpp:73-87): first unwritten Out cell
-            base = p * n_per
             off = 0
             miss = None
             for name, sz in zip(names, sizes):
@@ -102,7 +160,6 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
         any_undecided = False
         residual = False
         off = 0
-        base = p * n_per
         for name, sz in zip(names, sizes):
             for i in range(sz):
                 v = vc.vcs[base + off + i]
