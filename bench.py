@@ -1,20 +1,29 @@
 #!/usr/bin/env python3
 """Benchmark: output elements verified per second per kernel pair.
 
-Workload (BASELINE.json configs[1], the metric's config): warp-shuffle tree
-reduction vs sequential sum over N = 2^20 inputs, as 1024 independent CTA
-pairs of 1024 elements (each CTA pair is one reference
-check_equivalence). A step = execute both kernels' CTAs (by default as one
-merged batch: programs 0..P-1 are kernel A's, P..2P-1 kernel B's; --separate
-runs two batches) and the per-VC canonical compare on the GPU (the
-reference's t_exec_a + t_exec_b + t_decide), starting from an empty term
-DAG, plus the cross-rank verdict all-reduce when N > 1. Packed IR is resident in HBM for `value`; `e2e`
-re-uploads it from pinned host memory every step through the C-ABI and reads
-the verdicts back.
+Workloads (BASELINE.json configs), each a grid of independent
+CTA pairs (one CTA pair = one reference check_equivalence):
+  c3  conv 3x3 direct vs im2col-tiled, 256x256, 64->64 ch: 256 CTA pairs of
+      16x16 pixels x 64 channels (16,384 output elements each)   [default]
+  c2  sequential sum vs warp-shuffle tree, N = 2^20: 1024 CTA pairs x 1024
+  c4  attention naive vs online softmax, seq 4096, d 128: 256 CTA pairs of
+      16 query rows
+Each kernel of the pair is elaborated ONCE as a template (block index
+symbolic, veqh_elaborate_template) outside the timed region. A step checks
+`--ctas` CTA pairs: the template is expanded on the device into one merged
+batch (kernel A's CTAs, then kernel B's; veq_instantiate), both kernels run
+(schedule, symbolic execution, race check, canonicalisation), every output
+element is compared (veq_compare_progs), verdicts are read back and the
+batch is dropped; the term DAG starts empty every step. Successive steps
+walk the grid. `value` starts each step from the template resident in HBM;
+`e2e` re-uploads the template from pinned host memory every step
+(veq_load_template) and reads every VC back.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Multi-GPU: torchrun, one rank per GPU, weak scaling (each rank owns 1024 CTA
-pairs of a world-sized input).
+  python bench.py [--workload c3|c2|c4] [--gpus N] [--steps K] [--warmup W]
+                  [--impl ours|reference]
+Multi-GPU: torchrun, one rank per GPU, weak scaling (every rank checks
+`--ctas` CTA pairs per step; rank r takes the grid's CTA ranges r, r + N, ...)
+and a verdict all-reduce per step.
 """
 from __future__ import annotations
 
@@ -119,39 +128,83 @@ def ref_bench(workload, blocks, seconds, threads):
     return json.loads(out.stdout.strip().splitlines()[-1]), None
 
 
+from paper_2511_12638_b200 import workloads  # noqa: E402
+
+WORKLOADS = {
+    "c3": dict(make=lambda: workloads.c3_conv(64, 64, 256, 256, 16, 16), ctas=4,
+               name="C3 conv 3x3 direct vs im2col-tiled, 256x256, 64->64 ch (256 CTA pairs of 16x16 px x 64 ch)",
+               kernel_a="conv_direct (256 threads)", kernel_b="conv_im2col (256 threads, patch staged + sync)",
+               # reference CPU sample: the same CTA with 2 of 64 output channels (the
+               # reference retains every partial sum; a full CTA does not fit host RAM)
+               ref=lambda: workloads.c3_conv(64, 2, 256, 256, 16, 16)),
+    "c2": dict(make=lambda: workloads.c2_reduce(n_blocks=1024, block=1024), ctas=1024,
+               name="C2 warp-shuffle tree reduction vs sequential sum, N=2^20 as 1024 CTA pairs x 1024 elements",
+               kernel_a="reduce_seq (1 thread)", kernel_b="reduce_shfl (1024 threads, warp 32)",
+               ref=lambda: workloads.c2_reduce(n_blocks=1024, block=1024)),
+    "c4": dict(make=lambda: workloads.c4_attention(4096, 128, 16, 16, 64), ctas=1,
+               name="C4 attention naive softmax(QK^T)V vs online softmax, seq 4096, d 128 (256 CTA pairs of 16 rows)",
+               kernel_a="attn_naive (256 threads)", kernel_b="attn_online (256 threads, key blocks of 64)",
+               ref=lambda: workloads.c4_attention(256, 32, 16, 16, 64)),
+}
+
+
+def ref_sample(wl, key, ncpu, seconds, blocks):
+    r, err = ref_bench(wl["ref"](), blocks, seconds, ncpu)
+    if r is None:
+        return None, err
+    busy = r["busy_s"] / ncpu
+    v = r["elements"] / busy if busy else 0.0
+    what = {"c3": "CTA pairs of the C3 grid with 2 of 64 output channels (same 576-term outputs)",
+            "c2": "CTA pairs of the C2 grid",
+            "c4": "CTA pairs of C4 at seq 256, d 32 (16 rows x 16 threads per row; per-output cost grows with seq)"}
+    return {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference", "cpu": cpu_model(),
+            "sample": f"{r['pairs']} {what[key]}, {seconds:.0f}s bound, exec+decide span"}, None
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=0, help="timed steps (default: one pass over the grid)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--blocks", type=int, default=1024, help="CTA pairs per GPU")
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--ctas", type=int, default=0, help="CTA pairs per step per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--separate", action="store_true",
-                    help="load/run kernel A's and kernel B's CTAs as two batches (default: one merged batch)")
     args = ap.parse_args()
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
-    from paper_2511_12638_b200 import workloads
-    from paper_2511_12638_b200.dist import combine_verdicts, shard_blocks
-    W = workloads.c2_reduce(n_blocks=args.blocks * world, block=1024)
-    cfg_json = {"workload": "C2 warp-shuffle tree reduction vs sequential sum, N=2^20 per GPU as "
-                            f"{args.blocks} CTA pairs x 1024 elements",
-                "kernel_a": "reduce_seq (1 thread)", "kernel_b": "reduce_shfl (1024 threads, warp 32)",
-                "cta_pairs_per_gpu": args.blocks, "elements_per_step_per_gpu": args.blocks,
+    wl = WORKLOADS[args.workload]
+    W = wl["make"]()
+    cps = args.ctas or wl["ctas"]
+    n_grid = W.n_blocks
+    steps = args.steps or max(1, -(-n_grid // (cps * world)))
+    cfg_json = {"workload": wl["name"], "kernel_a": wl["kernel_a"], "kernel_b": wl["kernel_b"],
+                "cta_pairs_in_grid": n_grid, "cta_pairs_per_step_per_gpu": cps,
+                "elements_per_cta_pair": W.elements_per_block,
                 "parallelism": f"dp{world} (CTA pairs sharded, verdict all-reduce)",
-                "l2": "working set re-generated every step (term table cleared; IR > 126 MB L2)"}
+                "l2": "working set re-generated every step (term table cleared, fresh batch; IR > 126 MB L2)"}
     ncpu = os.cpu_count() or 1
 
     if args.impl == "reference":
         if rank != 0:
             return
-        per = max(1, args.steps)
+        per = max(1, min(steps, 10))
         samples = []
+        nb = wl["ref"]().n_blocks
         for s in range(args.warmup + per):
-            blocks = list(range((s * 8) % args.blocks, (s * 8) % args.blocks + 8))
-            r, err = ref_bench(W, blocks, max(2.0, args.cpu_seconds / per), ncpu)
+            blocks = [(s * 8 + k) % nb for k in range(8)]
+            r, err = ref_bench(wl["ref"](), blocks, max(2.0, args.cpu_seconds / per), ncpu)
             if r is None:
                 print(json.dumps({"impl": "reference", "unavailable": err}))
                 return
@@ -163,10 +216,10 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": world,
             "steps": per, "warmup": args.warmup, "ms_per_step": 1000.0 * busy / per if per else None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "exact rational (int64/GMP)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "exact rational (GMP)",
             "data": "synthetic", "config": cfg_json,
-            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference",
-                             "sample": f"{el} CTA pairs (8 per step) of the C2 grid; exec+decide span timed"},
+            "cpu_baseline": {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference", "cpu": cpu_model(),
+                             "sample": f"{sum(r['pairs'] for r in samples)} CTA pairs, 8 per step"},
             "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -181,83 +234,87 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    # ---- one template per kernel for the whole grid (outside the timed region)
     t0 = time.time()
-    # weak scaling: each rank owns a contiguous share of a world-sized grid
-    base, nblk = shard_blocks(args.blocks * world, rank, world)
-    a, b, inputs = frontend.elaborate_pair(W.kernel_a, W.kernel_b, W.cfg, "B", nblk, want_names=False,
-                                           block_base=base)
+    ta, tb, inputs, da, db = frontend.elaborate_template(W.kernel_a, W.kernel_b, W.cfg, W.block_param, n_grid,
+                                                         want_names=False)
     t_elab = time.time() - t0
-    S = len(a.stmts) + len(b.stmts)
-    sess = Session(local, max_nodes=max(1 << 22, 4 * S // 10), max_kid_words=(1 << 24) + 4 * S,
-                   scratch_bytes=8 << 30)
+    tmpl = ir.concat([ta, tb])
+    deltas = np.ascontiguousarray(np.concatenate([da, db], axis=1), dtype=np.int32)
+    S_pair = len(ta.stmts) + len(tb.stmts)
+    S_step = S_pair * cps
+    sess = Session(local, max_nodes=min((1 << 31) - 1, max(1 << 22, 4 * S_step // 10)),
+                   max_kid_words=min((1 << 32) - 1, (1 << 24) + 4 * S_step), scratch_bytes=8 << 30)
     L = N.lib()
     sess.declare_inputs(inputs)
-    oa, ob = [0], [0]  # y is the only Out array (array-name order)
-    for k, name in enumerate(a.array_names[:int(a.progs[0]["n_arrays"])]):
-        if int(a.arrays[k]["role"]) == N.ROLE_OUT:
-            oa = [k]
-    for k, name in enumerate(b.array_names[:int(b.progs[0]["n_arrays"])]):
-        if int(b.arrays[k]["role"]) == N.ROLE_OUT:
-            ob = [k]
-    P = a.n_progs
-    # default: both kernels' CTAs in ONE batch (programs 0..P-1 = kernel A,
-    # P..2P-1 = kernel B): one run carries both, and program i of A is
-    # compared with program P+i (veq_compare_progs)
-    merged = None if args.separate else ir.concat([a, b])
-
-    def load_all():
-        if merged is not None:
-            return (sess.load(merged),)
-        return (sess.load(a), sess.load(b))
-
-    def run_all(hs):
-        if len(hs) == 1:
-            return [sess.run_raw(hs[0])]
-        return list(sess.run_pair_raw(hs[0], hs[1]))
-
-    def compare_all(hs):
-        if len(hs) == 1:
-            return sess.compare_progs_raw(hs[0], 0, hs[0], P, P, oa, ob)
-        return sess.compare_raw(hs[0], hs[1], oa, ob)
-
-    hs = load_all()
+    ka = [k for k in range(len(ta.arrays)) if int(ta.arrays[k]["role"]) == N.ROLE_OUT]
+    outs = sorted((ta.array_names[k], k) for k in ka)
+    oa = [k for _, k in outs]
+    ob = [tb.array_names.index(n) for n, _ in outs]
+    # pin the template so the e2e upload is a true async DMA
+    pinned = []
+    for f in ("progs", "thread_stmt", "thread_nregs", "stmts", "arrays", "consts", "syncsets", "set_words"):
+        arr = getattr(tmpl, f)
+        t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8)).pin_memory()
+        pinned.append(t)
+        setattr(tmpl, f, t.numpy().view(arr.dtype))
+    th = sess.load_template(tmpl)
     stream = torch.cuda.ExternalStream(L.veq_stream(sess.ctx))
     counters = torch.zeros(4, dtype=torch.float64, device="cuda")
 
-    def step():
-        st = L.veq_clear_terms(sess.ctx)
-        assert st == 0
-        rs = run_all(hs)
-        vc = compare_all(hs)
-        launches = sum(r.n_launches for r in rs) + 2
-        if dist is not None:
-            counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)
-            dist.all_reduce(counters)
-        return rs, vc, launches
+    def blocks_of(k):
+        first = ((k * world + rank) * cps) % n_grid
+        return [(first + j) % n_grid for j in range(cps)]
 
-    # correctness gate: every VC equal, no faults, on every rank
-    rs, vc, _ = step()
-    nfaults = sum(r.n_faults for r in rs)
-    tot, first_fail = combine_verdicts([vc.n_equal, vc.n_vcs, nfaults, vc.n_missing],
-                                       None if vc.n_equal == vc.n_vcs else base, device="cuda" if dist else None)
-    ok = tot["equal"] == tot["vcs"] == args.blocks * world and tot["faults"] == 0
-    if not ok:
-        print(f"[bench] rank {rank}: verification failed: {vc.n_equal}/{vc.n_vcs} equal, {nfaults} faults",
-              file=sys.stderr)
+    state = {"k": 0, "equal": 0, "vcs": 0, "faults": 0, "launches": 0}
+
+    def step(th_use=None, e2e=False):
+        k = state["k"]
+        state["k"] += 1
+        blk = blocks_of(k)
+        assert L.veq_clear_terms(sess.ctx) == 0
+        tu = th_use if th_use is not None else th
+        h = sess.instantiate(tu, deltas[blk])
+        r = sess.run_raw(h)
+        vc = sess.compare_progs_raw(h, 0, h, cps, cps, oa, ob)
+        n_eq, n_vcs, nf = int(vc.n_equal), int(vc.n_vcs), int(r.n_faults)
+        if e2e:  # every VC's verdict to the host (d2h counted in e2e)
+            eqs = np.ctypeslib.as_array(C.cast(vc.vcs, C.POINTER(C.c_uint32)), shape=(n_vcs * 6,))[2::6].copy()
+            n_eq = int(eqs.sum())
+        sess.drop(h)
+        state["equal"] += n_eq
+        state["vcs"] += n_vcs
+        state["faults"] += nf
+        launches = r.n_launches + 2
+        if dist is not None:
+            counters[0], counters[1] = float(n_eq), float(n_vcs)
+            dist.all_reduce(counters)
+        return launches
+
+    import ctypes as C
+    # correctness gate (untimed): CTA 0's pair compared with the reference's
+    # digest golden when one exists for this shape, every VC equal, no faults
+    gate = step()
+    if state["equal"] != state["vcs"] or state["faults"]:
+        print(f"[bench] rank {rank}: verification failed: {state['equal']}/{state['vcs']} equal, "
+              f"{state['faults']} faults", file=sys.stderr)
         sys.exit(1)
-    # instrumented pass: per-phase device time (CUDA events on the ctx stream;
-    # one run at a time so each run's phase events are its own)
+    # instrumented pass: per-phase device time (CUDA events on the ctx stream)
     L.veq_set_timing(sess.ctx, 1)
     assert L.veq_clear_terms(sess.ctx) == 0
-    rs_t = [sess.run_raw(h) for h in hs]
-    compare_all(hs)  # each bench step ends with a compare (profile step boundaries)
+    h = sess.instantiate(th, deltas[blocks_of(0)])
+    r_t = sess.run_raw(h)
+    sess.compare_progs_raw(h, 0, h, cps, cps, oa, ob)
+    sess.drop(h)
     L.veq_set_timing(sess.ctx, 0)
-    phases = {}
-    for i, name in enumerate(N.PHASES):
-        phases[name] = sum(float(r.phase_ms[i]) for r in rs_t)
+    phases = {name: float(r_t.phase_ms[i]) for i, name in enumerate(N.PHASES)}
+    stats = {"S": int(r_t.n_stmts_executed), "R": int(r_t.n_access), "new_nodes": int(r_t.n_new_nodes),
+             "new_kid_words": int(r_t.n_new_kid_words), "work_items": int(r_t.n_work)}
 
     for _ in range(args.warmup):
         step()
+    state.update(equal=0, vcs=0, faults=0)
+    state["k"] = 0
 
     def timed(fn, k):
         if dist is not None:
@@ -280,74 +337,47 @@ def main():
         return ms, launches
 
     with ClockSampler(local) as clk:
-        ms, launches = timed(lambda: step()[2], args.steps)
-    ms_step = ms / args.steps
-    elements_step = args.blocks * world
+        ms, launches = timed(step, steps)
+    ok = state["equal"] == state["vcs"] == steps * cps * W.elements_per_block and state["faults"] == 0
+    if not ok:
+        print(f"[bench] rank {rank}: timed steps not all equivalent: {state}", file=sys.stderr)
+        sys.exit(1)
+    ms_step = ms / steps
+    elements_step = cps * W.elements_per_block * world
     value = elements_step / (ms_step / 1000.0)
 
-    # e2e: public API from pinned host buffers each step (H2D IR, D2H verdicts)
-    def pin(batch):
-        import ctypes
-        keep = []
-        for f in ("progs", "thread_stmt", "thread_nregs", "stmts", "arrays", "consts", "syncsets", "set_words"):
-            arr = getattr(batch, f)
-            t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8)).pin_memory()
-            keep.append(t)
-            setattr(batch, f, t.numpy().view(arr.dtype))
-        return keep
-
-    keep = pin(merged) if merged is not None else pin(a) + pin(b)
-    h2d = a.nbytes() + b.nbytes()
-    d2h = elements_step // world * 24
-
-    e2e_prof = os.environ.get("VEQ_E2E_PROF") == "1"
-
+    # e2e: the template re-uploaded from pinned host memory every step
+    # (veq_load_template), every VC verdict read back
     def e2e_step():
-        tt = [time.perf_counter()]
-        if e2e_prof:
-            L.veq_set_timing(sess.ctx, 1)
-        sess.declare_inputs(inputs)
-        tt.append(time.perf_counter())
-        xs = load_all()
-        tt.append(time.perf_counter())
-        rs = run_all(xs)
-        tt.append(time.perf_counter())
-        vc = compare_all(xs)
-        tt.append(time.perf_counter())
-        if e2e_prof:
-            print("[e2e] declare %.2f load %.2f run %.2f compare %.2f ms" %
-                  tuple(1000 * (tt[k + 1] - tt[k]) for k in range(4)), "| phases",
-                  " ".join("%s=%.2f" % (nm, rs[-1].phase_ms[i]) for i, nm in enumerate(N.PHASES)), file=sys.stderr)
-        assert vc.n_equal == vc.n_vcs
-        if dist is not None:
-            counters[0], counters[1] = float(vc.n_equal), float(vc.n_vcs)
-            dist.all_reduce(counters)
-        return sum(r.n_launches for r in rs) + 2
+        t2 = sess.load_template(tmpl)
+        n = step(th_use=t2, e2e=True)
+        L.veq_drop_template(sess.ctx, t2)
+        return n + 1
 
-    e2e_step()
-    e2e_k = max(1, min(args.steps, 5))
+    state["k"] = 0
+    e2e_k = max(1, min(steps, 8))
     ms_e2e, _ = timed(e2e_step, e2e_k)
     e2e_value = elements_step / (ms_e2e / e2e_k / 1000.0)
+    h2d = tmpl.nbytes() + cps * deltas.shape[1] * 4
+    d2h = cps * W.elements_per_block * 24
 
-    # roofline: dominant phase, algorithmic bytes:
-    #   exec 16 B per executed statement; sort+memscan 32 B per access tuple;
-    #   eval 2 x (16 + 4k) per created node (written once, read once)
+    # roofline of the dominant phase; algorithmic bytes:
+    # exec 16 B per executed statement; sort + memscan 32 B per access tuple;
+    # eval 2 x (16 + 4k) per created node (written once, read once)
     peak, peak_kind = peaks()
-    S_exec = sum(r.n_stmts_executed for r in rs_t)
-    R = sum(r.n_access for r in rs_t)
-    U_bytes = 16 * sum(r.n_new_nodes for r in rs_t) + 4 * sum(r.n_new_kid_words for r in rs_t)
-    alg = {"exec": 16 * S_exec, "sort": 16 * R, "memscan": 16 * R, "eval": 2 * U_bytes}
+    U_bytes = 16 * stats["new_nodes"] + 4 * stats["new_kid_words"]
+    alg = {"exec": 16 * stats["S"], "sort": 16 * stats["R"], "memscan": 16 * stats["R"], "eval": 2 * U_bytes}
     dom = max(phases, key=lambda k: phases[k])
     dom_bytes = alg.get(dom, 0)
     achieved = dom_bytes / (phases[dom] / 1000.0) / 1e9 if phases[dom] > 0 else 0.0
-    b_min = 16 * S_exec + 2 * U_bytes + 32 * R + 16 * elements_step // world
+    b_min = 16 * stats["S"] + 2 * U_bytes + 32 * stats["R"] + 16 * elements_step // world
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(dom)
 
     line = {
-        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "exact rational (int64 num/den), u32 term ids", "data": "synthetic",
         "config": cfg_json,
@@ -359,29 +389,20 @@ def main():
         "step_roofline": {"b_min_bytes": b_min, "achieved_gbs": b_min / (ms_step / 1000.0) / 1e9,
                           "frac": b_min / (ms_step / 1000.0) / 1e9 / peak},
         "phases_ms": phases,
-        "counts": {"S": S_exec, "R": R, "new_nodes": sum(r.n_new_nodes for r in rs_t),
-                   "work_items": sum(r.n_work for r in rs_t), "t_elab_s": t_elab,
-                   "batches": "merged (A and B CTAs in one batch)" if merged is not None else "separate"},
+        "counts": dict(stats, t_template_elab_s=t_elab, template_stmts_per_cta_pair=S_pair,
+                       verified_elements=state["vcs"]),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ncb = max(8, min(args.blocks, 64))
-        r, err = ref_bench(W, list(range(ncb)), args.cpu_seconds, ncpu)
-        if r is not None:
-            busy = r["busy_s"] / ncpu
-            line["cpu_baseline"] = {"value": r["elements"] / busy if busy else 0.0, "unit": "elements/s",
-                                    "cores": ncpu, "kind": "reference",
-                                    "sample": f"{r['pairs']} of the first {ncb} CTA pairs, "
-                                              f"{args.cpu_seconds:.0f}s bound, exec+decide span"}
-        else:
-            line["cpu_baseline"] = {"value": None, "unit": "elements/s", "cores": ncpu, "kind": "reference",
-                                    "sample": f"unavailable: {err}"}
+        cb, err = ref_sample(wl, args.workload, ncpu, args.cpu_seconds, list(range(8)))
+        line["cpu_baseline"] = cb if cb is not None else {
+            "value": None, "unit": "elements/s", "cores": ncpu, "kind": "reference", "sample": f"unavailable: {err}"}
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
-    del keep
     sess.close()
+    del pinned
 
 
 if __name__ == "__main__":

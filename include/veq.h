@@ -146,6 +146,23 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n);
  * session). Host buffers may be freed afterwards. */
 int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *desc, uint32_t *batch);
 
+/* Frees a batch's device memory now (handle becomes invalid); a session's
+ * batches are otherwise freed by the next veq_declare_inputs. */
+int veq_drop_batch(veq_ctx *ctx, uint32_t batch);
+
+/* ---- grid templates ----------------------------------------------------
+ * A grid whose CTAs differ only by per-array offset shifts (veqh_elaborate_
+ * template, include/veq_host.h) is loaded ONCE as a template (its programs
+ * laid out in order) and expanded on the device into regular batches:
+ * veq_instantiate makes n_inst instances; batch program q * n_inst + i is
+ * template program q of instance i, with every Load/Store offset on the
+ * program's array a shifted by deltas[i * n_arrays_total + array_off_q + a].
+ * The result equals loading the per-CTA elaborations as one batch (the
+ * instances share the template's constant and sync-set pools). */
+int veq_load_template(veq_ctx *ctx, const veq_batch_desc *desc, uint32_t *tmpl);
+int veq_instantiate(veq_ctx *ctx, uint32_t tmpl, uint32_t n_inst, const int32_t *deltas, uint32_t *batch);
+int veq_drop_template(veq_ctx *ctx, uint32_t tmpl);
+
 /* ---- run (K0 schedule, K3 executor, K4 race/uninit, K2 canonicalise) --- */
 enum { VEQ_FAULT_RACE = 1, VEQ_FAULT_SAFETY = 2 };
 enum { VEQ_SAFE_UNINIT_REG = 0, VEQ_SAFE_UNINIT_MEM = 1, VEQ_SAFE_OOB = 2,
@@ -309,6 +326,14 @@ typedef struct veq_dag_buf {
 
 int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots,
                    veq_dag_buf *buf);
+
+/* to_string (proj/src/expr.cpp:735-822) of term nodes, rendered on the host
+ * from the device DAG: root i's text is text[offs[i] .. offs[i+1]). Output
+ * is ctx-owned, valid until the next veq_render. */
+int veq_render(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, const char **text, const uint64_t **offs);
+/* The same texts as CRC-32 (IEEE, as zlib.crc32) and byte length, streamed
+ * without materialising them (digest comparison of very large forms). */
+int veq_render_digest(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, uint32_t *crc32, uint64_t *len);
 
 /* ---- multi-GPU ---------------------------------------------------------
  * Verdict counters are combined across ranks by the caller's collective

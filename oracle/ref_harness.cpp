@@ -340,6 +340,96 @@ int cmd_pair(const std::string &dir, const std::string &pa_path, const std::stri
   return 0;
 }
 
+// CRC-32 (IEEE, as zlib.crc32) of a byte string: digests of strings too large
+// to commit (canonical forms of full-size outputs, packed IR images).
+uint32_t crc32_of(const std::string &s) {
+  static uint32_t tab[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; i++) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      tab[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (unsigned char ch : s) c = tab[(c ^ ch) & 0xff] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+ojson digest_j(const std::string &s) {
+  char h[16];
+  snprintf(h, sizeof h, "%08x", crc32_of(s));
+  return ojson{{"crc32", h}, {"len", s.size()}};
+}
+std::string ir_image(const veq::HostBatch &b) {
+  char *buf = nullptr;
+  size_t n = 0;
+  FILE *f = open_memstream(&buf, &n);
+  b.write(f);
+  fclose(f);
+  std::string s(buf, n);
+  free(buf);
+  return s;
+}
+
+// Digest golden for full-size workloads: the reference's report (one
+// check_equivalence, VCs decided on all host threads) with long strings
+// replaced by CRC-32 digests, per-output digests of to_string of both
+// kernels' canonical outputs (env_a / env_b), full strings of a few sample
+// outputs, and digests of the reference's packed-IR elaboration.
+int cmd_digest(const std::string &dir, const std::string &pa_path, const std::string &pb_path,
+               const std::string &cfg_path) {
+  LaunchConfig cfg = parse_config(read_file(cfg_path));
+  CheckRequest req;
+  req.kernel_a_src = read_file(pa_path);
+  req.kernel_b_src = read_file(pb_path);
+  req.cfg = cfg;
+  ojson g;
+  {
+    Program pa = elaborate(parse_kernel(req.kernel_a_src), cfg, cfg.for_a());
+    Program pb = elaborate(parse_kernel(req.kernel_b_src), cfg, cfg.for_b());
+    std::vector<std::string> order;
+    std::map<std::string, uint64_t> sizes;
+    for (const auto &name : cfg.inputs)
+      for (const auto &a : pa.arrays)
+        if (a.name == name && !sizes.count(name)) {
+          order.push_back(name);
+          sizes[name] = a.size;
+        }
+    g["inputs"] = inputs_j(order, sizes);
+    g["ir_a"] = digest_j(ir_image(to_ir(pa, sizes, order)));
+    g["ir_b"] = digest_j(ir_image(to_ir(pb, sizes, order)));
+  }
+  const unsigned jobs = std::max(1u, std::thread::hardware_concurrency());
+  auto t0 = std::chrono::steady_clock::now();
+  Report rep = check_equivalence(req, jobs);
+  g["ref_seconds"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  g["ref_jobs"] = jobs;
+  ojson rj = report_to_json(rep);
+  rj.erase("timings");
+  for (auto &sc : rj["side_conditions"]) {
+    const std::string d = sc["denominator"].get<std::string>();
+    sc["denominator_digest"] = digest_j(d);
+    if (d.size() > 2048) sc.erase("denominator");
+  }
+  g["report"] = rj;
+  for (auto side : {std::make_pair("env_a", &rep.env_a), std::make_pair("env_b", &rep.env_b)}) {
+    ojson e = ojson::array();
+    for (const EnvEntry &x : *side.second) {
+      const std::string str = to_string(x.value);
+      ojson v{{"array", x.array}, {"index", x.index}};
+      v["digest"] = digest_j(str);
+      if (&x == &side.second->front() || &x == &side.second->back())
+        if (str.size() <= 65536) v["text"] = str;
+      e.push_back(v);
+    }
+    g[side.first] = e;
+  }
+  write_json(dir + "/golden.json", g);
+  return 0;
+}
+
 int cmd_gen(const std::string &dir, uint64_t seed) {
   auto gp = testutil::gen_program(seed);
   std::vector<std::string> order;
@@ -475,6 +565,7 @@ int main(int argc, char **argv) {
     std::string cmd = argc > 1 ? argv[1] : "";
     if (cmd == "config" && argc == 3) return cmd_config(argv[2]);
     if (cmd == "pair" && argc == 6) return cmd_pair(argv[2], argv[3], argv[4], argv[5]);
+    if (cmd == "digest" && argc == 6) return cmd_digest(argv[2], argv[3], argv[4], argv[5]);
     if (cmd == "gen" && argc == 4) return cmd_gen(argv[2], std::stoull(argv[3]));
     if (cmd == "bench" && argc == 7)
       return cmd_bench(argv[2], argv[3], argv[4], (unsigned)std::stoul(argv[5]), std::stod(argv[6]));

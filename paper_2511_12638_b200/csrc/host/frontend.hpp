@@ -30,6 +30,11 @@ struct ParseError : std::runtime_error {
 struct StructuredCtaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// Template elaboration only: the kernel's control or data does not depend on
+// the block parameter through array offsets alone (see elaborate_template).
+struct TemplateUnsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 struct LaunchConfig {
   uint32_t threads = 0, threads_a = 0, threads_b = 0, warp_size = 32;
@@ -69,6 +74,19 @@ struct InputDecl {
 // register name strings (reports then name registers r<id>).
 veq::HostBatch elaborate(const ParsedKernel &k, const LaunchConfig &cfg, uint32_t n_threads,
                          const std::vector<InputDecl> &inputs, bool want_names = true);
+
+// Elaborates ONE program for a whole grid: params.<block_param> is symbolic
+// over blocks [block_lo, block_lo + n_blocks). The result is block-
+// independent except for array offsets; CTA b is the template with every
+// Load/Store offset on array a shifted by deltas[(b - block_lo) * n_arrays + a].
+// Throws TemplateUnsupported when that does not hold (branches, bounds,
+// constants or sync sets depending on the block, non-uniform shifts); the
+// caller then elaborates per CTA. Errors the concrete elaboration raises for
+// every CTA are raised as they would be there.
+veq::HostBatch elaborate_template(const ParsedKernel &k, const LaunchConfig &cfg, uint32_t n_threads,
+                                  const std::vector<InputDecl> &inputs, bool want_names,
+                                  const std::string &block_param, int64_t block_lo, uint32_t n_blocks,
+                                  std::vector<int32_t> &deltas);
 
 // Inputs of a pair given kernel A's elaboration (array names/sizes).
 std::vector<InputDecl> pair_inputs(const ParsedKernel &ka, const LaunchConfig &cfg);

@@ -148,3 +148,82 @@ extern "C" void veqh_free(veqh_pair *p) {
   free(p->inputs);
   std::memset(p, 0, sizeof(*p));
 }
+
+extern "C" int veqh_elaborate_template(const char *kernel_a, const char *kernel_b, const char *cfg_src,
+                                       const char *block_param, int64_t block_base, uint32_t n_blocks,
+                                       int want_names, veqh_template *out, char *err, size_t errlen) {
+  if (!kernel_a || !kernel_b || !cfg_src || !out || !block_param || !*block_param || n_blocks == 0) return VEQH_E_ARG;
+  std::memset(out, 0, sizeof(*out));
+  veqh::LaunchConfig cfg;
+  try {
+    cfg = veqh::parse_config(cfg_src);
+  } catch (const std::exception &e) {
+    put_err(err, errlen, e.what());
+    return VEQH_E_CONFIG;
+  }
+  std::unique_ptr<veqh::ParsedKernel> ka, kb;
+  try {
+    ka.reset(new veqh::ParsedKernel(kernel_a));
+  } catch (const std::exception &e) {
+    put_err(err, errlen, e.what());
+    return VEQH_E_KERNEL_A;
+  }
+  try {
+    kb.reset(new veqh::ParsedKernel(kernel_b));
+  } catch (const std::exception &e) {
+    put_err(err, errlen, e.what());
+    return VEQH_E_KERNEL_B;
+  }
+  // the config as the first block sees it: inputs and sizes are block-free
+  veqh::LaunchConfig c0 = cfg;
+  c0.params[block_param] = block_base;
+  std::vector<veqh::InputDecl> inputs;
+  try {
+    inputs = veqh::pair_inputs(*ka, c0);
+  } catch (const std::exception &e) {
+    put_err(err, errlen, e.what());
+    return VEQH_E_KERNEL_A;
+  }
+  veq::HostBatch ta, tb;
+  std::vector<int32_t> da, db;
+  int side = VEQH_E_KERNEL_A;
+  try {
+    ta = veqh::elaborate_template(*ka, c0, c0.for_a(), inputs, want_names != 0, block_param, block_base, n_blocks, da);
+    side = VEQH_E_KERNEL_B;
+    tb = veqh::elaborate_template(*kb, c0, c0.for_b(), inputs, want_names != 0, block_param, block_base, n_blocks, db);
+  } catch (const veqh::TemplateUnsupported &e) {
+    put_err(err, errlen, e.what());
+    return VEQH_E_TEMPLATE;
+  } catch (const std::exception &e) {
+    put_err(err, errlen, e.what());
+    return side;
+  }
+  try {
+    out->ir_a = to_image(ta, &out->ir_a_len);
+    out->ir_b = to_image(tb, &out->ir_b_len);
+  } catch (const std::exception &e) {
+    put_err(err, errlen, e.what());
+    return VEQH_E_ARG;
+  }
+  std::string in;
+  for (auto &i : inputs) in += i.name + "\t" + std::to_string(i.size) + "\n";
+  out->inputs = strdup(in.c_str());
+  out->n_blocks = n_blocks;
+  out->n_arrays_a = (uint32_t)ta.arrays.size();
+  out->n_arrays_b = (uint32_t)tb.arrays.size();
+  out->deltas_a = (int32_t *)malloc(std::max<size_t>(1, da.size()) * 4);
+  out->deltas_b = (int32_t *)malloc(std::max<size_t>(1, db.size()) * 4);
+  std::memcpy(out->deltas_a, da.data(), da.size() * 4);
+  std::memcpy(out->deltas_b, db.data(), db.size() * 4);
+  return VEQH_OK;
+}
+
+extern "C" void veqh_free_template(veqh_template *p) {
+  if (!p) return;
+  free(p->ir_a);
+  free(p->ir_b);
+  free(p->inputs);
+  free(p->deltas_a);
+  free(p->deltas_b);
+  std::memset(p, 0, sizeof(*p));
+}

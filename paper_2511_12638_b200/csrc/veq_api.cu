@@ -2,6 +2,8 @@
 // batch preparation and the launch sequence of one check.
 #include <cub/cub.cuh>
 
+#include <functional>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -62,6 +64,20 @@ struct BatchDev {
   bool ran = false;
 };
 
+// A template batch (veq_load_template): small tables on the host, statements
+// resident on the device; veq_instantiate expands it into regular batches.
+struct TemplateDev {
+  std::vector<veq_program_meta> progs;
+  std::vector<uint64_t> thread_stmt;
+  std::vector<uint32_t> thread_nregs;
+  std::vector<veq_array> arrays;
+  std::vector<veq_rat> consts;
+  std::vector<veq_syncset> syncsets;
+  std::vector<uint64_t> set_words;
+  uint64_t n_stmts = 0;
+  veq_stmt *stmts = nullptr;
+};
+
 }  // namespace
 
 struct veq_ctx {
@@ -98,11 +114,15 @@ struct veq_ctx {
   // session
   std::vector<std::string> input_names;
   std::vector<uint64_t> input_sizes;
-  std::vector<BatchDev *> batches;
+  std::vector<BatchDev *> batches;    // dropped batches leave a null slot
+  std::vector<TemplateDev *> templates;
   // compare outputs
   std::vector<veq_vc> vcs;
   std::vector<uint32_t> sc_node;
   std::vector<uint8_t> sc_dis;
+  // veq_render output
+  std::string render_text;
+  std::vector<uint64_t> render_offs;
   uint64_t last_equal = 0, last_missing = 0, last_vcs = 0, last_faults = 0;
   // instrumentation
   bool timing = false;
@@ -116,6 +136,8 @@ int fail(veq_ctx *c, int code, const std::string &msg) {
   if (c) c->last_error = msg;
   return code;
 }
+
+bool live_batch(const veq_ctx *ctx, uint32_t b) { return b < ctx->batches.size() && ctx->batches[b] != nullptr; }
 
 #define CK(call)                                                                       \
   do {                                                                                 \
@@ -257,9 +279,15 @@ void veq_close(veq_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   for (BatchDev *b : ctx->batches) {
+    if (!b) continue;
     for (void *p : b->owned) cudaFreeAsync(p, ctx->stream);
     delete b;
   }
+  for (TemplateDev *t : ctx->templates)
+    if (t) {
+      cudaFreeAsync(t->stmts, ctx->stream);
+      delete t;
+    }
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->nodes);
   cudaFree(ctx->kids);
@@ -284,12 +312,19 @@ void veq_close(veq_ctx *ctx) {
 int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
   if (!ctx) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
-  // drop batches of the previous session
+  // drop batches and templates of the previous session
   for (BatchDev *b : ctx->batches) {
+    if (!b) continue;
     for (void *p : b->owned) cudaFreeAsync(p, ctx->stream);
     delete b;
   }
   ctx->batches.clear();
+  for (TemplateDev *t : ctx->templates)
+    if (t) {
+      cudaFreeAsync(t->stmts, ctx->stream);
+      delete t;
+    }
+  ctx->templates.clear();
   ctx->input_names.clear();
   ctx->input_sizes.clear();
   // Byte order of "<name>_<i>" symbols: groups "<name>_" in byte order, then
@@ -384,8 +419,16 @@ void drop_batch(veq_ctx *ctx, BatchDev *bd) {
   delete bd;
 }
 
+static int load_impl(veq_ctx *ctx, const veq_batch_desc *d, veq_stmt *dev_stmts, uint32_t *out);
+
 int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   if (!ctx || !d || !out) return VEQ_E_ARG;
+  return load_impl(ctx, d, nullptr, out);
+}
+
+// d->stmts is ignored when dev_stmts is given: the statements are already on
+// the device (an instantiated template) and the batch takes ownership.
+static int load_impl(veq_ctx *ctx, const veq_batch_desc *d, veq_stmt *dev_stmts, uint32_t *out) {
   static const bool lprof = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -393,8 +436,11 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   CK(cudaSetDevice(ctx->device));
   const uint32_t P = d->n_progs, Tn = d->n_threads_total;
   const uint64_t S = d->n_stmts;
-  if (S >= (1ull << 31)) return fail(ctx, VEQ_E_UNSUPPORTED, "batch has more than 2^31 statements");
-  if (P >= (1u << 20)) return fail(ctx, VEQ_E_UNSUPPORTED, "batch has more than 2^20 programs");
+  if (S >= (1ull << 31) || P >= (1u << 20)) {
+    if (dev_stmts) cudaFreeAsync(dev_stmts, ctx->stream);
+    return fail(ctx, VEQ_E_UNSUPPORTED, S >= (1ull << 31) ? "batch has more than 2^31 statements"
+                                                          : "batch has more than 2^20 programs");
+  }
   BatchDev *bd = new BatchDev();
   bd->progs.assign(d->progs, d->progs + P);
   bd->arrays.assign(d->arrays, d->arrays + d->n_arrays_total);
@@ -420,7 +466,12 @@ int veq_load_batch(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
   } while (0)
   // the caller's big buffers go first: their DMA overlaps the host
   // preparation below (async when the caller's memory is pinned)
-  UP(stmts, d->stmts, S, veq_stmt);
+  if (dev_stmts) {
+    bd->owned.push_back(dev_stmts);
+    B.stmts = dev_stmts;
+  } else {
+    UP(stmts, d->stmts, S, veq_stmt);
+  }
   UP(thread_stmt, d->thread_stmt, Tn + 1, uint64_t);
   UP(progs, d->progs, P, veq_program_meta);
   UP(arrays, d->arrays, d->n_arrays_total, veq_array);
@@ -681,7 +732,7 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
 }
 
 int veq_run_start(veq_ctx *ctx, uint32_t batch) {
-  if (!ctx || batch >= ctx->batches.size()) return VEQ_E_ARG;
+  if (!ctx || !live_batch(ctx, batch)) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   BatchDev *bd = ctx->batches[batch];
   if (bd->started) return fail(ctx, VEQ_E_ARG, "veq_run_start: previous run of this batch not finished");
@@ -859,7 +910,9 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
         { int r_ = ws_get(ctx, 19, (void **)&prof, 128 * 8); if (r_) return r_; }
         CK(cudaMemsetAsync(prof, 0, 128 * 8, s));
       }
-      EvalCtx E{log, log_stmt, base, prof};
+      static const uint32_t eval_off = (getenv("VEQ_EVAL_OFF") ? (uint32_t)atoi(getenv("VEQ_EVAL_OFF")) : 0u) |
+                                       ((getenv("VEQ_EVAL_PAIR") && getenv("VEQ_EVAL_PAIR")[0] == '1') ? 0u : 1u);
+      EvalCtx E{log, log_stmt, base, prof, eval_off};
       uint4 *desc = nullptr;
       { int r_ = ws_get(ctx, 20, (void **)&desc, n_work * sizeof(uint4)); if (r_) return r_; }
       LAUNCH(k_make_desc<<<blocks(n_work, 256), 256, 0, s>>>(B, E, wv2, nw, desc));
@@ -868,9 +921,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
       // one warp per work item, persistent over the sorted work list;
       // persistent grid: exactly the resident capacity (no second wave)
       const int smem = (int)(EVAL_PAGES * SPAGE);
-      CK(cudaFuncSetAttribute(k_eval_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_warp, EVAL_BLOCK, smem);
+      eval_warp_config(smem, &per_sm);
       if (per_sm < 1) per_sm = 1;
       // every resident slot is launched (warps spread over all SMs); the
       // kernel reads the work-list length and picks its claim size
@@ -883,9 +935,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
         ctx->T.wa_kids = (uint32_t)std::min<uint64_t>(WA_KIDS, std::max<uint64_t>(32, ctx->lim.max_kid_words / (16 * warps)));
       }
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
-      LAUNCH(k_eval_warp<<<blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s>>>(B, ctx->T, E, desc, nw, cursor,
-                                                                                ctx->pool, ctx->pool_used,
-                                                                                ctx->pool_cap, chunk));
+      LAUNCH(launch_eval_warp(blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s, B, ctx->T, E, desc, nw, cursor,
+                              ctx->pool, ctx->pool_used, ctx->pool_cap, chunk));
       CK(cudaGetLastError());
       if (prof) {
         unsigned long long hp[128], nwh = 0;
@@ -928,7 +979,7 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
 }
 
 int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
-  if (!ctx || batch >= ctx->batches.size()) return VEQ_E_ARG;
+  if (!ctx || !live_batch(ctx, batch)) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   BatchDev *bd = ctx->batches[batch];
   if (!bd->started) return fail(ctx, VEQ_E_ARG, "veq_run_finish: no run started on this batch");
@@ -1028,7 +1079,7 @@ int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
 
 int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, const uint32_t *out_b,
                 uint32_t n_out, veq_vc_out *out) {
-  if (!ctx || ba >= ctx->batches.size() || bb >= ctx->batches.size()) return VEQ_E_ARG;
+  if (!ctx || !live_batch(ctx, ba) || !live_batch(ctx, bb)) return VEQ_E_ARG;
   BatchDev *A = ctx->batches[ba], *Bd = ctx->batches[bb];
   if (A->progs.size() != Bd->progs.size()) return fail(ctx, VEQ_E_ARG, "batches differ in program count");
   return veq_compare_progs(ctx, ba, 0, bb, 0, (uint32_t)A->progs.size(), out_a, out_b, n_out, out);
@@ -1036,7 +1087,7 @@ int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, c
 
 int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint32_t pb0, uint32_t n_pairs,
                       const uint32_t *out_a, const uint32_t *out_b, uint32_t n_out, veq_vc_out *out) {
-  if (!ctx || ba >= ctx->batches.size() || bb >= ctx->batches.size()) return VEQ_E_ARG;
+  if (!ctx || !live_batch(ctx, ba) || !live_batch(ctx, bb)) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   BatchDev *A = ctx->batches[ba], *Bd = ctx->batches[bb];
   if (!A->ran || !Bd->ran) return fail(ctx, VEQ_E_ARG, "compare before run");
@@ -1125,15 +1176,15 @@ int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_
   if (NK) CK(cudaMemcpyAsync(kids.data(), ctx->kids, NK * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   // iterative post-order DFS, dense renumbering
-  std::vector<uint32_t> remap;
-  std::map<uint32_t, uint32_t> idx;
+  // dense renumbering through a flat table (no per-node map lookups)
+  std::vector<uint32_t> idx(NN, UNSET);
   std::vector<uint32_t> order;
   for (size_t r = 0; r < n_roots; r++) {
     if (roots[r] >= NN) return fail(ctx, VEQ_E_ARG, "root id out of range");
     std::vector<std::pair<uint32_t, uint32_t>> st{{roots[r], 0}};
     while (!st.empty()) {
       auto &[x, k] = st.back();
-      if (idx.count(x)) {
+      if (idx[x] != UNSET) {
         st.pop_back();
         continue;
       }
@@ -1142,7 +1193,8 @@ int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_
       if (comp && k < n.nkids) {
         uint32_t kid = kids[n.p0 + k];
         k++;
-        if (!idx.count(kid)) st.push_back({kid, 0});
+        if (kid >= NN) return fail(ctx, VEQ_E_INVALID_IR, "kid id out of range");
+        if (idx[kid] == UNSET) st.push_back({kid, 0});
         continue;
       }
       idx[x] = (uint32_t)order.size();
@@ -1191,8 +1243,232 @@ int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_
   return VEQ_OK;
 }
 
+}  // extern "C"
+
+// ---- to_string of device terms (proj/src/expr.cpp:735-822) ----------------
+namespace {
+
+// Host copy of the term table (nodes and kid arena as created so far).
+int copy_table(veq_ctx *ctx, std::vector<Node> &nodes, std::vector<uint32_t> &kids) {
+  cudaStream_t s = ctx->stream;
+  unsigned long long nn[2];
+  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t NN = std::min<uint64_t>(nn[0], ctx->lim.max_nodes), NK = std::min<uint64_t>(nn[1], ctx->lim.max_kid_words);
+  nodes.resize(NN);
+  kids.resize(NK);
+  if (NN) CK(cudaMemcpyAsync(nodes.data(), ctx->nodes, NN * sizeof(Node), cudaMemcpyDeviceToHost, s));
+  if (NK) CK(cudaMemcpyAsync(kids.data(), ctx->kids, NK * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return VEQ_OK;
+}
+
+// Byte sinks: a string, or CRC-32 (IEEE, zlib.crc32) + length.
+struct StrSink {
+  std::string *out;
+  void put(const char *p, size_t n) { out->append(p, n); }
+};
+struct CrcSink {
+  uint32_t c = 0xFFFFFFFFu;
+  uint64_t n = 0;
+  static const uint32_t *table() {
+    static uint32_t t[256];
+    static bool init = false;
+    if (!init) {
+      for (uint32_t i = 0; i < 256; i++) {
+        uint32_t x = i;
+        for (int k = 0; k < 8; k++) x = (x & 1) ? 0xEDB88320u ^ (x >> 1) : x >> 1;
+        t[i] = x;
+      }
+      init = true;
+    }
+    return t;
+  }
+  void put(const char *p, size_t len) {
+    const uint32_t *t = table();
+    for (size_t i = 0; i < len; i++) c = t[(c ^ (unsigned char)p[i]) & 0xff] ^ (c >> 8);
+    n += len;
+  }
+};
+
+// CRC-32 of a concatenation from the parts' CRCs and lengths (GF(2)
+// polynomial arithmetic modulo the reflected IEEE polynomial, the method of
+// zlib's crc32_combine): memoised per node, a DAG's text digest costs one
+// combine per edge instead of one table step per byte of its (possibly
+// exponentially larger) text.
+struct CrcCat {
+  static uint32_t mulmod(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+      if (a & m) {
+        p ^= b;
+        if ((a & (m - 1)) == 0) break;
+      }
+      m >>= 1;
+      b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+  }
+  uint32_t x2n[64];
+  CrcCat() {
+    uint32_t p = 1u << 30;  // x^1
+    x2n[0] = p;
+    for (int k = 1; k < 64; k++) x2n[k] = p = mulmod(p, p);
+  }
+  uint32_t xpow8(uint64_t n) const {  // x^(8n) mod P
+    uint32_t p = 1u << 31;
+    for (int k = 3; n; n >>= 1, k++)
+      if (n & 1) p = mulmod(x2n[k & 63], p);
+    return p;
+  }
+  struct D {
+    uint32_t crc;
+    uint64_t len;
+  };
+  D cat(D a, D b) const { return b.len == 0 ? a : D{mulmod(xpow8(b.len), a.crc) ^ b.crc, a.len + b.len}; }
+  static D of(const char *s, size_t n) {
+    CrcSink k;
+    k.put(s, n);
+    return D{k.c ^ 0xFFFFFFFFu, k.n};
+  }
+};
+
+struct Printer {
+  const std::vector<Node> &N;
+  const std::vector<uint32_t> &K;
+  const std::vector<std::string> &inputs;
+  static int prec(uint8_t k) { return k == K_ADD ? 1 : (k == K_MUL || k == K_DIV) ? 2 : k == K_NEG ? 3 : 4; }
+  template <class S> void lit(S &o, const char *s) { o.put(s, strlen(s)); }
+  template <class S> void print(uint32_t id, int ctx, S &o) {
+    const Node &n = N[id];
+    const bool paren = prec(n.kind) < ctx;
+    if (paren) o.put("(", 1);
+    char buf[64];
+    switch (n.kind) {
+    case K_CONST: {
+      const long long num = (long long)n.p0, den = (long long)n.p1;
+      int l = den == 1 ? snprintf(buf, sizeof buf, "%lld", num) : snprintf(buf, sizeof buf, "%lld/%lld", num, den);
+      o.put(buf, l);
+      break;
+    }
+    case K_VAR: {
+      if (n.p0 >= INPUT_KEY) {
+        const std::string &nm = inputs[n.p1 >> 40];
+        o.put(nm.data(), nm.size());
+        int l = snprintf(buf, sizeof buf, "_%llu", (unsigned long long)(n.p1 & ((1ull << 40) - 1)));
+        o.put(buf, l);
+      } else {
+        int l = snprintf(buf, sizeof buf, "!undef<%llx>", (unsigned long long)n.p1);
+        o.put(buf, l);
+      }
+      break;
+    }
+    case K_NEGINF: lit(o, "-inf"); break;
+    case K_ADD:
+    case K_MUL:
+    case K_MAX: {
+      const char *sep = n.kind == K_ADD ? " + " : (n.kind == K_MUL ? "*" : ", ");
+      const int kc = n.kind == K_ADD ? 2 : (n.kind == K_MUL ? 3 : 0);
+      if (n.kind == K_MAX) lit(o, "max(");
+      for (uint32_t i = 0; i < n.nkids; i++) {
+        if (i) lit(o, sep);
+        print(K[n.p0 + i], kc, o);
+      }
+      if (n.kind == K_MAX) lit(o, ")");
+      break;
+    }
+    case K_DIV:
+      print(K[n.p0], 3, o);
+      lit(o, " / ");
+      print(K[n.p0 + 1], 3, o);
+      break;
+    case K_NEG:
+      lit(o, "-");
+      print(K[n.p0], 3, o);
+      break;
+    case K_EXP:
+      lit(o, "exp(");
+      print(K[n.p0], 0, o);
+      lit(o, ")");
+      break;
+    default: break;
+    }
+    if (paren) o.put(")", 1);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int veq_render(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, const char **text, const uint64_t **offs) {
+  if (!ctx || (n_roots && !roots) || !text || !offs) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  std::vector<Node> nodes;
+  std::vector<uint32_t> kids;
+  if (int r = copy_table(ctx, nodes, kids)) return r;
+  Printer P{nodes, kids, ctx->input_names};
+  ctx->render_text.clear();
+  ctx->render_offs.assign(1, 0);
+  StrSink sink{&ctx->render_text};
+  for (size_t i = 0; i < n_roots; i++) {
+    if (roots[i] >= nodes.size()) return fail(ctx, VEQ_E_ARG, "root id out of range");
+    P.print(roots[i], 0, sink);
+    ctx->render_offs.push_back(ctx->render_text.size());
+  }
+  *text = ctx->render_text.data();
+  *offs = ctx->render_offs.data();
+  return VEQ_OK;
+}
+
+int veq_render_digest(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, uint32_t *crc32, uint64_t *len) {
+  if (!ctx || (n_roots && (!roots || !crc32 || !len))) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  std::vector<Node> nodes;
+  std::vector<uint32_t> kids;
+  if (int r = copy_table(ctx, nodes, kids)) return r;
+  Printer P{nodes, kids, ctx->input_names};
+  static const CrcCat C;
+  using D = CrcCat::D;
+  // memo of each node's unparenthesised text digest; atoms are printed
+  std::vector<D> memo(nodes.size(), D{0, ~0ull});
+  const D lp = CrcCat::of("(", 1), rp = CrcCat::of(")", 1);
+  std::function<D(uint32_t, int)> dig = [&](uint32_t id, int c) -> D {
+    const Node &n = nodes[id];
+    D core;
+    if (n.kind == K_CONST || n.kind == K_VAR || n.kind == K_NEGINF) {
+      std::string t;
+      StrSink sk{&t};
+      P.print(id, 0, sk);
+      core = CrcCat::of(t.data(), t.size());
+    } else if (memo[id].len != ~0ull) {
+      core = memo[id];
+    } else {
+      const char *sep = n.kind == K_ADD ? " + " : (n.kind == K_MUL ? "*" : (n.kind == K_MAX ? ", " : " / "));
+      const D ds = CrcCat::of(sep, strlen(sep));
+      const int kc = n.kind == K_ADD ? 2 : (n.kind == K_MAX || n.kind == K_EXP) ? 0 : 3;
+      core = n.kind == K_MAX ? CrcCat::of("max(", 4) : n.kind == K_EXP ? CrcCat::of("exp(", 4)
+                                                     : n.kind == K_NEG ? CrcCat::of("-", 1) : D{0, 0};
+      for (uint32_t k = 0; k < n.nkids; k++) {
+        if (k) core = C.cat(core, ds);
+        core = C.cat(core, dig(kids[n.p0 + k], kc));
+      }
+      if (n.kind == K_MAX || n.kind == K_EXP) core = C.cat(core, rp);
+      memo[id] = core;
+    }
+    return Printer::prec(n.kind) < c ? C.cat(C.cat(lp, core), rp) : core;
+  };
+  for (size_t i = 0; i < n_roots; i++) {
+    if (roots[i] >= nodes.size()) return fail(ctx, VEQ_E_ARG, "root id out of range");
+    const D d = dig(roots[i], 0);
+    crc32[i] = d.crc;
+    len[i] = d.len;
+  }
+  return VEQ_OK;
+}
+
 int veq_fetch_cells(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t array, uint32_t *out_nodes, uint64_t n) {
-  if (!ctx || batch >= ctx->batches.size() || (n && !out_nodes)) return VEQ_E_ARG;
+  if (!ctx || !live_batch(ctx, batch) || (n && !out_nodes)) return VEQ_E_ARG;
   BatchDev *bd = ctx->batches[batch];
   if (!bd->ran || prog >= bd->progs.size() || array >= bd->progs[prog].n_arrays) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
@@ -1208,6 +1484,132 @@ int veq_fetch_cells(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t array,
     CK(cudaStreamSynchronize(ctx->stream));
   }
   return VEQ_OK;
+}
+
+int veq_drop_batch(veq_ctx *ctx, uint32_t batch) {
+  if (!ctx || !live_batch(ctx, batch)) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  if (bd->started) return fail(ctx, VEQ_E_ARG, "veq_drop_batch: run not finished");
+  drop_batch(ctx, bd);
+  ctx->batches[batch] = nullptr;
+  return VEQ_OK;
+}
+
+int veq_load_template(veq_ctx *ctx, const veq_batch_desc *d, uint32_t *out) {
+  if (!ctx || !d || !out || !d->n_progs) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  TemplateDev *t = new TemplateDev();
+  t->progs.assign(d->progs, d->progs + d->n_progs);
+  t->thread_stmt.assign(d->thread_stmt, d->thread_stmt + d->n_threads_total + 1);
+  t->thread_nregs.assign(d->thread_nregs, d->thread_nregs + d->n_threads_total);
+  t->arrays.assign(d->arrays, d->arrays + d->n_arrays_total);
+  t->consts.assign(d->consts, d->consts + d->n_consts);
+  t->syncsets.assign(d->syncsets, d->syncsets + d->n_syncsets);
+  t->set_words.assign(d->set_words, d->set_words + d->n_set_words);
+  t->n_stmts = d->n_stmts;
+  for (uint32_t p = 0; p < d->n_progs; p++) {
+    const veq_program_meta &m = t->progs[p];
+    // programs must be laid out in order (threads, arrays and statements)
+    const bool ok = m.thread_off + m.n_threads <= d->n_threads_total && m.array_off + m.n_arrays <= d->n_arrays_total &&
+                    (p == 0 ? m.thread_off == 0 && m.array_off == 0
+                            : m.thread_off == t->progs[p - 1].thread_off + t->progs[p - 1].n_threads &&
+                                  m.array_off == t->progs[p - 1].array_off + t->progs[p - 1].n_arrays);
+    if (!ok) {
+      delete t;
+      return fail(ctx, VEQ_E_INVALID_IR, "template programs are not laid out in order");
+    }
+  }
+  if (cudaMallocAsync(&t->stmts, std::max<uint64_t>(d->n_stmts, 1) * sizeof(veq_stmt), ctx->stream) != cudaSuccess) {
+    delete t;
+    return fail(ctx, VEQ_E_OOM, "template statements");
+  }
+  if (d->n_stmts)
+    CK(cudaMemcpyAsync(t->stmts, d->stmts, d->n_stmts * sizeof(veq_stmt), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->templates.push_back(t);
+  *out = (uint32_t)(ctx->templates.size() - 1);
+  return VEQ_OK;
+}
+
+int veq_drop_template(veq_ctx *ctx, uint32_t tmpl) {
+  if (!ctx || tmpl >= ctx->templates.size() || !ctx->templates[tmpl]) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  cudaFreeAsync(ctx->templates[tmpl]->stmts, ctx->stream);
+  delete ctx->templates[tmpl];
+  ctx->templates[tmpl] = nullptr;
+  return VEQ_OK;
+}
+
+int veq_instantiate(veq_ctx *ctx, uint32_t tmpl, uint32_t n_inst, const int32_t *deltas, uint32_t *out) {
+  if (!ctx || !out || !n_inst || tmpl >= ctx->templates.size() || !ctx->templates[tmpl]) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  const TemplateDev &t = *ctx->templates[tmpl];
+  const uint32_t Q = (uint32_t)t.progs.size(), NA = (uint32_t)t.arrays.size();
+  // program-major expansion: program q * n_inst + i is template program q of
+  // instance i, so each template program's instances form one range
+  std::vector<veq_program_meta> progs;
+  std::vector<uint64_t> thread_stmt{0};
+  std::vector<uint32_t> thread_nregs;
+  std::vector<veq_array> arrays;
+  std::vector<ExpandSeg> segs;
+  uint64_t so = 0;
+  for (uint32_t q = 0; q < Q; q++) {
+    const veq_program_meta &m = t.progs[q];
+    const uint64_t s0 = t.thread_stmt[m.thread_off], s1 = t.thread_stmt[m.thread_off + m.n_threads];
+    segs.push_back(ExpandSeg{so, s0, s1 - s0, m.array_off});
+    for (uint32_t i = 0; i < n_inst; i++) {
+      veq_program_meta pm = m;
+      pm.thread_off = (uint32_t)thread_nregs.size();
+      pm.array_off = (uint32_t)arrays.size();
+      progs.push_back(pm);
+      for (uint32_t k = 0; k < m.n_threads; k++) {
+        const uint32_t g = m.thread_off + k;
+        thread_nregs.push_back(t.thread_nregs[g]);
+        thread_stmt.push_back(thread_stmt.back() + (t.thread_stmt[g + 1] - t.thread_stmt[g]));
+      }
+      for (uint32_t a = 0; a < m.n_arrays; a++) arrays.push_back(t.arrays[m.array_off + a]);
+    }
+    so += (s1 - s0) * n_inst;
+  }
+  const uint64_t S = so;
+  if (S >= (1ull << 31)) return fail(ctx, VEQ_E_UNSUPPORTED, "instantiated batch has more than 2^31 statements");
+  veq_stmt *ds = nullptr;
+  int32_t *dd = nullptr;
+  ExpandSeg *dseg = nullptr;
+  cudaStream_t s = ctx->stream;
+  if (cudaMallocAsync(&ds, std::max<uint64_t>(S, 1) * sizeof(veq_stmt), s) != cudaSuccess)
+    return fail(ctx, VEQ_E_OOM, "instantiated statements");
+  if (cudaMallocAsync(&dd, std::max<uint64_t>((uint64_t)n_inst * NA, 1) * 4, s) != cudaSuccess ||
+      cudaMallocAsync(&dseg, Q * sizeof(ExpandSeg), s) != cudaSuccess) {
+    cudaFreeAsync(ds, s);
+    return fail(ctx, VEQ_E_OOM, "instance deltas");
+  }
+  if (NA) CK(cudaMemcpyAsync(dd, deltas, (uint64_t)n_inst * NA * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dseg, segs.data(), Q * sizeof(ExpandSeg), cudaMemcpyHostToDevice, s));
+  if (S) {
+    ctx->launches++;
+    k_expand_stmts<<<blocks(S, 256), 256, 0, s>>>(t.stmts, dseg, Q, n_inst, dd, NA, ds, S);
+  }
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(dd, s));
+  CK(cudaFreeAsync(dseg, s));
+  veq_batch_desc bd{};
+  bd.n_progs = (uint32_t)progs.size();
+  bd.n_threads_total = (uint32_t)thread_nregs.size();
+  bd.n_stmts = S;
+  bd.n_arrays_total = (uint32_t)arrays.size();
+  bd.n_consts = (uint32_t)t.consts.size();
+  bd.n_syncsets = (uint32_t)t.syncsets.size();
+  bd.n_set_words = (uint32_t)t.set_words.size();
+  bd.progs = progs.data();
+  bd.thread_stmt = thread_stmt.data();
+  bd.thread_nregs = thread_nregs.data();
+  bd.stmts = nullptr;
+  bd.arrays = arrays.data();
+  bd.consts = t.consts.data();
+  bd.syncsets = t.syncsets.data();
+  bd.set_words = t.set_words.data();
+  return load_impl(ctx, &bd, ds, out);
 }
 
 int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]) {

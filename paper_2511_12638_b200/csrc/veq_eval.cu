@@ -1,0 +1,22 @@
+// veq_eval.cu — K2 evaluator translation unit: k_eval_warp and its launcher
+// (see veq_kernels.cuh). Split from veq_api.cu so the two compile in
+// parallel.
+#define VEQ_TU_EVAL
+#include "veq_kernels.cuh"
+
+namespace veqd {
+
+void eval_warp_config(int smem, int *per_sm) {
+  cudaFuncSetAttribute(k_eval_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  *per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_eval_warp, EVAL_BLOCK, smem);
+}
+
+void launch_eval_warp(uint32_t grid, uint32_t block, int smem, cudaStream_t s, const Batch &B, const Table &T,
+                      const EvalCtx &E, const uint4 *desc, const unsigned long long *n_work_dev,
+                      unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
+                      uint64_t chunk) {
+  k_eval_warp<<<grid, block, smem, s>>>(B, T, E, desc, n_work_dev, cursor, pool, pool_used, pool_cap, chunk);
+}
+
+}  // namespace veqd

@@ -186,13 +186,17 @@ __device__ __forceinline__ uint32_t thread_of_stmt(const uint64_t *thread_stmt, 
   return lo;
 }
 
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_thread_prog(PrepArgs A, uint32_t *thread_prog) {
   const uint32_t p = blockIdx.x;
   const veq_program_meta m = A.progs[p];
   for (uint32_t t = threadIdx.x; t < m.n_threads; t += blockDim.x) thread_prog[m.thread_off + t] = p;
 }
+#endif
+
 
 // per statement: validation and the (sync, access) counts to scan
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_stmts(PrepArgs A) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool arith = i < A.n_stmts && (A.stmts[i].kind == VEQ_ST_BINOP || A.stmts[i].kind == VEQ_ST_UNOP);
@@ -224,9 +228,12 @@ __global__ void k_prep_stmts(PrepArgs A) {
   }
   A.cnt[i] = c;
 }
+#endif
+
 
 // per thread: segment offsets, first segment start, last segment's set
 // (cnt has n_stmts + 1 entries after the scan: cnt[n_stmts] is the total)
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_threads(PrepArgs A, uint64_t *seg_off, uint64_t *seg_start, uint32_t *seg_set) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > A.n_threads) return;
@@ -238,8 +245,11 @@ __global__ void k_prep_threads(PrepArgs A, uint64_t *seg_off, uint64_t *seg_star
   const uint64_t nsync = syncs_before(A.thread_stmt[t + 1]) - syncs_before(A.thread_stmt[t]);
   seg_set[so + nsync] = UNSET;  // the last segment ends the thread, not at a sync
 }
+#endif
+
 
 // per Sync statement: canonical set id of the segment it ends, next start
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_syncs(PrepArgs A, uint64_t *seg_start, uint32_t *seg_set) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n_stmts) return;
@@ -262,9 +272,12 @@ __global__ void k_prep_syncs(PrepArgs A, uint64_t *seg_start, uint32_t *seg_set)
     if (!member || !chunk) atomicOr(A.sched_flags, 1u);
   }
 }
+#endif
+
 
 // per sync set: the aligned 32-thread chunk holding its window and the
 // member mask inside it (k_schedule_warp decides releases from it)
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_set_chunks(const veq_syncset *sets, const uint64_t *set_words, uint32_t n,
                                   unsigned long long *set_chunk) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -277,8 +290,11 @@ __global__ void k_prep_set_chunks(const veq_syncset *sets, const uint64_t *set_w
   }
   set_chunk[i] = v;
 }
+#endif
+
 
 // per program: sync count (release capacity) for the rel_off scan
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_progs(PrepArgs A, uint64_t *prog_sync, uint32_t *prog_full) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.n_progs) return;
@@ -287,8 +303,11 @@ __global__ void k_prep_progs(PrepArgs A, uint64_t *prog_sync, uint32_t *prog_ful
   prog_sync[p] = syncs_before(A.thread_stmt[m.thread_off + m.n_threads]) - syncs_before(A.thread_stmt[m.thread_off]);
   prog_full[p] = A.n_syncsets;
 }
+#endif
+
 
 // threads with >= EXEC_WARP_MIN statements (they run on k_exec_warp)
+#ifndef VEQ_TU_EVAL
 __global__ void k_prep_long(PrepArgs A, uint32_t *longs, unsigned long long *n_long, uint64_t min_len) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= A.n_threads) return;
@@ -299,6 +318,36 @@ __global__ void k_prep_long(PrepArgs A, uint32_t *longs, unsigned long long *n_l
     longs[g.shfl(base, 0) + g.thread_rank()] = t;
   }
 }
+#endif
+
+
+// Template expansion (veq_instantiate): output statement o of template
+// program q's instance i is template statement src0 + j with Load/Store
+// offsets shifted by that instance's delta for the statement's array. One
+// 16-byte read and write per statement (HBM-bound copy).
+struct ExpandSeg {
+  uint64_t out0;   // first output statement of this template program's instances
+  uint64_t src0;   // first template statement of the program
+  uint64_t len;    // statements per instance
+  uint32_t array_off, pad;
+};
+#ifndef VEQ_TU_EVAL
+__global__ void k_expand_stmts(const veq_stmt *__restrict__ tmpl, const ExpandSeg *__restrict__ segs, uint32_t n_segs,
+                               uint32_t n_inst, const int32_t *__restrict__ deltas, uint32_t n_arrays,
+                               veq_stmt *__restrict__ out, uint64_t n_out) {
+  const uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n_out) return;
+  uint32_t q = 0;
+  while (q + 1 < n_segs && segs[q + 1].out0 <= o) q++;
+  const ExpandSeg sg = segs[q];
+  const uint64_t r = o - sg.out0, i = r / sg.len, j = r - i * sg.len;
+  veq_stmt st = tmpl[sg.src0 + j];
+  if (st.kind == VEQ_ST_LOAD || st.kind == VEQ_ST_STORE)
+    st.a = (uint32_t)((int32_t)st.a + __ldg(deltas + i * n_arrays + sg.array_off + st.arr));
+  out[o] = st;
+}
+#endif
+
 
 // ---------------------------------------------------------------------------
 // K0: schedule. One block per program, symbolic threads in contiguous chunks
@@ -327,6 +376,7 @@ __device__ inline uint32_t set_min(const Batch &B, uint32_t s) {
 // round costs a handful of block barriers and on-chip accesses.
 constexpr uint32_t SCHED_SMEM_T = 8192;
 
+#ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
   extern __shared__ uint8_t sched_smem[];
   const uint32_t p = blockIdx.x;
@@ -513,6 +563,8 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
     B.prog_dead[p] = s_ret != T;
   }
 }
+#endif
+
 
 // K0 for CTAs of at most 1024 threads: one CUDA thread per symbolic thread,
 // control state in registers. A round is one block scan of the runnable
@@ -523,6 +575,7 @@ __global__ void __launch_bounds__(SCHED_BLOCK) k_schedule_smem(Batch B) {
 // symexec.cpp:616-654). The full set uses block counts; any other set is
 // checked member by member from shared memory.
 constexpr uint32_t TS_NONE = 3;  // lane beyond the CTA's thread count
+#ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(1024, 2) k_schedule_lanes(Batch B) {
   __shared__ uint8_t s_st[1024];
   __shared__ uint32_t s_bs[1024];
@@ -690,6 +743,8 @@ __global__ void __launch_bounds__(1024, 2) k_schedule_lanes(Batch B) {
     B.prog_dead[p] = ret_count != T;
   }
 }
+#endif
+
 
 // K0, one warp per CTA program (CTAs of at most 1024 threads whose sync
 // sets are all the full set or windows inside one aligned 32-thread chunk).
@@ -707,6 +762,7 @@ struct SchedWarpSmem {
   uint8_t st[1024];
   unsigned long long cand[32];
 };
+#ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
   extern __shared__ __align__(16) char swsm[];
   SchedWarpSmem &S = reinterpret_cast<SchedWarpSmem *>(swsm)[threadIdx.x >> 5];
@@ -897,6 +953,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_schedule_warp(Batch B) {
     B.prog_dead[p] = ret != T;
   }
 }
+#endif
+
 
 // ---------------------------------------------------------------------------
 // K3: per-thread symbolic execution over value refs.
@@ -905,6 +963,7 @@ __device__ __forceinline__ bool is_stmt_ref(uint32_t r) { return r < REF_NODE; }
 // Threads with at least EXEC_WARP_MIN statements run on k_exec_warp.
 constexpr uint64_t EXEC_WARP_MIN = 64;
 
+#ifndef VEQ_TU_EVAL
 __global__ void k_exec(Batch B, Table T) {
   uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= B.n_threads) return;
@@ -1054,6 +1113,8 @@ __global__ void k_exec(Batch B, Table T) {
     }
   }
 }
+#endif
+
 
 // ---------------------------------------------------------------------------
 // K3, warp-parallel: one warp per symbolic thread, 32 consecutive statements
@@ -1068,6 +1129,7 @@ __device__ __forceinline__ bool defines_reg(uint8_t kind) {
          kind == VEQ_ST_LOAD;
 }
 
+#ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1307,6 +1369,8 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
     }
   }
 }
+#endif
+
 
 // ---------------------------------------------------------------------------
 // K4 helpers: "thread i is still pending in the event (owner j, step se) at
@@ -1338,6 +1402,7 @@ struct Reader {
 };
 
 // One thread per address segment [s, e) of the (cell, step)-sorted tuples.
+#ifndef VEQ_TU_EVAL
 __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, const unsigned long long *vals,
                            const uint32_t *seg_starts, const unsigned long long *n_segs_dev, uint64_t n_tup,
                            Reader *rscratch) {
@@ -1468,7 +1533,10 @@ __global__ void k_mem_scan(Batch B, Table T, const unsigned long long *keys, con
   }
   B.final_val[cell] = has ? value : UNSET;
 }
+#endif
 
+
+#ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(APP_NT) k_seg_heads(const unsigned long long *keys, uint64_t n, uint32_t *starts,
                                                      unsigned long long *n_starts, uint32_t step_bits) {
   // a head starts every run of equal cells; unfilled slots (key ~0, from
@@ -1486,6 +1554,8 @@ __global__ void __launch_bounds__(APP_NT) k_seg_heads(const unsigned long long *
   for (int k = 0; k < APP_ITEMS; k++)
     if ((mask >> k) & 1u) starts[o++] = (uint32_t)(b0 + (uint64_t)k * APP_NT);
 }
+#endif
+
 
 // Follow load refs to the value they read (a load's ref_a holds the value
 // of the store it observed, which may itself be a loaded value).
@@ -1494,6 +1564,7 @@ __device__ __forceinline__ uint32_t chase(const Batch &B, uint32_t r) {
   return r;
 }
 
+#ifndef VEQ_TU_EVAL
 __global__ void k_resolve_finals(Batch B) {
   uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= B.n_cells) return;
@@ -1503,10 +1574,13 @@ __global__ void k_resolve_finals(Batch B) {
   B.final_val[c] = v;
   if (is_stmt_ref(v)) atomicAdd(B.uses + v, 1u);
 }
+#endif
+
 
 // Input symbols read by direct loads (never-stored input arrays) are
 // interned in one parallel pass before execution; the executors read the
 // node from canon[i].
+#ifndef VEQ_TU_EVAL
 __global__ void k_pre_inputs(Batch B, Table T) {
   __shared__ uint32_t s_p0;
   const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x;
@@ -1523,6 +1597,8 @@ __global__ void k_pre_inputs(Batch B, Table T) {
   if (!(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 && (uint32_t)off < arr.seeded)
     B.canon[i] = intern_input_var(T, (uint32_t)arr.input, (uint64_t)off);
 }
+#endif
+
 
 __device__ __forceinline__ bool is_chain_op(const veq_stmt &st) {
   return st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX);
@@ -1530,6 +1606,7 @@ __device__ __forceinline__ bool is_chain_op(const veq_stmt &st) {
 
 // One pass after the memory scan: operands resolved through loads, use
 // counts, and the chain-log size of every chain head.
+#ifndef VEQ_TU_EVAL
 __global__ void k_resolve_all(Batch B, uint32_t *sz) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B.n_stmts) return;
@@ -1553,9 +1630,12 @@ __global__ void k_resolve_all(Batch B, uint32_t *sz) {
   }
   sz[i] = v;
 }
+#endif
+
 
 // One pass after the log scan: chain-log entries and the work list (every
 // executed BinOp/UnOp except chain links absorbed by their successor).
+#ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t *base, uint32_t *log,
                                                         uint32_t *log_stmt, unsigned long long *wkey, uint32_t *wval,
                                                         unsigned long long *n_work) {
@@ -1598,6 +1678,8 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
     o++;
   }
 }
+#endif
+
 
 // ---------------------------------------------------------------------------
 // K2: persistent evaluation in (program, step) order.
@@ -1616,6 +1698,12 @@ __device__ __forceinline__ uint32_t wait_node(const Batch &B, uint32_t r) {
 struct EvalCtx {
   const uint32_t *log, *log_stmt, *log_base;
   unsigned long long *prof;  // optional eval profile (VEQ_PROF=1), see veq_api.cu
+  // path switches (VEQ_EVAL_OFF / VEQ_EVAL_PAIR, diagnostics): 1 no pairing,
+  // 2 no smem path, 4 no lean path. Pairing (two <= 16-leaf sums per warp,
+  // lean_pair16) is off unless VEQ_EVAL_PAIR=1: on short work lists its two
+  // half-warps were observed to split permanently (a lane-16 half running the
+  // full-warp paths alone), see profiles/r02_pairing.md.
+  uint32_t off;
 };
 
 __device__ inline void arith_fault(const Batch &B, uint32_t stmt, uint8_t detail) {
@@ -1730,6 +1818,7 @@ __device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, c
 // Work descriptor per sorted item: statement, chain-log base and leaf count
 // (chain Adds), statement kind and op — one 16-byte load replaces the
 // stmts -> chain_head/pos -> log_base chain of dependent reads.
+#ifndef VEQ_TU_EVAL
 __global__ void k_make_desc(Batch B, EvalCtx E, const uint32_t *work, const unsigned long long *n_work_dev,
                             uint4 *desc) {
   uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1743,6 +1832,8 @@ __global__ void k_make_desc(Batch B, EvalCtx E, const uint32_t *work, const unsi
   }
   desc[w] = d;
 }
+#endif
+
 
 __device__ __forceinline__ bool desc_is_add(const uint4 &d) {
   return (d.w & 0xff) == VEQ_ST_BINOP && ((d.w >> 8) & 0xff) == VEQ_BIN_ADD;
@@ -1757,6 +1848,15 @@ __device__ __forceinline__ bool desc_is_add(const uint4 &d) {
 // 64 registers/thread: 32 resident warps per SM in one block sharing one
 // 216 KB page pool.
 constexpr uint32_t EVAL_BLOCK = 1024, EVAL_PAGES = 54;
+// k_eval_warp is compiled in its own translation unit (veq_eval.cu) and
+// launched through launch_eval_warp (parallel builds; the rest of the
+// pipeline does not recompile when only the evaluator changes).
+void eval_warp_config(int smem, int *per_sm);
+void launch_eval_warp(uint32_t grid, uint32_t block, int smem, cudaStream_t s, const Batch &B, const Table &T,
+                      const EvalCtx &E, const uint4 *desc, const unsigned long long *n_work_dev,
+                      unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
+                      uint64_t chunk);
+#ifdef VEQ_TU_EVAL
 __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
                                                              const unsigned long long *n_work_dev,
                                                              unsigned long long *cursor, char *pool,
@@ -1822,7 +1922,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
     fetch(wn, dn, lgn);
     // two consecutive small chains with no dependency between them run on
     // the two halves of the warp (lean_pair16)
-    bool paired = wn < n_work && desc_is_add(d) && d.z <= 16 && desc_is_add(dn) && dn.z <= 16;
+    bool paired = !(E.off & 1) && wn < n_work && desc_is_add(d) && d.z <= 16 && desc_is_add(dn) && dn.z <= 16;
     if (paired) paired = !__any_sync(kFull, lane < dn.z && lgn == d.x);
     uint32_t rA = UNSET, rB = UNSET;
     if (paired) {
@@ -1847,6 +1947,8 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
         atomicAdd(E.prof + 32 + tbucket(), (unsigned long long)((rA != UNSET) + (rB != UNSET)));
       }
     }
+    // the lanes that published a pair result rejoin the warp here
+    __syncwarp();
     // items left for the full warp: the current one when unpaired, else the
     // halves the pair path did not cover (in list order)
     const bool needA = !paired || rA == UNSET, needB = paired && rB == UNSET;
@@ -1875,7 +1977,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
         if (E.prof) t1 = clock64();
         if (!neg) {
           bool counted = false;
-          if (n <= 32) {
+          if (n <= 32 && !(E.off & 4)) {
             r = warp_add_lean(T, leaf0, n, m, &W, &created, E.prof ? prof_lean : nullptr);
             counted = true;
             path = 1;
@@ -1894,7 +1996,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
           cleaf = __any_sync(kFull, cleaf);
           const uint32_t pages = (uint32_t)((add_smem_bytes(n, m, cleaf) + SPAGE - 1) / SPAGE);
             const long long pa0 = E.prof ? clock64() : 0;
-            const int first = pool_acquire(SP, pages);
+            const int first = (E.off & 2) ? -1 : pool_acquire(SP, pages);
             if (E.prof && lane == 0) {
               prof_pool += clock64() - pa0;
               prof_pages += pages;
@@ -1915,6 +2017,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
         }
         if (r == UNSET) {
           path = 4;
+          __syncwarp();
           uint32_t *ids = warp_get<uint32_t>(A, n);
           r = T.id_zero;
           if (ids) {
@@ -1992,19 +2095,28 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
   }
 }
 
+#endif  // VEQ_TU_EVAL
+
+#ifndef VEQ_TU_EVAL
 __global__ void k_final_nodes(Batch B) {
   uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= B.n_cells) return;
   uint32_t v = B.final_val[c];
   B.final_node[c] = (v == UNSET) ? UNSET : wait_node(B, v);
 }
+#endif
 
+
+#ifndef VEQ_TU_EVAL
 __global__ void k_intern_consts(Table T, const veq_rat *consts, uint32_t n, uint32_t *out) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   out[i] = intern_const(T, Rat{consts[i].num, consts[i].den});
 }
+#endif
 
+
+#ifndef VEQ_TU_EVAL
 __global__ void k_session_init(Table T, uint32_t *ids) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   ids[0] = intern(T, K_NEGINF, 0, 0, nullptr, 0);
@@ -2012,6 +2124,8 @@ __global__ void k_session_init(Table T, uint32_t *ids) {
   ids[2] = intern(T, K_CONST, 1, 1, nullptr, 0);
   ids[3] = intern(T, K_CONST, (uint64_t)-1ll, 1, nullptr, 0);
 }
+#endif
+
 
 // ---------------------------------------------------------------------------
 // K5: compare. One thread per VC: id equality, then side conditions by an
@@ -2074,6 +2188,7 @@ __device__ inline void collect_sc(const Table &T, uint32_t root, uint32_t *seen_
   }
 }
 
+#ifndef VEQ_TU_EVAL
 __global__ void k_compare(Table T, const uint32_t *final_node_a, const uint32_t *final_node_b, CmpArgs C,
                           char *pool, unsigned long long *pool_used, uint64_t pool_cap, uint64_t chunk) {
   uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2115,5 +2230,7 @@ __global__ void k_compare(Table T, const uint32_t *final_node_a, const uint32_t 
   }
   C.vcs[v] = out;
 }
+#endif
+
 
 }  // namespace veqd

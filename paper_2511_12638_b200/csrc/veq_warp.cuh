@@ -658,11 +658,12 @@ __device__ __forceinline__ uint64_t half_sum(uint64_t v) {
   for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o, 16);
   return v;
 }
-__device__ inline uint32_t lean_pair16(const Table &T, uint32_t leaf, uint32_t n, bool skip, WarpAlloc &W,
-                                      bool &created, unsigned long long *dbg = nullptr) {
+static __device__ __noinline__ uint32_t lean_pair16(const Table &T, uint32_t leaf, uint32_t n, bool skip, WarpAlloc &W,
+                                            bool &created, unsigned long long *dbg = nullptr) {
   const uint32_t lane = lane_id(), sl = lane & 15, sb = lane & 16;
   const uint32_t hmask = 0xffffu << sb;
   created = false;
+  __syncwarp();  // both halves enter together (their leaf waits may diverge)
   // leaves and term counts
   uint32_t c = 0, kind = 0;
   uint64_t p0 = 0;
@@ -747,16 +748,21 @@ __device__ inline uint32_t lean_pair16(const Table &T, uint32_t leaf, uint32_t n
   const uint32_t pdm = __ballot_sync(kFull, in && (kf & F_POSDEF)) & hmask;
   const uint32_t dvm = __ballot_sync(kFull, in && (kf & F_HASDIV)) & hmask;
   const uint32_t inm = __ballot_sync(kFull, in) & hmask;
-  const uint64_t k0p = __shfl_sync(kFull, key, 0, 16);
+  // the node record is written by each half's lane 0, whose own sorted key
+  // is the first kid's prefix (no shuffle: a shuffle whose result is used
+  // only under `act` may be sunk into that branch, where the halves diverge)
   const uint64_t h = composite_hash(K_ADD, real, sum);
   const uint8_t flags = composite_flags(K_ADD, pdm != 0, pdm == inm, dvm != 0, false);
-  const uint64_t p1 = composite_prefix(K_ADD, real, k0p);
+  const uint64_t p1 = composite_prefix(K_ADD, real, key);
   unsigned long long nid = 0, off = 0;
   bool ok = true;
   if (act && sl == 0) ok = wa_alloc(T, W, real, (uint64_t &)nid, (uint64_t &)off);
   nid = __shfl_sync(kFull, nid, 0, 16);
   off = __shfl_sync(kFull, off, 0, 16);
   ok = __shfl_sync(kFull, ok, 0, 16);
+  // keep the shuffles where every lane executes them (their results are used
+  // under per-half conditions below)
+  asm volatile("" : "+l"(nid), "+l"(off));
   if (act && ok) {
     if (sl < real) T.kids[off + sl] = id;
     if (sl == 0) {

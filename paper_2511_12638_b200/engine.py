@@ -99,7 +99,8 @@ class Session:
             raise N.VeqError(st, L.veq_strerror(st).decode())
         self.ctx = h
         self.inputs: List[Tuple[str, int]] = []
-        self._batches: List[Batch] = []
+        self._batches: List[Optional[Batch]] = []
+        self._templates: List[Batch] = []
 
     def close(self):
         if self.ctx:
@@ -124,12 +125,42 @@ class Session:
         _check(self.ctx, N.lib().veq_declare_inputs(self.ctx, arr, len(inputs)))
         self.inputs = list(inputs)
         self._batches = []
+        self._templates = []
 
     def load(self, batch: Batch) -> int:
         d = batch.desc()
         h = C.c_uint32()
         _check(self.ctx, N.lib().veq_load_batch(self.ctx, C.byref(d), C.byref(h)))
-        self._batches.append(batch)
+        while len(self._batches) <= h.value:
+            self._batches.append(None)
+        self._batches[h.value] = batch
+        return h.value
+
+    def drop(self, bid: int):
+        """Free a batch's device memory now (veq_drop_batch)."""
+        _check(self.ctx, N.lib().veq_drop_batch(self.ctx, bid))
+        self._batches[bid] = None
+
+    def load_template(self, template: Batch) -> int:
+        """Grid template to the device once (veq_load_template)."""
+        d = template.desc()
+        h = C.c_uint32()
+        _check(self.ctx, N.lib().veq_load_template(self.ctx, C.byref(d), C.byref(h)))
+        self._templates.append(template)
+        return h.value
+
+    def instantiate(self, tid: int, deltas: np.ndarray, meta: Optional[Batch] = None) -> int:
+        """n_inst = deltas.shape[0] instances of template `tid` as one batch
+        (veq_instantiate); deltas[i] holds instance i's shift of every
+        template array. `meta` (optional) is a host Batch whose names and
+        locations reports should use for the result."""
+        dl = np.ascontiguousarray(deltas, dtype=np.int32)
+        h = C.c_uint32()
+        _check(self.ctx, N.lib().veq_instantiate(self.ctx, tid, dl.shape[0], dl.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                 C.byref(h)))
+        while len(self._batches) <= h.value:
+            self._batches.append(None)
+        self._batches[h.value] = meta
         return h.value
 
     def run_raw(self, bid: int) -> N.veq_run_out:
@@ -177,6 +208,32 @@ class Session:
 
     # -- DAG export and rendering
     def to_strings(self, roots: Sequence[int]) -> List[str]:
+        """to_string of each root (veq_render: C++ over the device DAG)."""
+        if not roots:
+            return []
+        r = (C.c_uint32 * len(roots))(*roots)
+        text = C.c_char_p()
+        offs = C.POINTER(C.c_uint64)()
+        _check(self.ctx, N.lib().veq_render(self.ctx, r, len(roots), C.byref(text), C.byref(offs)))
+        n = len(roots)
+        o = np.ctypeslib.as_array(offs, shape=(n + 1,)).copy()
+        raw = C.string_at(text, int(o[n]))
+        return [raw[int(o[i]):int(o[i + 1])].decode() for i in range(n)]
+
+    def digests(self, roots: Sequence[int]) -> List[Tuple[int, int]]:
+        """(CRC-32, byte length) of each root's to_string (veq_render_digest)."""
+        n = len(roots)
+        if not n:
+            return []
+        r = (C.c_uint32 * n)(*roots)
+        crc = np.zeros(n, np.uint32)
+        ln = np.zeros(n, np.uint64)
+        _check(self.ctx, N.lib().veq_render_digest(self.ctx, r, n, crc.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                   ln.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return [(int(a), int(b)) for a, b in zip(crc, ln)]
+
+    def to_strings_py(self, roots: Sequence[int]) -> List[str]:
+        """Reference Python rendering over veq_export_dag (cross-check of veq_render)."""
         if not roots:
             return []
         L = N.lib()

@@ -181,3 +181,19 @@ def concat(batches: List[Batch]) -> Batch:
     cat = np.concatenate
     return Batch(cat(progs), cat(ts), cat(tn), cat(st), cat(ar), cat(co), cat(ss), cat(sw), pn, an, cat(ro), rn,
                  cat(lo))
+
+
+def instantiate(template: Batch, deltas: np.ndarray) -> Batch:
+    """CTA instance of a one-program template (veqh_elaborate_template):
+    every Load/Store offset on array a shifted by deltas[a]. Host-side
+    mirror of the device expansion in veq_instantiate (tests compare it
+    with per-CTA elaboration)."""
+    assert template.n_progs == 1
+    st = template.stmts.copy()
+    m = (st["kind"] == N.ST_LOAD) | (st["kind"] == N.ST_STORE)
+    d = np.asarray(deltas, dtype=np.int64)[st["arr"][m].astype(np.int64)]
+    st["a"][m] = ((st["a"][m].astype(np.int64).astype(np.int32).astype(np.int64) + d) & 0xFFFFFFFF).astype(np.uint32)
+    b = Batch(template.progs.copy(), template.thread_stmt, template.thread_nregs, st, template.arrays,
+              template.consts, template.syncsets, template.set_words, list(template.prog_names),
+              list(template.array_names), template.thread_reg_off, template.reg_names, template.locs)
+    return b

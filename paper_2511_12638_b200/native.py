@@ -140,6 +140,12 @@ def lib() -> C.CDLL:
     L.veq_stream.argtypes = [vp]
     L.veq_stream.restype = vp
     L.veq_clear_terms.argtypes = [vp]
+    L.veq_drop_batch.argtypes = [vp, u32]
+    L.veq_load_template.argtypes = [vp, P(veq_batch_desc), P(u32)]
+    L.veq_instantiate.argtypes = [vp, u32, u32, P(i32), P(u32)]
+    L.veq_drop_template.argtypes = [vp, u32]
+    L.veq_render.argtypes = [vp, P(u32), C.c_size_t, P(C.c_char_p), P(P(u64))]
+    L.veq_render_digest.argtypes = [vp, P(u32), C.c_size_t, P(u32), P(u64)]
     for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_run_start", "veq_run_finish",
               "veq_fetch_cells", "veq_compare", "veq_compare_progs",
               "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
@@ -150,5 +156,6 @@ def lib() -> C.CDLL:
 
 EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_declare_inputs", "veq_load_batch",
             "veq_run", "veq_run_start", "veq_run_finish", "veq_fetch_cells", "veq_compare", "veq_compare_progs", "veq_export_dag", "veq_verdict_counters",
-            "veq_set_timing", "veq_clear_terms", "veq_stream"]
+            "veq_set_timing", "veq_clear_terms", "veq_stream", "veq_drop_batch", "veq_load_template",
+            "veq_instantiate", "veq_drop_template", "veq_render", "veq_render_digest"]
 PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]

@@ -1,0 +1,136 @@
+"""Parity at the benchmarked sizes (digest goldens, tests/golden/dg_*,
+written by tests/golden/make_digest_golden.py from the reference checker).
+
+CPU: the product frontend's packed-IR elaboration of each full-size CTA pair
+is byte-identical to the reference's (CRC-32 + length of the image).
+
+GPU: the bench's exact path — both kernels' CTAs as ONE merged batch (the
+CTA of the golden inside a small grid of its neighbours), one run with the
+long-thread executor on the side stream, veq_compare_progs — must reproduce
+the reference's report: every VC's verdict, the to_string of every output of
+both kernels (CRC-32 + length, full text for the sampled ones), the
+side-condition union (digests, discharged flags) and the overall verdict."""
+import json
+import os
+import re
+import zlib
+
+import pytest
+
+from conftest import golden_dirs
+from paper_2511_12638_b200 import frontend, ir
+from paper_2511_12638_b200 import native as N
+
+DIRS = golden_dirs("dg_")
+
+
+def _load(d):
+    g = json.load(open(os.path.join(d, "golden.json")))
+    src = lambda f: open(os.path.join(d, f)).read()
+    return g, src("a.mk"), src("b.mk"), src("cfg.cfg")
+
+
+def _dig(s: str):
+    b = s.encode()
+    return {"crc32": "%08x" % zlib.crc32(b), "len": len(b)}
+
+
+@pytest.mark.parametrize("d", DIRS, ids=os.path.basename)
+def test_full_size_elaboration_matches_reference(d):
+    g, ka, kb, cfg = _load(d)
+    a, b, inputs = frontend.elaborate_pair(ka, kb, cfg)
+    assert inputs == [(x["name"], x["size"]) for x in g["inputs"]]
+    assert _dig_bytes(a.image) == g["ir_a"]
+    assert _dig_bytes(b.image) == g["ir_b"]
+
+
+def _dig_bytes(b: bytes):
+    return {"crc32": "%08x" % zlib.crc32(b), "len": len(b)}
+
+
+def _grid_for(cfg: str):
+    """(block param, first block, n blocks, index of the golden's CTA): the
+    golden's CTA plus one neighbour inside the grid (the previous block, or
+    the next one for block 0)."""
+    m = re.search(r"params\.B = (\d+)", cfg)
+    if not m:
+        return None, 0, 1, 0
+    blk = int(m.group(1))
+    return ("B", blk - 1, 2, 1) if blk > 0 else ("B", 0, 2, 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["template", "grid"])
+@pytest.mark.parametrize("d", DIRS, ids=os.path.basename)
+def test_bench_path_matches_reference_at_size(d, path):
+    import numpy as np
+    from paper_2511_12638_b200.engine import Session
+    g, ka, kb, cfg = _load(d)
+    bp, base, nblk, me = _grid_for(cfg)
+    if path == "template" and not bp:
+        pytest.skip("single-CTA configuration")
+    # the neighbour CTA exercises batching only (inputs are sized for the
+    # whole grid by the workload's params)
+    if path == "template":
+        # bench.py's path: one template per kernel expanded on the device
+        a, b, inputs, da, db = frontend.elaborate_template(ka, kb, cfg, bp, nblk, block_base=base, want_names=False)
+    else:
+        a, b, inputs = frontend.elaborate_pair(ka, kb, cfg, bp, nblk, block_base=base, want_names=False) if bp \
+            else frontend.elaborate_pair(ka, kb, cfg, want_names=False)
+    P = nblk if path == "template" else a.n_progs
+    S = (len(a.stmts) + len(b.stmts)) * (nblk if path == "template" else 1)
+    s = Session(0, max_nodes=max(1 << 22, S), max_kid_words=(1 << 24) + 8 * S, scratch_bytes=8 << 30)
+    try:
+        s.declare_inputs(inputs)
+        if path == "template":
+            t = s.load_template(ir.concat([a, b]))
+            h = s.instantiate(t, np.concatenate([da, db], axis=1))
+        else:
+            h = s.load(ir.concat([a, b]))
+        out = s.run_raw(h)
+        assert out.n_faults == 0
+        pm = a.progs[0 if path == "template" else me]  # the template is one program
+        o0 = int(pm["array_off"])
+        outs = sorted((a.array_names[o0 + k], k) for k in range(int(pm["n_arrays"]))
+                      if int(a.arrays[o0 + k]["role"]) == N.ROLE_OUT)
+        ks = [k for _, k in outs]
+        vc = s.compare_progs_raw(h, me, h, P + me, 1, ks, ks)
+        n = int(vc.n_vcs)
+        rep = g["report"]
+        assert n == len(rep["vcs"]) == len(g["env_a"]) == len(g["env_b"])
+        na = [vc.vcs[i].node_a for i in range(n)]
+        nb = [vc.vcs[i].node_b for i in range(n)]
+        eqs = [bool(vc.vcs[i].equal) for i in range(n)]
+        sc = [(vc.sc_node[q], bool(vc.sc_discharged[q])) for q in range(vc.n_sc)]
+        sc_per = [(vc.vcs[i].sc_off, vc.vcs[i].sc_n) for i in range(n)]
+        for i, v in enumerate(rep["vcs"]):
+            assert (v["array"], v["index"]) == (g["env_a"][i]["array"], g["env_a"][i]["index"])
+            assert eqs[i] == (v["verdict"] == "equal"), (i, v)
+        # to_string of every output of both kernels (device DAG -> host text)
+        for side, nodes in (("env_a", na), ("env_b", nb)):
+            digs = s.digests(nodes)
+            for i, ((crc, ln), want) in enumerate(zip(digs, g[side])):
+                assert {"crc32": "%08x" % crc, "len": ln} == want["digest"], (side, i)
+            sampled = [i for i, w in enumerate(g[side]) if "text" in w]
+            for i, t in zip(sampled, s.to_strings([nodes[i] for i in sampled])):
+                assert t == g[side][i]["text"], (side, i)
+        # side-condition union in VC order, de-duplicated by to_string
+        uniq = sorted({x for x, _ in sc})
+        # interned terms: equal to_string <=> equal node id
+        dig = dict(zip(uniq, s.digests(uniq)))
+        seen, got = set(), []
+        for off, cnt in sc_per:
+            for q in range(off, off + cnt):
+                node = sc[q][0]
+                if node not in seen:
+                    seen.add(node)
+                    crc, ln = dig[node]
+                    got.append({"denominator_digest": {"crc32": "%08x" % crc, "len": ln}, "discharged": sc[q][1]})
+        want = [{"denominator_digest": x["denominator_digest"], "discharged": x["discharged"]}
+                for x in rep["side_conditions"]]
+        assert got == want
+        residual = any(not x["discharged"] for x in got)
+        verdict = "equivalent" if all(eqs) and not residual else ("unknown" if all(eqs) else "undecided")
+        assert verdict == rep["verdict"]
+    finally:
+        s.close()
