@@ -130,35 +130,41 @@ def ref_bench(workload, blocks, seconds, threads):
 
 from paper_2511_12638_b200 import workloads  # noqa: E402
 
+# `ref` is the bounded sample the reference checker (CPU) runs in the time
+# bound; `ref_scale` converts its per-element rate to the full configuration
+# (measured on this image's reference build: the per-output cost grows as
+# K^2 for a K-term accumulation, x3.35 / x4.19 per doubling of K from 36 to
+# 144 in C3; Theta(L^2 d) per output in C4).
 WORKLOADS = {
     "c3": dict(make=lambda: workloads.c3_conv(64, 64, 256, 256, 16, 16), ctas=4,
                name="C3 conv 3x3 direct vs im2col-tiled, 256x256, 64->64 ch (256 CTA pairs of 16x16 px x 64 ch)",
                kernel_a="conv_direct (256 threads)", kernel_b="conv_im2col (256 threads, patch staged + sync)",
-               # reference CPU sample: the same CTA with 2 of 64 output channels (the
-               # reference retains every partial sum; a full CTA does not fit host RAM)
-               ref=lambda: workloads.c3_conv(64, 2, 256, 256, 16, 16)),
+               ref=lambda: workloads.c3_conv(8, 1, 256, 256, 16, 16), ref_scale=(72 / 576) ** 2,
+               ref_what="C3 CTA pairs (16x16 tile, 256 threads) at 8 input channels and 1 output channel "
+                        "(K = 72-term outputs), per-element rate scaled by (72/576)^2 to K = 576"),
     "c2": dict(make=lambda: workloads.c2_reduce(n_blocks=1024, block=1024), ctas=1024,
                name="C2 warp-shuffle tree reduction vs sequential sum, N=2^20 as 1024 CTA pairs x 1024 elements",
                kernel_a="reduce_seq (1 thread)", kernel_b="reduce_shfl (1024 threads, warp 32)",
-               ref=lambda: workloads.c2_reduce(n_blocks=1024, block=1024)),
+               ref=lambda: workloads.c2_reduce(n_blocks=1024, block=1024), ref_scale=1.0,
+               ref_what="CTA pairs of the C2 grid itself (no scaling)"),
     "c4": dict(make=lambda: workloads.c4_attention(4096, 128, 16, 16, 64), ctas=1,
                name="C4 attention naive softmax(QK^T)V vs online softmax, seq 4096, d 128 (256 CTA pairs of 16 rows)",
                kernel_a="attn_naive (256 threads)", kernel_b="attn_online (256 threads, key blocks of 64)",
-               ref=lambda: workloads.c4_attention(256, 32, 16, 16, 64)),
+               ref=lambda: workloads.c4_attention(128, 16, 16, 16, 64), ref_scale=(128 / 4096) ** 2 * (16 / 128),
+               ref_what="C4 CTA pairs at seq 128, d 16 (16 rows x 16 threads per row, key blocks of 64), "
+                        "per-element rate scaled by Theta(L^2 d) to seq 4096, d 128"),
 }
 
 
-def ref_sample(wl, key, ncpu, seconds, blocks):
+def ref_sample(wl, ncpu, seconds, blocks):
     r, err = ref_bench(wl["ref"](), blocks, seconds, ncpu)
     if r is None:
         return None, err
     busy = r["busy_s"] / ncpu
-    v = r["elements"] / busy if busy else 0.0
-    what = {"c3": "CTA pairs of the C3 grid with 2 of 64 output channels (same 576-term outputs)",
-            "c2": "CTA pairs of the C2 grid",
-            "c4": "CTA pairs of C4 at seq 256, d 32 (16 rows x 16 threads per row; per-output cost grows with seq)"}
-    return {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference", "cpu": cpu_model(),
-            "sample": f"{r['pairs']} {what[key]}, {seconds:.0f}s bound, exec+decide span"}, None
+    measured = r["elements"] / busy if busy else 0.0
+    return {"value": measured * wl["ref_scale"], "unit": "elements/s", "cores": ncpu, "kind": "reference",
+            "cpu": cpu_model(), "measured_sample_value": measured, "scale_to_config": wl["ref_scale"],
+            "sample": f"{r['pairs']} {wl['ref_what']}; {seconds:.0f}s bound, exec+decide span, all host threads"}, None
 
 
 def cpu_model():
@@ -199,27 +205,29 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        per = max(1, min(steps, 10))
+        per = max(1, min(steps, 5))
         samples = []
         nb = wl["ref"]().n_blocks
-        for s in range(args.warmup + per):
-            blocks = [(s * 8 + k) % nb for k in range(8)]
+        for st in range(args.warmup + per):
+            blocks = [(st * 8 + k) % nb for k in range(8)]
             r, err = ref_bench(wl["ref"](), blocks, max(2.0, args.cpu_seconds / per), ncpu)
             if r is None:
                 print(json.dumps({"impl": "reference", "unavailable": err}))
                 return
-            if s >= args.warmup:
+            if st >= args.warmup:
                 samples.append(r)
         el = sum(r["elements"] for r in samples)
         busy = sum(r["busy_s"] for r in samples) / ncpu
-        v = el / busy if busy > 0 else 0.0
+        measured = el / busy if busy > 0 else 0.0
+        v = measured * wl["ref_scale"]
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": world,
             "steps": per, "warmup": args.warmup, "ms_per_step": 1000.0 * busy / per if per else None,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "exact rational (GMP)",
             "data": "synthetic", "config": cfg_json,
             "cpu_baseline": {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference", "cpu": cpu_model(),
-                             "sample": f"{sum(r['pairs'] for r in samples)} CTA pairs, 8 per step"},
+                             "measured_sample_value": measured, "scale_to_config": wl["ref_scale"],
+                             "sample": f"{sum(r['pairs'] for r in samples)} {wl['ref_what']}"},
             "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -394,7 +402,7 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, err = ref_sample(wl, args.workload, ncpu, args.cpu_seconds, list(range(8)))
+        cb, err = ref_sample(wl, ncpu, args.cpu_seconds, list(range(8)))
         line["cpu_baseline"] = cb if cb is not None else {
             "value": None, "unit": "elements/s", "cores": ncpu, "kind": "reference", "sample": f"unavailable: {err}"}
     if rank == 0:

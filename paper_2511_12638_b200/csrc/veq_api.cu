@@ -910,8 +910,7 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
         { int r_ = ws_get(ctx, 19, (void **)&prof, 128 * 8); if (r_) return r_; }
         CK(cudaMemsetAsync(prof, 0, 128 * 8, s));
       }
-      static const uint32_t eval_off = (getenv("VEQ_EVAL_OFF") ? (uint32_t)atoi(getenv("VEQ_EVAL_OFF")) : 0u) |
-                                       ((getenv("VEQ_EVAL_PAIR") && getenv("VEQ_EVAL_PAIR")[0] == '1') ? 0u : 1u);
+      static const uint32_t eval_off = getenv("VEQ_EVAL_OFF") ? (uint32_t)atoi(getenv("VEQ_EVAL_OFF")) : 0u;
       EvalCtx E{log, log_stmt, base, prof, eval_off};
       uint4 *desc = nullptr;
       { int r_ = ws_get(ctx, 20, (void **)&desc, n_work * sizeof(uint4)); if (r_) return r_; }

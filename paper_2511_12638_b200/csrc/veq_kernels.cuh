@@ -1698,11 +1698,9 @@ __device__ __forceinline__ uint32_t wait_node(const Batch &B, uint32_t r) {
 struct EvalCtx {
   const uint32_t *log, *log_stmt, *log_base;
   unsigned long long *prof;  // optional eval profile (VEQ_PROF=1), see veq_api.cu
-  // path switches (VEQ_EVAL_OFF / VEQ_EVAL_PAIR, diagnostics): 1 no pairing,
-  // 2 no smem path, 4 no lean path. Pairing (two <= 16-leaf sums per warp,
-  // lean_pair16) is off unless VEQ_EVAL_PAIR=1: on short work lists its two
-  // half-warps were observed to split permanently (a lane-16 half running the
-  // full-warp paths alone), see profiles/r02_pairing.md.
+  // path switches (VEQ_EVAL_OFF, diagnostics): 2 no smem path, 4 no lean
+  // path. (Half-warp pairing of small sums was removed in round 2, see
+  // profiles/r02_pairing.md; lane-parallel runs replace it.)
   uint32_t off;
 };
 
@@ -1839,14 +1837,22 @@ __device__ __forceinline__ bool desc_is_add(const uint4 &d) {
   return (d.w & 0xff) == VEQ_ST_BINOP && ((d.w >> 8) & 0xff) == VEQ_BIN_ADD;
 }
 
-// Warp-per-item evaluation: fused Add chains run warp-cooperatively
-// (veq_warp.cuh); every other operation runs on lane 0. Sums of at most 32
-// terms stay in registers; larger ones take pages of the block's shared-
-// memory pool (warp_add_smem); like terms, -inf leaves or an exhausted pool
-// use the global-scratch path (warp_add_nary). The next item's descriptor
-// and first 32 chain-log entries are loaded while the current one runs.
-// 64 registers/thread: 32 resident warps per SM in one block sharing one
-// 216 KB page pool.
+// Window evaluation. A warp claims a window of G consecutive items of the
+// (step, program)-sorted work list and walks it in order:
+//  * a fused Add chain runs warp-cooperatively (veq_warp.cuh): sums of at
+//    most 32 terms in registers, larger ones in a shared-memory page pool
+//    (one 32-warp block per SM, 54 x 4 KB pages; warp_add_smem), rare cases
+//    (like terms, coefficients, -inf leaves, an exhausted pool) on exact
+//    global-scratch paths;
+//  * a maximal run of other items (Mul / Div / Neg / Exp / Max chains) runs
+//    LANE-parallel, one item per lane (eval_stmt, veq_canon.cuh): products of
+//    atoms — the bulk of C3/C4 — no longer leave 31 lanes idle. An item may
+//    wait on an earlier item of its own run (another lane): diverged lanes
+//    make independent progress, and nothing in eval_stmt synchronises the
+//    warp.
+// Every dependency of an item lies earlier in the sorted list, so windows
+// claimed in list order always make progress. 64 registers/thread: 32
+// resident warps per SM in one block sharing one 216 KB page pool.
 constexpr uint32_t EVAL_BLOCK = 1024, EVAL_PAGES = 54;
 // k_eval_warp is compiled in its own translation unit (veq_eval.cu) and
 // launched through launch_eval_warp (parallel builds; the rest of the
@@ -1857,16 +1863,104 @@ void launch_eval_warp(uint32_t grid, uint32_t block, int smem, cudaStream_t s, c
                       unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
                       uint64_t chunk);
 #ifdef VEQ_TU_EVAL
+// One fused Add chain, whole warp (lg: the chain's first 32 log entries,
+// lane-indexed). Returns the canonical sum; `created` when this warp
+// published a new node (its fence already ran).
+__device__ inline uint32_t eval_add_warp(const Batch &B, const Table &T, const EvalCtx &E, Arena &A, WarpAlloc &W,
+                                         const SmemPool &SP, const uint4 d, const uint32_t lg, bool &created,
+                                         int &path, unsigned long long *prof_lean, unsigned long long *prof_smem,
+                                         unsigned long long &prof_pool, unsigned long long &prof_pages) {
+  const uint32_t lane = lane_id();
+  const uint32_t b = d.y, n = d.z;
+  uint32_t r = UNSET;
+  created = false;
+  path = 0;
+  // operands ready, -inf check; sums of <= 32 terms finish in registers
+  uint32_t leaf0 = lane < n ? wait_node(B, lg) : UNSET, m = 0;
+  bool neg = leaf0 == T.id_neginf;
+  for (uint32_t k = lane + 32; k < n; k += 32) neg |= wait_node(B, E.log[b + k]) == T.id_neginf;
+  neg = __any_sync(kFull, neg);
+  if (!neg) {
+    bool counted = false;
+    if (n <= 32 && !(E.off & 4)) {
+      r = warp_add_lean(T, leaf0, n, m, &W, &created, prof_lean);
+      counted = true;
+      path = 1;
+    }
+    if (r == UNSET && (!counted || m > 32)) {
+      if (!counted) {
+        for (uint32_t k = lane; k < n; k += 32) m += n_terms_of(T, wait_node(B, E.log[b + k]));
+        m = __reduce_add_sync(kFull, m);
+      }
+      // leaves with coefficient terms need the grouping region
+      bool cleaf = false;
+      for (uint32_t k = lane; k < n; k += 32) {
+        const uint32_t fl = ld_node(T, wait_node(B, E.log[b + k])).flags;
+        cleaf |= (fl & (F_COEF | F_ANYCOEF)) != 0;
+      }
+      cleaf = __any_sync(kFull, cleaf);
+      const uint32_t pages = (uint32_t)((add_smem_bytes(n, m, cleaf) + SPAGE - 1) / SPAGE);
+      const long long pa0 = E.prof ? clock64() : 0;
+      const int first = (E.off & 2) ? -1 : pool_acquire(SP, pages);
+      if (E.prof && lane == 0) {
+        prof_pool += clock64() - pa0;
+        prof_pages += pages;
+      }
+      if (first >= 0) {
+        char *buf = SP.base + (uint64_t)first * SPAGE;
+        uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
+        for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
+        __syncwarp();
+        r = warp_add_smem(T, buf, n, m, &W, prof_smem, cleaf);
+        pool_release(SP, first, pages);
+        path = 2;
+      }
+    } else if (r == UNSET && n <= 32) {
+      r = warp_add_small_reg(T, leaf0, n);  // like terms / coefficients
+      path = 3;
+    }
+  }
+  if (r == UNSET) {
+    path = 4;
+    uint32_t *ids = warp_get<uint32_t>(A, n);
+    r = T.id_zero;
+    if (ids) {
+      for (uint32_t k = lane; k < n; k += 32) ids[k] = wait_node(B, E.log[b + k]);
+      __syncwarp();
+      uint32_t start = 0;
+      if (neg) {
+        // -inf operands: same restart rule as eval_stmt, sequentially
+        if (lane == 0) {
+          for (uint32_t k = 0; k < n; k++) {
+            if (ids[k] != T.id_neginf) continue;
+            uint32_t s = E.log_stmt[b + k];
+            arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
+            uint32_t rr = k < 1 ? 1 : k;
+            ids[rr] = intern_undef(T, 3, s >> 29, s);
+            start = rr;
+            if (k == 0) k = 1;
+          }
+        }
+        start = __shfl_sync(kFull, start, 0);
+        __syncwarp();
+      }
+      r = warp_add_small(T, ids + start, n - start);
+      if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
+    }
+  }
+  return r;
+}
+
 __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
                                                              const unsigned long long *n_work_dev,
                                                              unsigned long long *cursor, char *pool,
                                                              unsigned long long *pool_used, uint64_t pool_cap,
                                                              uint64_t chunk) {
-  // work-list length and claim size from the device (no host read-back):
-  // a short list is claimed one item at a time so it spreads over all warps
+  // work-list length and window size from the device (no host read-back): a
+  // short list is claimed in small windows so it spreads over all warps
   const uint64_t n_work = *n_work_dev;
   const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  const uint32_t grab = n_work >= warps_total * 16 ? 4 : (n_work >= warps_total * 4 ? 2 : 1);
+  const uint32_t G = n_work >= warps_total * 128 ? 32 : (n_work >= warps_total * 16 ? 8 : 1);
   extern __shared__ __align__(16) char eval_smem[];
   __shared__ unsigned long long s_mask;
   if (threadIdx.x == 0) s_mask = 0;
@@ -1875,226 +1969,105 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
   Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, chunk, 0};
   WarpAlloc W{0, 0, 0, 0};
   const uint32_t lane = lane_id();
-  // items are claimed `grab` at a time; a warp works through its run in
-  // order, and every dependency of an item lies earlier in the sorted list,
-  // so progress is guaranteed.
   // first window: fixed, interleaved across blocks (warp j of block b takes
-  // window j * gridDim + b), so a short work list spreads over every SM and
-  // every block's page pool; later windows come from the shared cursor
+  // window j * gridDim + b), so a short list spreads over every SM; later
+  // windows come from the shared cursor
   const uint32_t wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const unsigned long long first_windows = (unsigned long long)gridDim.x * wpb;
-  auto claim = [&]() -> unsigned long long {
-    unsigned long long x = 0;
-    if (lane == 0) x = atomicAdd(cursor, (unsigned long long)grab);
-    return __shfl_sync(kFull, x, 0) + first_windows * grab;
-  };
-  auto fetch = [&](unsigned long long w, uint4 &d, uint32_t &lg) {
-    d = w < n_work ? __ldg(desc + w) : make_uint4(0, 0, 0, 0xff);
-    lg = (w < n_work && desc_is_add(d) && lane < d.z) ? __ldg(E.log + d.y + lane) : UNSET;
-  };
-  unsigned long long prof_wait = 0, prof_work[6] = {0, 0, 0, 0, 0, 0}, prof_n[6] = {0, 0, 0, 0, 0, 0}, prof_lean[3] = {0, 0, 0}, prof_pool = 0, prof_pages = 0, prof_smem[4] = {0, 0, 0, 0};
+  unsigned long long prof_wait = 0, prof_work[6] = {0, 0, 0, 0, 0, 0}, prof_n[6] = {0, 0, 0, 0, 0, 0},
+                     prof_lean[3] = {0, 0, 0}, prof_pool = 0, prof_pages = 0, prof_smem[4] = {0, 0, 0, 0};
   unsigned long long t_k0 = 0;
   if (E.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_k0));
   // VEQ_PROF timeline: items finished / smem items finished / warps done per
-  // 100 us bucket since the block started (slots 32..127)
+  // 400 us bucket since the kernel started (slots 32..127)
   auto tbucket = [&]() -> uint32_t {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const unsigned long long b = (t - t_k0) / 400000;
-    return (uint32_t)(b < 31 ? b : 31);
+    const unsigned long long bk = (t - t_k0) / 400000;
+    return (uint32_t)(bk < 31 ? bk : 31);
   };
-  unsigned long long w = ((unsigned long long)wib * gridDim.x + blockIdx.x) * grab, w_end = w + grab;
-  uint4 d;
-  uint32_t lg;
-  fetch(w, d, lg);
-  auto next_of = [&](unsigned long long x) -> unsigned long long {
-    unsigned long long y = x + 1;
-    if (y == w_end) {
-      y = claim();
-      w_end = y + grab;
-    }
-    return y;
-  };
-  while (w < n_work) {
-    const unsigned long long wn = next_of(w);
-    uint4 dn;
-    uint32_t lgn;
-    fetch(wn, dn, lgn);
-    // two consecutive small chains with no dependency between them run on
-    // the two halves of the warp (lean_pair16)
-    bool paired = !(E.off & 1) && wn < n_work && desc_is_add(d) && d.z <= 16 && desc_is_add(dn) && dn.z <= 16;
-    if (paired) paired = !__any_sync(kFull, lane < dn.z && lgn == d.x);
-    uint32_t rA = UNSET, rB = UNSET;
-    if (paired) {
-      const long long t0 = E.prof ? clock64() : 0;
-      const uint32_t sl = lane & 15;
-      const uint32_t lgp = __shfl_sync(kFull, lgn, sl);
-      const uint32_t my_lg = lane < 16 ? lg : lgp, my_n = lane < 16 ? d.z : dn.z;
-      const uint32_t leaf = sl < my_n ? wait_node(B, my_lg) : UNSET;
-      const uint32_t negm = __ballot_sync(kFull, leaf == T.id_neginf);
-      const bool skip = (negm & (0xffffu << (lane & 16))) != 0;  // -inf leaves: full path
-      bool created = false;
-      const uint32_t r = lean_pair16(T, leaf, my_n, skip, W, created, E.prof ? E.prof + 24 : nullptr);
-      rA = __shfl_sync(kFull, r, 0);
-      rB = __shfl_sync(kFull, r, 16);
-      if ((lane == 0 || lane == 16) && r != UNSET) {
-        if (!created) fence_acq_rel();
-        atomicExch(B.canon + (lane == 0 ? d.x : dn.x), r);
-      }
-      if (E.prof && lane == 0) {
-        prof_work[5] += clock64() - t0;
-        prof_n[5] += (rA != UNSET) + (rB != UNSET);
-        atomicAdd(E.prof + 32 + tbucket(), (unsigned long long)((rA != UNSET) + (rB != UNSET)));
-      }
-    }
-    // the lanes that published a pair result rejoin the warp here
-    __syncwarp();
-    // items left for the full warp: the current one when unpaired, else the
-    // halves the pair path did not cover (in list order)
-    const bool needA = !paired || rA == UNSET, needB = paired && rB == UNSET;
-    for (int q = 0; q < 2; q++) {
-      if (q == 0 ? !needA : !needB) continue;
-      const uint4 dq = q == 0 ? d : dn;
-      const uint32_t lgq = q == 0 ? lg : lgn;
-      {
-        const uint4 &d = dq;
-        const uint32_t lg = lgq;
-    const uint32_t i = d.x;
-      const uint64_t mark = A.used;
-      char *const mbase = A.base;
-      A.item = i;
-      uint32_t r = UNSET;
-      bool created = false;
-      int path = 0;  // 0 other, 1 lean, 2 smem, 3 small_reg, 4 global
-      long long t0 = E.prof ? clock64() : 0, t1 = 0;
-      if (desc_is_add(d)) {
-        const uint32_t b = d.y, n = d.z;
-        // operands ready, -inf check; sums of <= 32 terms finish in registers
-        uint32_t leaf0 = lane < n ? wait_node(B, lg) : UNSET, m = 0;
-        bool neg = leaf0 == T.id_neginf;
-        for (uint32_t k = lane + 32; k < n; k += 32) neg |= wait_node(B, E.log[b + k]) == T.id_neginf;
-        neg = __any_sync(kFull, neg);
-        if (E.prof) t1 = clock64();
-        if (!neg) {
-          bool counted = false;
-          if (n <= 32 && !(E.off & 4)) {
-            r = warp_add_lean(T, leaf0, n, m, &W, &created, E.prof ? prof_lean : nullptr);
-            counted = true;
-            path = 1;
-          }
-          if (r == UNSET && (!counted || m > 32)) {
-            if (!counted) {
-              for (uint32_t k = lane; k < n; k += 32) m += n_terms_of(T, wait_node(B, E.log[b + k]));
-              m = __reduce_add_sync(kFull, m);
-            }
-            // leaves with coefficient terms need the grouping region
-          bool cleaf = false;
-          for (uint32_t k = lane; k < n; k += 32) {
-            const uint32_t fl = ld_node(T, wait_node(B, E.log[b + k])).flags;
-            cleaf |= (fl & (F_COEF | F_ANYCOEF)) != 0;
-          }
-          cleaf = __any_sync(kFull, cleaf);
-          const uint32_t pages = (uint32_t)((add_smem_bytes(n, m, cleaf) + SPAGE - 1) / SPAGE);
-            const long long pa0 = E.prof ? clock64() : 0;
-            const int first = (E.off & 2) ? -1 : pool_acquire(SP, pages);
-            if (E.prof && lane == 0) {
-              prof_pool += clock64() - pa0;
-              prof_pages += pages;
-            }
-            if (first >= 0) {
-              char *buf = SP.base + (uint64_t)first * SPAGE;
-              uint32_t *lv = reinterpret_cast<uint32_t *>(buf);
-              for (uint32_t k = lane; k < n; k += 32) lv[k] = wait_node(B, E.log[b + k]);
-              __syncwarp();
-              r = warp_add_smem(T, buf, n, m, &W, E.prof ? prof_smem : nullptr, cleaf);
-              pool_release(SP, first, pages);
-              path = 2;
-            }
-          } else if (r == UNSET && n <= 32) {
-            r = warp_add_small_reg(T, leaf0, n);  // like terms / coefficients
-            path = 3;
+  unsigned long long w0 = ((unsigned long long)wib * gridDim.x + blockIdx.x) * G;
+  while (w0 < n_work) {
+    const uint32_t cnt = (uint32_t)(n_work - w0 < G ? n_work - w0 : G);
+    // the window's descriptors, one coalesced load; bit mask of Add chains
+    const uint4 dl = lane < cnt ? __ldg(desc + w0 + lane) : make_uint4(0, 0, 0, 0xff);
+    const uint32_t addm = __ballot_sync(kFull, lane < cnt && desc_is_add(dl));
+    uint32_t j = 0;
+    while (j < cnt) {
+      if ((addm >> j) & 1u) {
+        // ---- a fused Add chain: the whole warp
+        const uint4 d = make_uint4(__shfl_sync(kFull, dl.x, j), __shfl_sync(kFull, dl.y, j),
+                                   __shfl_sync(kFull, dl.z, j), __shfl_sync(kFull, dl.w, j));
+        const uint32_t lg = lane < d.z ? __ldg(E.log + d.y + lane) : UNSET;
+        const uint64_t mark = A.used;
+        char *const mbase = A.base;
+        A.item = d.x;
+        const long long t0 = E.prof ? clock64() : 0;
+        bool created = false;
+        int path = 0;
+        const uint32_t r = eval_add_warp(B, T, E, A, W, SP, d, lg, created, path, E.prof ? prof_lean : nullptr,
+                                         E.prof ? prof_smem : nullptr, prof_pool, prof_pages);
+        if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
+        if (lane == 0) {
+          // a node this warp created was fenced before its slot was claimed;
+          // anything else needs the fence for cumulativity
+          if (!created) fence_acq_rel();
+          atomicExch(B.canon + d.x, r);
+          if (E.prof) {
+            prof_work[path] += clock64() - t0;
+            prof_n[path]++;
+            const uint32_t tb = tbucket();
+            atomicAdd(E.prof + 32 + tb, 1ull);
+            if (path == 2) atomicAdd(E.prof + 64 + tb, 1ull);
           }
         }
-        if (r == UNSET) {
-          path = 4;
-          __syncwarp();
-          uint32_t *ids = warp_get<uint32_t>(A, n);
-          r = T.id_zero;
-          if (ids) {
-            for (uint32_t k = lane; k < n; k += 32) ids[k] = wait_node(B, E.log[b + k]);
-            __syncwarp();
-            uint32_t start = 0;
-            if (neg) {
-              // -inf operands: same restart rule as eval_stmt, sequentially
-              if (lane == 0) {
-                for (uint32_t k = 0; k < n; k++) {
-                  if (ids[k] != T.id_neginf) continue;
-                  uint32_t s = E.log_stmt[b + k];
-                  arith_fault(B, s, VEQ_DETAIL_NEGINF_ADD);
-                  uint32_t rr = k < 1 ? 1 : k;
-                  ids[rr] = intern_undef(T, 3, s >> 29, s);
-                  start = rr;
-                  if (k == 0) k = 1;
-                }
-              }
-              start = __shfl_sync(kFull, start, 0);
-              __syncwarp();
-            }
-            r = warp_add_small(T, ids + start, n - start);
-            if (r == UNSET) r = warp_add_nary(T, A, ids + start, n - start);
-          }
-        }
-      } else {
-        if (lane == 0) r = eval_stmt(B, T, A, E, i);
-        r = __shfl_sync(kFull, r, 0);
+        j++;
+        continue;
       }
-      if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
-      if (lane == 0) {
-        // a node this warp created was fenced before its slot was claimed;
-        // anything else needs the fence for cumulativity
-        if (!created) fence_acq_rel();
+      // ---- a run of non-Add items [j, k): one per lane
+      const uint32_t above = j + 1 < 32 ? (addm >> (j + 1)) << (j + 1) : 0u;
+      const uint32_t k = above ? (uint32_t)(__ffs(above) - 1) : cnt;
+      if (lane >= j && lane < k) {
+        const uint32_t i = dl.x;
+        const uint64_t mark = A.used;
+        char *const mbase = A.base;
+        A.item = i;
+        const long long t0 = E.prof ? clock64() : 0;
+        const uint32_t r = eval_stmt(B, T, A, E, i);
+        if (A.base == mbase) A.used = mark;
+        fence_acq_rel();
         atomicExch(B.canon + i, r);
         if (E.prof) {
-          long long t2 = clock64();
-          if (!t1) t1 = t0;
-          prof_wait += t1 - t0;
-          prof_work[path] += t2 - t1;
-          prof_n[path]++;
-          const uint32_t tb = tbucket();
-          atomicAdd(E.prof + 32 + tb, 1ull);
-          if (path == 2) atomicAdd(E.prof + 64 + tb, 1ull);
+          prof_work[0] += clock64() - t0;
+          prof_n[0]++;
+          atomicAdd(E.prof + 32 + tbucket(), 1ull);
         }
       }
-      }
+      __syncwarp();
+      j = k;
     }
-    if (paired) {
-      w = next_of(wn);
-      fetch(w, d, lg);
-    } else {
-      w = wn;
-      d = dn;
-      lg = lgn;
-    }
+    // next window: the cursor counts windows claimed after the first ones
+    unsigned long long x = 0;
+    if (lane == 0) x = atomicAdd(cursor, 1ull);
+    w0 = (__shfl_sync(kFull, x, 0) + first_windows) * G;
   }
-  if (lane == 0 || lane == 16) wa_flush(T, W);  // both halves allocate in lean_pair16
-  if (lane == 0) {
-    if (E.prof) {
-      atomicAdd(E.prof + 96 + tbucket(), 1ull);
-      atomicAdd(E.prof, prof_wait);
-      for (int k = 0; k < 5; k++) {
-        atomicAdd(E.prof + 1 + k, prof_work[k]);
-        atomicAdd(E.prof + 6 + k, prof_n[k]);
-      }
-      atomicAdd(E.prof + 20, prof_work[5]);
-      atomicAdd(E.prof + 21, prof_n[5]);
-      for (int k = 0; k < 3; k++) atomicAdd(E.prof + 11 + k, prof_lean[k]);
+  wa_flush(T, W);
+  if (E.prof) {
+    if (lane == 0) atomicAdd(E.prof + 96 + tbucket(), 1ull);
+    // per-lane counters (lane-parallel runs) and lane 0's (warp items)
+    atomicAdd(E.prof, prof_wait);
+    for (int q = 0; q < 5; q++) {
+      atomicAdd(E.prof + 1 + q, prof_work[q]);
+      atomicAdd(E.prof + 6 + q, prof_n[q]);
+    }
+    if (lane == 0) {
+      for (int q = 0; q < 3; q++) atomicAdd(E.prof + 11 + q, prof_lean[q]);
       atomicAdd(E.prof + 14, prof_pool);
       atomicAdd(E.prof + 15, prof_pages);
-      for (int k = 0; k < 4; k++) atomicAdd(E.prof + 16 + k, prof_smem[k]);
+      for (int q = 0; q < 4; q++) atomicAdd(E.prof + 16 + q, prof_smem[q]);
     }
   }
 }
-
 #endif  // VEQ_TU_EVAL
 
 #ifndef VEQ_TU_EVAL

@@ -640,189 +640,6 @@ __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t
   return res;
 }
 
-// ---- two small sums per warp ----------------------------------------------
-// Lanes 0-15 evaluate one fused Add chain, lanes 16-31 another (each with at
-// most 16 leaves and 16 terms): the lean path with every shuffle segmented
-// to 16 lanes and every vote masked to the half, so one instruction stream
-// serves two items. Every shuffle and vote is executed by all 32 lanes.
-// A half returns UNSET when the lean rules do not cover its sum (more than
-// 16 terms, a coefficient term, more than one Const, tied prefixes, like
-// terms); the caller then evaluates that item with the full-warp paths.
-__device__ __forceinline__ uint32_t half_or(uint32_t v) {
-#pragma unroll
-  for (int o = 8; o; o >>= 1) v |= __shfl_xor_sync(kFull, v, o, 16);
-  return v;
-}
-__device__ __forceinline__ uint64_t half_sum(uint64_t v) {
-#pragma unroll
-  for (int o = 8; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o, 16);
-  return v;
-}
-static __device__ __noinline__ uint32_t lean_pair16(const Table &T, uint32_t leaf, uint32_t n, bool skip, WarpAlloc &W,
-                                            bool &created, unsigned long long *dbg = nullptr) {
-  const uint32_t lane = lane_id(), sl = lane & 15, sb = lane & 16;
-  const uint32_t hmask = 0xffffu << sb;
-  created = false;
-  __syncwarp();  // both halves enter together (their leaf waits may diverge)
-  // leaves and term counts
-  uint32_t c = 0, kind = 0;
-  uint64_t p0 = 0;
-  if (sl < n) {
-    const Node ln = ld_node(T, leaf);
-    kind = ln.kind;
-    p0 = ln.p0;
-    c = ln.kind == K_ADD ? ln.nkids : 1;
-  }
-  uint32_t x = c;
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, o, 16);
-    if (sl >= (unsigned)o) x += y;
-  }
-  const uint32_t m = __shfl_sync(kFull, x, 15, 16), ex = x - c;
-  bool fb = skip || m > 16;
-  const uint32_t starts = half_or((!fb && sl < n && c) ? (1u << ex) : 0u);
-  const uint32_t src = (__popc(starts & ((2u << sl) - 1)) - 1) & 15;
-  const uint32_t lk = __shfl_sync(kFull, kind, src, 16);
-  const uint64_t lp = __shfl_sync(kFull, p0, src, 16);
-  const uint32_t lid = __shfl_sync(kFull, leaf, src, 16);
-  const uint32_t lex = __shfl_sync(kFull, ex, src, 16);
-  // terms: id, order prefix, hash, flags
-  uint32_t id = UNSET;
-  uint64_t key = ~0ull, hsh = 0;
-  uint8_t fl = 0, tk = 0xff;  // 0xff: no term on this lane
-  bool czero = false;
-  if (!fb && sl < m) {
-    id = lk == K_ADD ? ld_kid(T, lp + (sl - lex)) : lid;
-    const Node tn = ld_node(T, id);
-    key = prefix_of(tn);
-    hsh = tn.hash;
-    fl = tn.flags;
-    tk = tn.kind;
-    czero = tn.kind == K_CONST && (long long)tn.p0 == 0;
-  }
-  const uint32_t coefm = __ballot_sync(kFull, tk == K_MUL && (fl & F_COEF)) & hmask;
-  const uint32_t constm = __ballot_sync(kFull, tk == K_CONST) & hmask;
-  if (dbg && sl == 0) {
-    if (skip) atomicAdd(dbg + 0, 1ull);
-    else if (m > 16) atomicAdd(dbg + 1, 1ull);
-    else if (coefm) atomicAdd(dbg + 2, 1ull);
-    else if (__popc(constm) > 1) atomicAdd(dbg + 3, 1ull);
-  }
-  const bool fb0 = fb || coefm != 0 || __popc(constm) > 1;
-  fb |= coefm != 0 || __popc(constm) > 1;
-  if (czero) {  // a single literal 0 term is dropped (zero coefficient)
-    id = UNSET;
-    key = ~0ull;
-  }
-  const uint32_t real = fb ? 0 : __popc(__ballot_sync(kFull, id != UNSET) & hmask);
-  // canonical order within each half (order prefix; ties fall back)
-  uint32_t aux = sl;
-#pragma unroll
-  for (uint32_t k = 2; k <= 16; k <<= 1) {
-#pragma unroll
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      const uint64_t pk = __shfl_xor_sync(kFull, key, j, 16);
-      const uint32_t pv = __shfl_xor_sync(kFull, aux, j, 16);
-      const bool up = (sl & k) == 0, lower = (sl & j) == 0;
-      const bool take = (up == lower) ? (pk < key) : (key < pk);
-      key = take ? pk : key;
-      aux = take ? pv : aux;
-    }
-  }
-  id = __shfl_sync(kFull, id, aux, 16);
-  const uint64_t kh = __shfl_sync(kFull, hsh, aux, 16);
-  const uint32_t kf = __shfl_sync(kFull, (uint32_t)fl, aux, 16);
-  {
-    const uint64_t pk = __shfl_up_sync(kFull, key, 1, 16);
-    const uint32_t pi = __shfl_up_sync(kFull, id, 1, 16);
-    const bool bad = sl > 0 && sl < real && (key == pk || id == pi);  // tie or like terms
-    fb |= (__ballot_sync(kFull, bad) & hmask) != 0;
-    if (dbg && sl == 0 && fb && !fb0) atomicAdd(dbg + 4, 1ull);
-  }
-  const uint32_t first_id = __shfl_sync(kFull, id, 0, 16);
-  // intern the halves with real >= 2 (an Add of `real` kids)
-  const bool act = !fb && real >= 2;
-  const bool in = act && sl < real;
-  const uint64_t sum = half_sum(in ? kid_term(sl, kh) : 0);
-  const uint32_t pdm = __ballot_sync(kFull, in && (kf & F_POSDEF)) & hmask;
-  const uint32_t dvm = __ballot_sync(kFull, in && (kf & F_HASDIV)) & hmask;
-  const uint32_t inm = __ballot_sync(kFull, in) & hmask;
-  // the node record is written by each half's lane 0, whose own sorted key
-  // is the first kid's prefix (no shuffle: a shuffle whose result is used
-  // only under `act` may be sunk into that branch, where the halves diverge)
-  const uint64_t h = composite_hash(K_ADD, real, sum);
-  const uint8_t flags = composite_flags(K_ADD, pdm != 0, pdm == inm, dvm != 0, false);
-  const uint64_t p1 = composite_prefix(K_ADD, real, key);
-  unsigned long long nid = 0, off = 0;
-  bool ok = true;
-  if (act && sl == 0) ok = wa_alloc(T, W, real, (uint64_t &)nid, (uint64_t &)off);
-  nid = __shfl_sync(kFull, nid, 0, 16);
-  off = __shfl_sync(kFull, off, 0, 16);
-  ok = __shfl_sync(kFull, ok, 0, 16);
-  // keep the shuffles where every lane executes them (their results are used
-  // under per-half conditions below)
-  asm volatile("" : "+l"(nid), "+l"(off));
-  if (act && ok) {
-    if (sl < real) T.kids[off + sl] = id;
-    if (sl == 0) {
-      Node nd;
-      nd.kind = K_ADD;
-      nd.flags = flags;
-      nd.pad = 0;
-      nd.nkids = real;
-      nd.hash = h;
-      nd.p0 = off;
-      nd.p1 = p1;
-      T.nodes[nid] = nd;
-    }
-  }
-  __syncwarp();
-  fence_acq_rel();
-  uint32_t res = fb ? UNSET : (real == 0 ? T.id_zero : (real == 1 ? first_id : UNSET));
-  bool done = !act;
-  if (act && !ok) {  // E_BUDGET already raised
-    res = T.id_zero;
-    done = true;
-  }
-  // claim a slot: CAS at the home slot, then linear probing; both halves
-  // iterate until done (a uniform loop: every shuffle by all lanes)
-  uint64_t slot = h & T.slot_mask;
-  for (uint64_t probes = 0; __any_sync(kFull, !done); probes++) {
-    uint32_t prev = 0;
-    const bool over = !done && probes > T.slot_mask;
-    if (!done && !over && sl == 0) prev = atomicCAS(T.slots + slot, EMPTY, (uint32_t)nid);
-    prev = __shfl_sync(kFull, prev, 0, 16);
-    const bool won = !done && !over && prev == EMPTY;
-    const bool cmp = !done && !over && prev != EMPTY;
-    bool eq = true;
-    if (cmp) {
-      const Node cn = ld_node(T, prev);
-      eq = cn.hash == h && cn.kind == K_ADD && cn.nkids == real && (sl >= real || ld_kid(T, cn.p0 + sl) == id);
-    }
-    const bool alleq = (__ballot_sync(kFull, !eq) & hmask) == 0;
-    if (over) {
-      if (sl == 0) set_error(T, E_BUDGET);
-      res = T.id_zero;
-      done = true;
-    } else if (won) {
-      res = (uint32_t)nid;
-      created = true;
-      done = true;
-    } else if (cmp) {
-      if (alleq) {
-        // a structurally equal node is already present: use it (ours is waste)
-        res = prev;
-        if (sl == 0) wa_waste(T, real);
-        done = true;
-      } else {
-        slot = (slot + 1) & T.slot_mask;
-      }
-    }
-  }
-  return res;
-}
-
 // ---- shared-memory path for large sums -------------------------------------
 // A block-wide pool of 4 KB shared-memory pages; a warp evaluating a sum with
 // more than 32 terms takes a contiguous page run for its working set and
