@@ -5,7 +5,7 @@ the key counters of the full capture of the dominant kernel, and
 profiles/traffic.json (DRAM bytes per launch, read by bench.py for the
 roofline `traffic` field).
 
-  python scripts/ncu_summary.py gpurun_out/launches.csv gpurun_out/prof.ncu-rep r01 eval
+  python scripts/ncu_summary.py gpurun_out/launches.csv gpurun_out/prof.ncu-rep r02_c3 eval [c3]
 """
 import collections
 import csv
@@ -61,13 +61,14 @@ def raw_metrics(rep):
 
 def main():
     lpath, rep, tag, phase = sys.argv[1:5]
+    wl = sys.argv[5] if len(sys.argv) > 5 else "c2"
     step = one_step(launches(lpath))
     agg = collections.OrderedDict()
     for k, us in step:
         n, t = agg.get(k, (0, 0.0))
         agg[k] = (n + 1, t + us)
     tot = sum(t for _, t in agg.values())
-    lines = [f"# {tag}: kernel launches of the device-timed C2 bench step (ncu --metrics gpu__time_duration.sum, "
+    lines = [f"# {tag}: kernel launches of the device-timed {wl.upper()} bench step (ncu --metrics gpu__time_duration.sum, "
              "--clock-control none; cold-cache, serialised: compare shares, not absolutes)", "",
              "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -84,7 +85,7 @@ def main():
             "launch__grid_size", "launch__block_size", "l1tex__t_sector_hit_rate.pct",
             "smsp__average_warp_latency_issue_stalled_long_scoreboard", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
     lines = [f"# {tag}: ncu --set full of the dominant kernel ({phase}), {len(ms)} launch(es); "
-             f"each launch is one bench step's {phase} (kernel A's and kernel B's CTAs in one merged batch)", "",
+             f"each launch is one {wl.upper()} bench step's {phase} (kernel A's and kernel B's CTAs in one merged batch)", "",
              "| metric | unit | " + " | ".join(f"launch {i}" for i in range(len(ms))) + " |",
              "|---|---|" + "---|" * len(ms)]
     for k in keys:
@@ -102,7 +103,7 @@ def main():
         return v * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}.get(u, 1.0)
     # per launch (= per step with merged batches): mean over the captured launches
     traffic = sum(num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum") for m in ms) / max(1, len(ms))
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
     t = json.load(open(tp)) if os.path.exists(tp) else {}
     t[phase] = traffic
     t[f"{phase}_source"] = (f"profiles/{tag}_{phase}_ncu.md (dram__bytes_read.sum + dram__bytes_write.sum, "
