@@ -147,7 +147,7 @@ WORKLOADS = {
                kernel_a="reduce_seq (1 thread)", kernel_b="reduce_shfl (1024 threads, warp 32)",
                ref=lambda: workloads.c2_reduce(n_blocks=1024, block=1024), ref_scale=1.0,
                ref_what="CTA pairs of the C2 grid itself (no scaling)"),
-    "c4": dict(make=lambda: workloads.c4_attention(4096, 128, 16, 16, 64), ctas=1,
+    "c4": dict(make=lambda: workloads.c4_attention(4096, 128, 16, 16, 64), ctas=4, steps=2, scratch_gb=40,
                name="C4 attention naive softmax(QK^T)V vs online softmax, seq 4096, d 128 (256 CTA pairs of 16 rows)",
                kernel_a="attn_naive (256 threads)", kernel_b="attn_online (256 threads, key blocks of 64)",
                ref=lambda: workloads.c4_attention(128, 16, 16, 16, 64), ref_scale=(128 / 4096) ** 2 * (16 / 128),
@@ -194,7 +194,9 @@ def main():
     W = wl["make"]()
     cps = args.ctas or wl["ctas"]
     n_grid = W.n_blocks
-    steps = args.steps or max(1, -(-n_grid // (cps * world)))
+    # default: one pass over the grid (C4: two steps of four full-size CTA
+    # pairs, ~7.5 s each; the whole 256-pair grid takes ~8 min)
+    steps = args.steps or wl.get("steps") or max(1, -(-n_grid // (cps * world)))
     cfg_json = {"workload": wl["name"], "kernel_a": wl["kernel_a"], "kernel_b": wl["kernel_b"],
                 "cta_pairs_in_grid": n_grid, "cta_pairs_per_step_per_gpu": cps,
                 "elements_per_cta_pair": W.elements_per_block,
@@ -252,7 +254,8 @@ def main():
     S_pair = len(ta.stmts) + len(tb.stmts)
     S_step = S_pair * cps
     sess = Session(local, max_nodes=min((1 << 31) - 1, max(1 << 22, 4 * S_step // 10)),
-                   max_kid_words=min((1 << 32) - 1, (1 << 24) + 4 * S_step), scratch_bytes=8 << 30)
+                   max_kid_words=min((1 << 32) - 1, (1 << 24) + 4 * S_step),
+                   scratch_bytes=wl.get("scratch_gb", 8) << 30)
     L = N.lib()
     sess.declare_inputs(inputs)
     ka = [k for k in range(len(ta.arrays)) if int(ta.arrays[k]["role"]) == N.ROLE_OUT]

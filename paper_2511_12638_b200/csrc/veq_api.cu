@@ -46,6 +46,7 @@ struct BatchDev {
   unsigned long long *d_stats = nullptr;  // [0..7] table counters at run start, [8] work items
   bool started = false;                   // veq_run_start enqueued, veq_run_finish pending
   bool timing_run = false;                // phase events recorded by this run
+  bool no_defer = false;                  // deferral off for this batch (set after an E_DEFER fallback)
   uint32_t run_launches = 0;
   unsigned long long n_work_last = 0;  // work items of the last run (read back with its results)
   uint32_t n_threads = 0;
@@ -120,6 +121,10 @@ struct veq_ctx {
   std::vector<veq_vc> vcs;
   std::vector<uint32_t> sc_node;
   std::vector<uint8_t> sc_dis;
+  // deferred-scaling merge memo (EvalCtx::mkeys/mvals), grown per run
+  unsigned long long *mkeys = nullptr;
+  uint32_t *mvals = nullptr;
+  uint64_t mslots = 0;
   // veq_render output
   std::string render_text;
   std::vector<uint64_t> render_offs;
@@ -298,6 +303,8 @@ void veq_close(veq_ctx *ctx) {
   cudaFree(ctx->session_ids);
   cudaFree(ctx->pool);
   cudaFree(ctx->pool_used);
+  cudaFree(ctx->mkeys);
+  cudaFree(ctx->mvals);
   cudaFree(ctx->in_base);
   cudaFree(ctx->in_size);
   cudaFree(ctx->in_cache);
@@ -701,6 +708,8 @@ static int load_impl(veq_ctx *ctx, const veq_batch_desc *d, veq_stmt *dev_stmts,
   AL(chain_len, S, uint32_t);
   AL(uses, S, uint32_t);
   AL(continued, S, uint8_t);
+  AL(user, S, uint32_t);
+  AL(defer, (S + 4) & ~3ull, uint8_t);
   AL(tup_key, n_access, unsigned long long);
   AL(tup_val, n_access, unsigned long long);
   AL(n_tup, 1, unsigned long long);
@@ -747,6 +756,11 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   CK(cudaMemsetAsync(B.canon, 0xff, S * 4, s));
   CK(cudaMemsetAsync(B.uses, 0, S * 4, s));
   CK(cudaMemsetAsync(B.continued, 0, S, s));
+  CK(cudaMemsetAsync(B.defer, 0, (S + 4) & ~3ull, s));
+  {
+    static const bool env_off = getenv("VEQ_NO_DEFER") && getenv("VEQ_NO_DEFER")[0] == '1';
+    B.no_defer = (env_off || bd->no_defer) ? 1u : 0u;
+  }
   // the tuple buffer holds every checked access; slots of accesses that
   // never execute (deadlock) keep key ~0 and sort last, so the sort needs no
   // host read-back of the tuple count
@@ -855,6 +869,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     LAUNCH(k_resolve_all<<<blocks(S, 256), 256, 0, s>>>(B, sz));
   }
   if (bd->n_cells) LAUNCH(k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
+  // deferred scaling: products of a used-once sum feeding a chain (k_mark_defer)
+  if (S && !B.no_defer) LAUNCH(k_mark_defer<<<blocks(S, 256), 256, 0, s>>>(B));
   PH1(VEQ_PH_RESOLVE);
   CK(cudaGetLastError());
   // chain logs
@@ -907,11 +923,30 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
       static const bool prof_on = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
       unsigned long long *prof = nullptr;
       if (prof_on) {
-        { int r_ = ws_get(ctx, 19, (void **)&prof, 128 * 8); if (r_) return r_; }
-        CK(cudaMemsetAsync(prof, 0, 128 * 8, s));
+        { int r_ = ws_get(ctx, 19, (void **)&prof, 256 * 8); if (r_) return r_; }
+        CK(cudaMemsetAsync(prof, 0, 256 * 8, s));
       }
       static const uint32_t eval_off = getenv("VEQ_EVAL_OFF") ? (uint32_t)atoi(getenv("VEQ_EVAL_OFF")) : 0u;
-      EvalCtx E{log, log_stmt, base, prof, eval_off};
+      // merge memo: sized from the arithmetic statements, cleared per run
+      uint64_t want = 1ull << 16;
+      while (want < (bd->n_arith / 8) && want < (1ull << 24)) want <<= 1;
+      if (want > ctx->mslots) {
+        CK(cudaStreamSynchronize(s));
+        cudaFree(ctx->mkeys);
+        cudaFree(ctx->mvals);
+        ctx->mkeys = nullptr;
+        ctx->mvals = nullptr;
+        ctx->mslots = 0;
+        if (cudaMalloc(&ctx->mkeys, want * 8) != cudaSuccess || cudaMalloc(&ctx->mvals, want * 4) != cudaSuccess)
+          return fail(ctx, VEQ_E_OOM, "merge memo");
+        ctx->mslots = want;
+      }
+      CK(cudaMemsetAsync(ctx->mkeys, 0xff, ctx->mslots * 8, s));
+      CK(cudaMemsetAsync(ctx->mvals, 0xff, ctx->mslots * 4, s));
+      static const uint32_t bucket_us = getenv("VEQ_PROF_BUCKET_US") ? (uint32_t)atoi(getenv("VEQ_PROF_BUCKET_US")) : 400u;
+      static const bool no_memo = getenv("VEQ_NO_MEMO") && getenv("VEQ_NO_MEMO")[0] == '1';
+      EvalCtx E{log, log_stmt, base, prof, eval_off, no_memo ? nullptr : ctx->mkeys, ctx->mvals, ctx->mslots - 1,
+                bucket_us ? bucket_us : 400u};
       uint4 *desc = nullptr;
       { int r_ = ws_get(ctx, 20, (void **)&desc, n_work * sizeof(uint4)); if (r_) return r_; }
       LAUNCH(k_make_desc<<<blocks(n_work, 256), 256, 0, s>>>(B, E, wv2, nw, desc));
@@ -938,8 +973,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
                               ctx->pool, ctx->pool_used, ctx->pool_cap, chunk));
       CK(cudaGetLastError());
       if (prof) {
-        unsigned long long hp[128], nwh = 0;
-        CK(cudaMemcpyAsync(hp, prof, 128 * 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long hp[256], nwh = 0;
+        CK(cudaMemcpyAsync(hp, prof, 256 * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&nwh, nw, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         fprintf(stderr, "[veq prof] items %llu warps %llu | wait %.1f us/item |", nwh, (unsigned long long)(threads / 32),
@@ -950,15 +985,20 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
         if (hp[7])
           fprintf(stderr, " | lean phases: loads %.2f sort %.2f intern %.2f us", hp[11] / 1965.0 / hp[7],
                   hp[12] / 1965.0 / hp[7], hp[13] / 1965.0 / hp[7]);
-        if (hp[21] || hp[24] || hp[25] || hp[26] || hp[27] || hp[28])
-          fprintf(stderr, " | pairs: %llu items %.2f us per item; fallbacks skip %llu m>16 %llu coef %llu consts %llu ties %llu",
-                  hp[21], hp[20] / 1965.0 / std::max<unsigned long long>(1, hp[21]), hp[24], hp[25], hp[26], hp[27],
-                  hp[28]);
         if (hp[8])
           fprintf(stderr, " | smem: pool wait %.2f us/item, %.1f pages/item; runs %.2f gather %.2f merge %.2f intern %.2f us",
                   hp[14] / 1965.0 / hp[8], (double)hp[15] / hp[8], hp[16] / 1965.0 / hp[8], hp[17] / 1965.0 / hp[8],
                   hp[18] / 1965.0 / hp[8], hp[19] / 1965.0 / hp[8]);
-        fprintf(stderr, "\n[veq prof] timeline (per 400 us: items, smem items, warps done):");
+        if (hp[27])
+          fprintf(stderr, " | deferred: n=%llu expand %.1f terms %.1f sum %.1f us", hp[27], hp[24] / 1965.0 / hp[27],
+                  hp[25] / 1965.0 / hp[27], hp[26] / 1965.0 / hp[27]);
+        {
+          const char *on[8] = {"mul", "div", "max", "neg", "exp", "?", "?", "?"};
+          fprintf(stderr, "\n[veq prof] lane items (n, us/item incl. waits):");
+          for (int k = 0; k < 5; k++)
+            if (hp[128 + k]) fprintf(stderr, " %s n=%llu %.1f", on[k], hp[128 + k], hp[136 + k] / 1965.0 / hp[128 + k]);
+        }
+        fprintf(stderr, "\n[veq prof] timeline (per %u us: items, smem items, warps done):", bucket_us ? bucket_us : 400u);
         for (int k = 0; k < 32; k++)
           if (hp[32 + k] || hp[96 + k]) fprintf(stderr, " %d:%llu/%llu/%llu", k, hp[32 + k], hp[64 + k], hp[96 + k]);
         fprintf(stderr, "\n");
@@ -1002,6 +1042,19 @@ int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   unsigned long long nn[8] = {0};
   CK(cudaMemcpyAsync(nn, ctx->counters, 64, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  {
+    // -inf met inside a deferred expansion: repeat the run without deferral
+    // so faults are reported exactly where the reference raises them
+    int h = 0;
+    CK(cudaMemcpy(&h, ctx->error, sizeof(int), cudaMemcpyDeviceToHost));
+    if (h == E_DEFER && !bd->no_defer) {
+      CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), s));
+      bd->no_defer = true;
+      int r = veq_run_start(ctx, batch);
+      if (r) return r;
+      return veq_run_finish(ctx, batch, out);
+    }
+  }
   int er = check_error_flag(ctx);
   if (er) return er;
   if (nf > B.fault_cap) return fail(ctx, VEQ_E_BUDGET, "fault buffer overflow");

@@ -14,7 +14,9 @@
 //   max_nary   = max_of (expr.cpp:254-289)
 //
 // Work buffers come from a per-thread bump arena carved out of a global
-// scratch pool; one item's buffers die when the item completes.
+// scratch pool; one item's buffers die when the item completes (the lane's
+// current chunk is reused from offset 0 by its next item, so the pool only
+// grows when an item needs a larger chunk than any before it on that lane).
 #pragma once
 #include "veq_dev.cuh"
 
@@ -209,7 +211,7 @@ __device__ inline uint32_t finish_term(const Table &T, Arena &A, Rat c, const Te
 
 // Group like terms, drop zero coefficients, rebuild and add()
 // (canon_add_kids tail + rebuild, expr.cpp:402-424).
-__device__ inline uint32_t collect_terms(const Table &T, Arena &A, Term *ts, uint32_t n) {
+VEQ_NOINLINE uint32_t collect_terms(const Table &T, Arena &A, Term *ts, uint32_t n) {
   if (n == 0) return T.id_zero;
   uint32_t *idx = A.get<uint32_t>(n), *tmp = A.get<uint32_t>(n);
   if (!idx || !tmp) return T.id_zero;
@@ -241,7 +243,7 @@ __device__ inline uint32_t collect_terms(const Table &T, Arena &A, Term *ts, uin
 }
 
 // canon_add_kids over canonical leaves (expr.cpp:415-424).
-__device__ inline uint32_t add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
+VEQ_NOINLINE uint32_t add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
   uint32_t total = 0;
   for (uint32_t i = 0; i < n; i++) total += n_terms_of(T, leaves[i]);
   Term *ts = A.get<Term>(total ? total : 1);
@@ -276,7 +278,7 @@ __device__ inline uint32_t merge_exp_factors(const Table &T, Arena &A, uint32_t 
 }
 
 // canon_mul_kids over canonical operands (expr.cpp:426-481).
-__device__ inline uint32_t mul_canon(const Table &T, Arena &A, const uint32_t *ops, uint32_t n) {
+VEQ_NOINLINE uint32_t mul_canon(const Table &T, Arena &A, const uint32_t *ops, uint32_t n) {
   Rat coeff{1, 1};
   uint32_t nfac = 0, nsum = 0;
   for (uint32_t i = 0; i < n; i++) {
@@ -436,7 +438,7 @@ __device__ inline uint32_t split_coeff(const Table &T, Arena &A, uint32_t e, Rat
 }
 
 // canon_div (expr.cpp:543-559); den is not the literal 0 (checked by div()).
-__device__ inline uint32_t canon_div(const Table &T, Arena &A, uint32_t num, uint32_t den) {
+VEQ_NOINLINE uint32_t canon_div(const Table &T, Arena &A, uint32_t num, uint32_t den) {
   Node dn = ld_node(T, den);
   if (dn.kind == K_CONST) {
     uint32_t ops[2] = {intern_const(T, rat_div(T, Rat{1, 1}, const_val(dn))), num};
@@ -454,35 +456,82 @@ __device__ inline uint32_t canon_div(const Table &T, Arena &A, uint32_t num, uin
   return mul_canon(T, A, ops, 2);
 }
 
-// max_of over canonical leaves (expr.cpp:254-289).
-__device__ inline uint32_t max_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
-  uint32_t total = 0;
-  for (uint32_t i = 0; i < n; i++) {
-    Node k = ld_node(T, leaves[i]);
-    total += k.kind == K_MAX ? k.nkids : 1;
+// max_of over canonical leaves (expr.cpp:254-289): flatten Max kids, drop
+// -inf, sort, dedup by structure, keep only the largest Const. A Max leaf's
+// kids are already a sorted, duplicate-free run, so the result is a merge:
+// the loose leaves are sorted on their own, then every run is merged in with
+// binary-search insertion of the smaller side (the online-softmax chain
+// max(m_prev, s_0..s_63) costs ~64 log n compares instead of a full
+// n log n re-sort of m_prev's kids). Same result as sorting everything.
+__device__ inline int mx_cmp(const Table &T, uint32_t a, uint64_t pa, uint32_t b, uint64_t pb) {
+  return cmp_pref(T, pa, a, pb, b);
+}
+// first index in run[0..n) whose element is not less than x (lower bound)
+__device__ inline uint32_t mx_lower(const Table &T, const uint32_t *run, uint32_t n, uint32_t x, uint64_t px) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) / 2;
+    const uint32_t y = __ldcg(run + mid);
+    if (mx_cmp(T, y, prefix_id(T, y), x, px) < 0) lo = mid + 1;
+    else hi = mid;
   }
-  uint32_t *flat = A.get<uint32_t>(total ? total : 1);
-  if (!flat) return T.id_zero;
-  uint32_t m = 0;
+  return lo;
+}
+VEQ_NOINLINE uint32_t max_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
+  uint32_t total = 0, nloose = 0;
   for (uint32_t i = 0; i < n; i++) {
     Node k = ld_node(T, leaves[i]);
-    if (k.kind == K_MAX) {
-      for (uint32_t j = 0; j < k.nkids; j++) flat[m++] = ld_kid(T, k.p0 + j);
-    } else if (k.kind != K_NEGINF) {
-      flat[m++] = leaves[i];
+    if (k.kind == K_MAX) total += k.nkids;
+    else if (k.kind != K_NEGINF) {
+      total++;
+      nloose++;
     }
   }
-  if (m == 0) return T.id_neginf;
-  sort_canonical(T, A, flat, m);
-  uint32_t u = 0;
-  for (uint32_t i = 0; i < m; i++)
-    if (u == 0 || flat[u - 1] != flat[i]) flat[u++] = flat[i];
-  uint32_t nc = 0;
-  while (nc < u && ld_kind(T, flat[nc]) == K_CONST) nc++;
-  uint32_t start = nc > 1 ? nc - 1 : 0;
-  uint32_t cnt = u - start;
-  if (cnt == 1) return flat[start];
-  return intern(T, K_MAX, 0, 0, flat + start, cnt);
+  if (total == 0) return T.id_neginf;
+  uint32_t *cur = A.get<uint32_t>(total), *tmp = A.get<uint32_t>(total), *loose = A.get<uint32_t>(nloose ? nloose : 1);
+  if (!cur || !tmp || !loose) return T.id_zero;
+  uint32_t m = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    const uint8_t k = ld_kind(T, leaves[i]);
+    if (k != K_MAX && k != K_NEGINF) loose[m++] = leaves[i];
+  }
+  sort_canonical(T, A, loose, nloose);
+  uint32_t nc = 0;  // merged so far (in cur)
+  for (uint32_t i = 0; i < nloose; i++)
+    if (nc == 0 || cur[nc - 1] != loose[i]) cur[nc++] = loose[i];
+  for (uint32_t i = 0; i < n; i++) {
+    const Node k = ld_node(T, leaves[i]);
+    if (k.kind != K_MAX) continue;
+    // merge cur[0..nc) with the run kids[p0 .. p0 + nk): insert the smaller
+    // side into the larger by lower-bound searches, copying the gaps
+    const uint32_t *run = T.kids + k.p0;
+    const uint32_t nk = k.nkids;
+    const bool small_cur = nc <= nk;
+    const uint32_t *big = small_cur ? run : cur, *sml = small_cur ? cur : run;
+    const uint32_t nb = small_cur ? nk : nc, ns = small_cur ? nc : nk;
+    uint32_t o = 0, bpos = 0;
+    for (uint32_t j = 0; j < ns; j++) {
+      const uint32_t x = small_cur ? sml[j] : __ldcg(sml + j);
+      const uint64_t px = prefix_id(T, x);
+      const uint32_t lb = bpos + mx_lower(T, big + bpos, nb - bpos, x, px);
+      for (; bpos < lb; bpos++) tmp[o++] = small_cur ? __ldcg(big + bpos) : big[bpos];
+      // equal elements (same interned id) appear once
+      const bool dup = bpos < nb && (small_cur ? __ldcg(big + bpos) : big[bpos]) == x;
+      if (!dup) tmp[o++] = x;
+    }
+    for (; bpos < nb; bpos++) tmp[o++] = small_cur ? __ldcg(big + bpos) : big[bpos];
+    uint32_t *t = cur;
+    cur = tmp;
+    tmp = t;
+    nc = o;
+  }
+  // keep only the largest Const (Consts sort first)
+  uint32_t ncst = 0;
+  while (ncst < nc && ld_kind(T, cur[ncst]) == K_CONST) ncst++;
+  const uint32_t start = ncst > 1 ? ncst - 1 : 0;
+  const uint32_t cnt = nc - start;
+  if (cnt == 1) return cur[start];
+  return intern(T, K_MAX, 0, 0, cur + start, cnt);
 }
 
 }  // namespace veqd

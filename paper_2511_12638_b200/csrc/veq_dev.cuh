@@ -11,6 +11,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Heavy canonicalisation routines stay out-of-line: smaller kernels, much
+// shorter builds (static: one private copy per translation unit that uses it).
+#define VEQ_NOINLINE static __device__ __noinline__
+
 namespace veqd {
 
 // ctaeq::Kind order (expr.hpp:20): Const < NegInf < Var < Exp < Max < Div <

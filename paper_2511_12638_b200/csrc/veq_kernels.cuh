@@ -25,6 +25,12 @@ namespace cg = cooperative_groups;
 namespace veqd {
 
 constexpr uint8_t TS_RUN = 0, TS_BLOCK = 1, TS_RET = 2;
+// deferred scaling (k_mark_defer, eval_add_deferred)
+constexpr uint32_t USER_FINAL = 0xFFFFFFFEu;
+constexpr uint8_t DF_LEAF = 1, DF_SUM = 2, DF_CHAIN = 4;  // deferred product / deferred sum / chain expands leaves
+constexpr uint32_t DESC_DEFER = 1u << 16;                 // desc.w bit: the chain has deferred leaves
+constexpr int E_DEFER = 11;
+
 constexpr uint64_t UNSET64 = ~0ull;
 
 struct Batch {
@@ -64,6 +70,11 @@ struct Batch {
   uint32_t *ref_a, *ref_b, *st_step, *canon;
   uint32_t *chain_head, *chain_pos, *chain_len, *uses;
   uint8_t *continued;
+  // deferred scaling (k_mark_defer): the single consumer of a value used
+  // once (USER_FINAL: a final memory cell), and per statement DF_* flags
+  uint32_t *user;
+  uint8_t *defer;
+  uint32_t no_defer;  // 1: deferral disabled (VEQ_NO_DEFER, or the -inf fallback)
   unsigned long long *tup_key, *tup_val;
   unsigned long long *n_tup;
 
@@ -1572,7 +1583,10 @@ __global__ void k_resolve_finals(Batch B) {
   if (v == UNSET) return;
   v = chase(B, v);
   B.final_val[c] = v;
-  if (is_stmt_ref(v)) atomicAdd(B.uses + v, 1u);
+  if (is_stmt_ref(v)) {
+    atomicAdd(B.uses + v, 1u);
+    B.user[v] = USER_FINAL;
+  }
 }
 #endif
 
@@ -1617,13 +1631,23 @@ __global__ void k_resolve_all(Batch B, uint32_t *sz) {
       const uint32_t a = chase(B, B.ref_a[i]), b = chase(B, B.ref_b[i]);
       B.ref_a[i] = a;
       B.ref_b[i] = b;
-      if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
-      if (is_stmt_ref(b)) atomicAdd(B.uses + b, 1u);
+      // user[] is meaningful only where uses ends at 1 (a single writer)
+      if (is_stmt_ref(a)) {
+        atomicAdd(B.uses + a, 1u);
+        B.user[a] = (uint32_t)i;
+      }
+      if (is_stmt_ref(b)) {
+        atomicAdd(B.uses + b, 1u);
+        B.user[b] = (uint32_t)i;
+      }
       if ((st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX) && B.chain_head[i] == (uint32_t)i) v = B.chain_len[i] + 1;
     } else if (st.kind == VEQ_ST_UNOP) {
       const uint32_t a = chase(B, B.ref_a[i]);
       B.ref_a[i] = a;
-      if (is_stmt_ref(a)) atomicAdd(B.uses + a, 1u);
+      if (is_stmt_ref(a)) {
+        atomicAdd(B.uses + a, 1u);
+        B.user[a] = (uint32_t)i;
+      }
     } else if (st.kind == VEQ_ST_STORE || st.kind == VEQ_ST_LOAD) {
       B.ref_a[i] = chase(B, B.ref_a[i]);
     }
@@ -1633,8 +1657,53 @@ __global__ void k_resolve_all(Batch B, uint32_t *sz) {
 #endif
 
 
+// ---- deferred scaling ------------------------------------------------------
+// A product M = X * c whose only use is as a LEAF of a fused Add chain, where
+// X is the end of another fused Add chain used only by M, is never
+// canonicalised on its own: the consuming chain expands it into X's leaves,
+// each scaled by c (multiplied into any enclosing scale). canon_mul_kids
+// distributes a sum term by term and canon_add_kids merges term multisets
+// (proj/src/expr.cpp:415-481), and exp factors merge through the same
+// multiset sum, so sum_y canon(y * S) collected equals canon(canon(sum_y y) * S)
+// (SURVEY App. A.4): the canonical forms are unchanged, while the online-
+// softmax rescale `acc = acc_prev * c` (C4) stops re-distributing every
+// accumulated term once per key block. -inf anywhere in an expansion sets
+// E_DEFER and the run is repeated without deferral (exact fault reports).
+
+__device__ __forceinline__ bool is_add_chain_end(const Batch &B, uint32_t x) {
+  if (!is_stmt_ref(x) || B.st_step[x] == UNSET) return false;
+  const veq_stmt sx = B.stmts[x];
+  return sx.kind == VEQ_ST_BINOP && sx.op == VEQ_BIN_ADD && !B.continued[x];
+}
+
+#ifndef VEQ_TU_EVAL
+__global__ void k_mark_defer(Batch B) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts || B.no_defer || B.st_step[i] == UNSET) return;
+  const veq_stmt st = B.stmts[i];
+  if (st.kind != VEQ_ST_BINOP || st.op != VEQ_BIN_MUL || B.uses[i] != 1) return;
+  const uint32_t u = B.user[i];
+  if (u == USER_FINAL || u >= B.n_stmts) return;
+  const veq_stmt su = B.stmts[u];
+  if (su.kind != VEQ_ST_BINOP || su.op != VEQ_BIN_ADD) return;  // consumed as a chain leaf
+  const uint32_t a = B.ref_a[i], b = B.ref_b[i];
+  uint32_t X = UNSET;
+  if (is_add_chain_end(B, a) && B.uses[a] == 1 && B.user[a] == (uint32_t)i) X = a;
+  else if (is_add_chain_end(B, b) && B.uses[b] == 1 && B.user[b] == (uint32_t)i) X = b;
+  if (X == UNSET) return;
+  // flags of different statements share 32-bit words: set them atomically
+  auto set_flag = [&](uint32_t x, uint8_t f) {
+    atomicOr(reinterpret_cast<unsigned int *>(B.defer + (x & ~3u)), (unsigned)f << (8 * (x & 3u)));
+  };
+  set_flag((uint32_t)i, DF_LEAF);
+  set_flag(X, DF_SUM);
+  set_flag(B.chain_head[u], DF_CHAIN);
+}
+#endif
+
 // One pass after the log scan: chain-log entries and the work list (every
-// executed BinOp/UnOp except chain links absorbed by their successor).
+// executed BinOp/UnOp except chain links absorbed by their successor, and
+// deferred products and sums).
 #ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t *base, uint32_t *log,
                                                         uint32_t *log_stmt, unsigned long long *wkey, uint32_t *wval,
@@ -1664,6 +1733,7 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
       }
       if (B.continued[i] && B.uses[i] == 1) continue;  // absorbed by its successor
     }
+    if (B.defer[i] & (DF_LEAF | DF_SUM)) continue;  // expanded by the consuming chain
     mask |= 1u << k;
   }
   unsigned long long o = block_append<APP_NT>(n_work, __popc(mask));
@@ -1702,6 +1772,12 @@ struct EvalCtx {
   // path. (Half-warp pairing of small sums was removed in round 2, see
   // profiles/r02_pairing.md; lane-parallel runs replace it.)
   uint32_t off;
+  // memo of exp merges under deferred scales: key (exp node << 32 | scale
+  // node) -> merged factor (veq_api.cu sizes and clears it per run)
+  unsigned long long *mkeys;
+  uint32_t *mvals;
+  uint64_t mmask;
+  uint32_t bucket_us;  // VEQ_PROF timeline bucket width
 };
 
 __device__ inline void arith_fault(const Batch &B, uint32_t stmt, uint8_t detail) {
@@ -1724,7 +1800,7 @@ __device__ inline void arith_fault(const Batch &B, uint32_t stmt, uint8_t detail
   emit_fault(B, f);
 }
 
-__device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, const EvalCtx &E, uint32_t i) {
+VEQ_NOINLINE uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, const EvalCtx &E, uint32_t i) {
   const veq_stmt st = B.stmts[i];
   auto undef_of = [&](uint32_t s) { return intern_undef(T, 3, s >> 29, s); };
   if (st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX)) {
@@ -1827,6 +1903,7 @@ __global__ void k_make_desc(Batch B, EvalCtx E, const uint32_t *work, const unsi
   if (st.kind == VEQ_ST_BINOP && st.op == VEQ_BIN_ADD) {
     d.y = E.log_base[B.chain_head[i]];
     d.z = B.chain_pos[i] + 2;
+    if (B.defer[B.chain_head[i]] & DF_CHAIN) d.w |= DESC_DEFER;
   }
   desc[w] = d;
 }
@@ -1866,7 +1943,7 @@ void launch_eval_warp(uint32_t grid, uint32_t block, int smem, cudaStream_t s, c
 // One fused Add chain, whole warp (lg: the chain's first 32 log entries,
 // lane-indexed). Returns the canonical sum; `created` when this warp
 // published a new node (its fence already ran).
-__device__ inline uint32_t eval_add_warp(const Batch &B, const Table &T, const EvalCtx &E, Arena &A, WarpAlloc &W,
+VEQ_NOINLINE uint32_t eval_add_warp(const Batch &B, const Table &T, const EvalCtx &E, Arena &A, WarpAlloc &W,
                                          const SmemPool &SP, const uint4 d, const uint32_t lg, bool &created,
                                          int &path, unsigned long long *prof_lean, unsigned long long *prof_smem,
                                          unsigned long long &prof_pool, unsigned long long &prof_pages) {
@@ -1951,6 +2028,218 @@ __device__ inline uint32_t eval_add_warp(const Batch &B, const Table &T, const E
   return r;
 }
 
+// ---- deferred scaling: expansion of a chain with deferred leaves ----------
+// exp(a) * exp(s) -> exp(a + s) (merge_exp_factors, expr.cpp:371-391), memoised
+// per (exp, scale): the online-softmax terms of one row share their merged
+// exponents across every output column. Returns the merged factor (T.id_one
+// when the exponents cancel). The first lane to claim a key computes it;
+// others wait for the value.
+constexpr unsigned long long MEMO_EMPTY = ~0ull;
+VEQ_NOINLINE uint32_t merge_exp_pair(const Table &T, Arena &A, uint32_t e, uint32_t sc) {
+  const Node ne = ld_node(T, e), ns = ld_node(T, sc);
+  uint32_t args[2] = {ld_kid(T, ne.p0), ld_kid(T, ns.p0)};
+  const uint32_t arg = add_nary(T, A, args, 2);
+  return arg == T.id_zero ? T.id_one : intern(T, K_EXP, 0, 0, &arg, 1);
+}
+__device__ inline uint32_t memo_merge(const Table &T, const EvalCtx &E, Arena &A, uint32_t e, uint32_t sc) {
+  if (!E.mkeys) return merge_exp_pair(T, A, e, sc);
+  const unsigned long long key = ((unsigned long long)e << 32) | sc;
+  uint64_t h = mix64(key) & E.mmask;
+  for (uint64_t probes = 0; probes <= E.mmask; probes++, h = (h + 1) & E.mmask) {
+    unsigned long long k = *((volatile unsigned long long *)(E.mkeys + h));
+    if (k == MEMO_EMPTY) {
+      k = atomicCAS(E.mkeys + h, MEMO_EMPTY, key);
+      if (k == MEMO_EMPTY) {
+        const uint32_t v = merge_exp_pair(T, A, e, sc);
+        fence_acq_rel();
+        atomicExch(E.mvals + h, v);
+        return v;
+      }
+    }
+    if (k == key) {
+      volatile uint32_t *pv = E.mvals + h;
+      uint32_t v = *pv;
+      for (int spins = 0; v == UNSET; v = *pv)
+        if (++spins > 16) __nanosleep(64);
+      return v;
+    }
+  }
+  return merge_exp_pair(T, A, e, sc);  // table full: compute without the memo
+}
+
+// canon(y * sc) for canonical y and scale sc (canon_mul_kids, expr.cpp:426-481)
+// with a fast path for the common shapes: y an Exp, or a coefficient-free
+// product with one Exp factor, and sc an Exp.
+VEQ_NOINLINE uint32_t scaled_term(const Table &T, const EvalCtx &E, Arena &A, uint32_t y, uint32_t sc) {
+  if (sc == T.id_one) return y;
+  const Node ns = ld_node(T, sc), ny = ld_node(T, y);
+  if (ns.kind == K_EXP) {
+    if (ny.kind == K_EXP) return memo_merge(T, E, A, y, sc);
+    if (ny.kind == K_MUL && ny.nkids <= 8) {
+      uint32_t f[8];
+      int ex = -1, nexp = 0;
+      bool plain = true;
+      for (uint32_t k = 0; k < ny.nkids; k++) {
+        f[k] = ld_kid(T, ny.p0 + k);
+        const uint8_t kk = ld_kind(T, f[k]);
+        if (kk == K_EXP) {
+          ex = (int)k;
+          nexp++;
+        }
+        plain &= kk != K_CONST && kk != K_ADD && kk != K_MUL;
+      }
+      if (plain && nexp == 1) {
+        const uint32_t m = memo_merge(T, E, A, f[ex], sc);
+        uint32_t nf = 0, g[8];
+        for (uint32_t k = 0; k < ny.nkids; k++)
+          if ((int)k != ex) g[nf++] = f[k];
+        if (m != T.id_one) g[nf++] = m;
+        if (nf == 1) return g[0];
+        // canonical factor order (insertion sort on order prefixes)
+        uint64_t pk[8];
+        for (uint32_t k = 0; k < nf; k++) pk[k] = prefix_id(T, g[k]);
+        for (uint32_t k = 1; k < nf; k++) {
+          const uint32_t x = g[k];
+          const uint64_t px = pk[k];
+          int q = (int)k - 1;
+          while (q >= 0 && cmp_pref(T, px, x, pk[q], g[q]) < 0) {
+            g[q + 1] = g[q];
+            pk[q + 1] = pk[q];
+            q--;
+          }
+          g[q + 1] = x;
+          pk[q + 1] = px;
+        }
+        return intern(T, K_MUL, 0, 0, g, nf);
+      }
+    }
+  }
+  uint32_t ops[2] = {y, sc};
+  return mul_canon(T, A, ops, 2);
+}
+
+// One fused Add chain whose leaves include deferred products M = X * c: the
+// leaves are expanded (X's chain leaves, each under the scale c times the
+// enclosing scale, recursively), every leaf is scaled lane-parallel, and the
+// scaled terms are summed (canon_add_kids). Whole warp.
+VEQ_NOINLINE uint32_t eval_add_deferred(const Batch &B, const Table &T, const EvalCtx &E, Arena &A,
+                                             const uint4 d) {
+  const uint32_t lane = lane_id();
+  const long long c0 = E.prof ? clock64() : 0;
+  uint32_t cap = d.z * 8 + 1024;
+  uint32_t *ref = warp_get<uint32_t>(A, cap), *scl = warp_get<uint32_t>(A, cap);
+  if (!ref || !scl) return T.id_zero;
+  uint32_t total = 0;
+  // job stack (lane 0): (log base, leaf count, scale)
+  constexpr int MAXJ = 64;
+  uint32_t jb[MAXJ], jn[MAXJ], js[MAXJ];
+  int nj = 0;
+  if (lane == 0) {
+    jb[0] = d.y;
+    jn[0] = d.z;
+    js[0] = T.id_one;
+    nj = 1;
+  }
+  for (;;) {
+    nj = __shfl_sync(kFull, nj, 0);
+    if (nj == 0) break;
+    uint32_t base = 0, cnt = 0, scale = 0;
+    if (lane == 0) {
+      nj--;
+      base = jb[nj];
+      cnt = jn[nj];
+      scale = js[nj];
+    }
+    base = __shfl_sync(kFull, base, 0);
+    cnt = __shfl_sync(kFull, cnt, 0);
+    scale = __shfl_sync(kFull, scale, 0);
+    if (total + cnt > cap) {  // grow (bump arena; the old buffers die with the item)
+      uint32_t ncap = 2 * (total + cnt);
+      uint32_t *r2 = warp_get<uint32_t>(A, ncap), *s2 = warp_get<uint32_t>(A, ncap);
+      if (!r2 || !s2) return T.id_zero;
+      for (uint32_t k = lane; k < total; k += 32) {
+        r2[k] = ref[k];
+        s2[k] = scl[k];
+      }
+      ref = r2;
+      scl = s2;
+      cap = ncap;
+    }
+    for (uint32_t k = lane; k < cnt; k += 32) {
+      const uint32_t v = __ldg(E.log + base + k);
+      const bool dl = is_stmt_ref(v) && (B.defer[v] & DF_LEAF);
+      ref[total + k] = dl ? UNSET : v;
+      scl[total + k] = dl ? v : scale;  // a deferred product: its statement, expanded below
+    }
+    __syncwarp();
+    // deferred products among the new entries become jobs (lane 0)
+    if (lane == 0) {
+      for (uint32_t k = 0; k < cnt; k++) {
+        if (ref[total + k] != UNSET) continue;
+        const uint32_t M = scl[total + k];
+        const uint32_t a = B.ref_a[M], b = B.ref_b[M];
+        const bool xa = is_stmt_ref(a) && (B.defer[a] & DF_SUM);
+        const uint32_t X = xa ? a : b, c = xa ? b : a;
+        const uint32_t cn = wait_node(B, c);
+        uint32_t ns;
+        if (cn == T.id_neginf || scale == T.id_neginf) {
+          set_error(T, E_DEFER);
+          ns = T.id_one;
+        } else if (scale == T.id_one) {
+          ns = cn;
+        } else if (ld_kind(T, cn) == K_EXP && ld_kind(T, scale) == K_EXP) {
+          ns = memo_merge(T, E, A, cn, scale);
+        } else {
+          uint32_t ops[2] = {cn, scale};
+          ns = mul_canon(T, A, ops, 2);
+        }
+        if (nj >= MAXJ) {
+          set_error(T, E_DEFER);
+          break;
+        }
+        jb[nj] = E.log_base[B.chain_head[X]];
+        jn[nj] = B.chain_pos[X] + 2;
+        js[nj] = ns;
+        nj++;
+      }
+    }
+    total += cnt;
+    __syncwarp();
+  }
+  const long long c1 = E.prof ? clock64() : 0;
+  // scaled terms, lane-parallel; removed entries (expanded products) drop out
+  uint32_t *out = warp_get<uint32_t>(A, total ? total : 1);
+  if (!out) return T.id_zero;
+  uint32_t m = 0;
+  for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    uint32_t t = UNSET;
+    if (k < total && ref[k] != UNSET) {
+      const uint32_t y = wait_node(B, ref[k]);
+      if (y == T.id_neginf) {
+        set_error(T, E_DEFER);
+        t = T.id_zero;
+      } else {
+        t = scaled_term(T, E, A, y, scl[k]);
+      }
+    }
+    const uint32_t has = __ballot_sync(kFull, t != UNSET);
+    if (t != UNSET) out[m + __popc(has & ((1u << lane) - 1))] = t;
+    m += __popc(has);
+  }
+  __syncwarp();
+  const long long c2 = E.prof ? clock64() : 0;
+  uint32_t r = warp_add_small(T, out, m);
+  if (r == UNSET) r = warp_add_nary(T, A, out, m);
+  if (E.prof && lane == 0) {  // [24..27]: expand, scaled terms, sum cycles; items
+    atomicAdd(E.prof + 24, (unsigned long long)(c1 - c0));
+    atomicAdd(E.prof + 25, (unsigned long long)(c2 - c1));
+    atomicAdd(E.prof + 26, (unsigned long long)(clock64() - c2));
+    atomicAdd(E.prof + 27, 1ull);
+  }
+  return r;
+}
+
 __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
                                                              const unsigned long long *n_work_dev,
                                                              unsigned long long *cursor, char *pool,
@@ -1983,7 +2272,7 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
   auto tbucket = [&]() -> uint32_t {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    const unsigned long long bk = (t - t_k0) / 400000;
+    const unsigned long long bk = (t - t_k0) / (1000ull * E.bucket_us);
     return (uint32_t)(bk < 31 ? bk : 31);
   };
   unsigned long long w0 = ((unsigned long long)wib * gridDim.x + blockIdx.x) * G;
@@ -1999,15 +2288,19 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
         const uint4 d = make_uint4(__shfl_sync(kFull, dl.x, j), __shfl_sync(kFull, dl.y, j),
                                    __shfl_sync(kFull, dl.z, j), __shfl_sync(kFull, dl.w, j));
         const uint32_t lg = lane < d.z ? __ldg(E.log + d.y + lane) : UNSET;
-        const uint64_t mark = A.used;
-        char *const mbase = A.base;
         A.item = d.x;
         const long long t0 = E.prof ? clock64() : 0;
         bool created = false;
         int path = 0;
-        const uint32_t r = eval_add_warp(B, T, E, A, W, SP, d, lg, created, path, E.prof ? prof_lean : nullptr,
-                                         E.prof ? prof_smem : nullptr, prof_pool, prof_pages);
-        if (A.base == mbase) A.used = mark;  // every lane recycles its own arena
+        uint32_t r;
+        if (d.w & DESC_DEFER) {
+          r = eval_add_deferred(B, T, E, A, d);
+          path = 4;
+        } else {
+          r = eval_add_warp(B, T, E, A, W, SP, d, lg, created, path, E.prof ? prof_lean : nullptr,
+                            E.prof ? prof_smem : nullptr, prof_pool, prof_pages);
+        }
+        A.used = 0;  // items are independent: each lane reuses its current chunk
         if (lane == 0) {
           // a node this warp created was fenced before its slot was claimed;
           // anything else needs the fence for cumulativity
@@ -2029,18 +2322,23 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
       const uint32_t k = above ? (uint32_t)(__ffs(above) - 1) : cnt;
       if (lane >= j && lane < k) {
         const uint32_t i = dl.x;
-        const uint64_t mark = A.used;
-        char *const mbase = A.base;
         A.item = i;
         const long long t0 = E.prof ? clock64() : 0;
         const uint32_t r = eval_stmt(B, T, A, E, i);
-        if (A.base == mbase) A.used = mark;
+        A.used = 0;
         fence_acq_rel();
         atomicExch(B.canon + i, r);
         if (E.prof) {
-          prof_work[0] += clock64() - t0;
+          const long long dt = clock64() - t0;
+          prof_work[0] += dt;
           prof_n[0]++;
           atomicAdd(E.prof + 32 + tbucket(), 1ull);
+          // per operation: mul div max | neg exp (slots 128.., cycles 136..)
+          const uint32_t kind = dl.w & 0xff, op = (dl.w >> 8) & 0xff;
+          const uint32_t slot = kind == VEQ_ST_BINOP ? (op == VEQ_BIN_MUL ? 0 : op == VEQ_BIN_DIV ? 1 : 2)
+                                                     : (op == VEQ_UN_NEG ? 3 : 4);
+          atomicAdd(E.prof + 128 + slot, 1ull);
+          atomicAdd(E.prof + 136 + slot, (unsigned long long)dt);
         }
       }
       __syncwarp();
