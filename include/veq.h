@@ -251,6 +251,81 @@ int veq_run(veq_ctx *ctx, uint32_t batch, veq_run_out *out);
 int veq_run_start(veq_ctx *ctx, uint32_t batch);
 int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out);
 
+/* ---- options -----------------------------------------------------------
+ * VEQ_OPT_KEEP_REGS (0/1): runs started afterwards keep every thread's final
+ * register file and canonicalise its values (veq_fetch_regs): the Final
+ * outcome's register files (ctaeq::Outcome::regs, symexec.hpp:155-156)
+ * that outcome_key and run()-level tests compare. Off by default: the
+ * check pipeline only needs Out arrays (pipeline.cpp:214-220). */
+enum { VEQ_OPT_KEEP_REGS = 1 };
+int veq_set_option(veq_ctx *ctx, int option, int value);
+/* Final register file of thread `tid` of program `prog`: canonical node per
+ * thread-local register id (~0: never assigned); *n_regs = register count
+ * (call with out_nodes NULL to size). Requires VEQ_OPT_KEEP_REGS at run. */
+int veq_fetch_regs(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t tid, uint32_t *out_nodes, uint32_t n,
+                   uint32_t *n_regs);
+
+/* ---- run reports (ctaeq::RunResult, proj/include/ctaeq/symexec.hpp:214-225)
+ * veq_run_report assembles one program's RunResult from the raw device
+ * faults the way the reference's Collector does (symexec.cpp:308-328):
+ * races and safety faults in execution order (step, then check order inside
+ * a statement), de-duplicated by their identity without step numbers; the
+ * deadlock report with every thread's final state and the first conflicting
+ * pair (make_deadlock_report, symexec.cpp:335-365); and the outcome by
+ * precedence race > safety > deadlock > final (symexec.cpp:838-845).
+ * Statements are batch-global indices; the caller maps them to source
+ * locations and register ids to names. Identity uses the per-statement
+ * location keys given by veq_batch_locs (default: the statement index).
+ * Output is ctx-owned, valid until the next veq_run_report on the batch. */
+enum { VEQ_OUT_FINAL = 0, VEQ_OUT_RACE = 1, VEQ_OUT_DEADLOCK = 2, VEQ_OUT_SAFETY = 3 }; /* Outcome::Kind */
+enum { VEQ_TS_RUNNABLE = 0, VEQ_TS_BLOCKED = 1, VEQ_TS_RETURNED = 2 };
+typedef struct veq_access {
+  uint32_t tid, stmt;
+  uint64_t step;
+  uint32_t is_write, pad;
+} veq_access;
+typedef struct veq_race_report {
+  uint32_t arr;      /* program-local array index */
+  int32_t offset;
+  veq_access first;  /* the access recorded in the event context */
+  veq_access second; /* the access whose check failed */
+} veq_race_report;
+typedef struct veq_safety_report {
+  uint32_t kind;     /* VEQ_SAFE_* */
+  uint32_t tid, stmt, detail;
+  uint64_t step;
+  uint32_t has_addr, arr;
+  int32_t offset;
+  uint32_t reg;      /* thread-local register id (register kinds), else ~0 */
+  uint32_t is_store; /* out-of-bounds: write side */
+  uint32_t pad;
+} veq_safety_report;
+typedef struct veq_thread_report {
+  uint32_t state;    /* VEQ_TS_* */
+  uint32_t set;      /* blocked: sync-set id (veq_set_members), else ~0 */
+  uint32_t stmt;     /* blocked: the Sync statement, else ~0 */
+  uint32_t pad;
+} veq_thread_report;
+typedef struct veq_report {
+  uint32_t outcome;  /* VEQ_OUT_* */
+  uint32_t releases;
+  uint64_t steps;
+  uint64_t n_races;
+  const veq_race_report *races;
+  uint64_t n_safeties;
+  const veq_safety_report *safeties;
+  uint32_t deadlocked;
+  uint32_t n_threads; /* thread reports (deadlocked runs only) */
+  const veq_thread_report *threads;
+  int32_t conflict_a, conflict_b; /* -1: none */
+  uint32_t conflict_set_a, conflict_set_b;
+} veq_report;
+int veq_batch_locs(veq_ctx *ctx, uint32_t batch, const uint64_t *loc_keys); /* [n_stmts] or NULL */
+int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out);
+/* Members (program-local tids, ascending) of a sync-set id of a report. */
+int veq_set_members(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t set, uint32_t *tids, uint32_t cap,
+                    uint32_t *n);
+
 /* Final shared-memory contents after veq_run (the Final payload of
  * ctaeq::Outcome, symexec.hpp:155): canonical term node of each cell of
  * program `prog`'s array `array` (program-local index), or 0xFFFFFFFF when
@@ -300,6 +375,29 @@ int veq_compare_progs(veq_ctx *ctx, uint32_t batch_a, uint32_t prog_a0, uint32_t
                       uint32_t n_pairs, const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
                       uint32_t n_out_per_pair, veq_vc_out *out);
 
+/* ---- slow path of the verdict API (ctaeq::eq, proj/src/decide.cpp:728-859)
+ * For a VC whose canonical forms differ: d = canon(f - g) on the device; if
+ * d is 0, or the exp-polynomial normal form of d's rationalized numerator
+ * vanishes with every Max an opaque atom, the VC is equal; otherwise the
+ * rigorous random witness search (MPFR intervals, libmpfr.so.6 loaded at run
+ * time; same trials, seed and sampling as refute_random) looks for a
+ * separating rational point: not-equal with the witness, else unknown with
+ * the reference's reason text. A difference that still contains Max after
+ * the opaque pass would need the max case split (split_max), which is not
+ * restated: VEQ_UNDECIDED. Output strings are ctx-owned (next veq_decide). */
+enum { VEQ_EQUAL = 0, VEQ_NOT_EQUAL = 1, VEQ_UNKNOWN = 2, VEQ_UNDECIDED = 3 };
+typedef struct veq_decision {
+  uint32_t kind;            /* VEQ_EQUAL .. VEQ_UNDECIDED (ctaeq::VerdictKind + undecided) */
+  uint32_t precision;       /* witness: MPFR precision that separated                     */
+  const char *reason;       /* unknown / undecided                                         */
+  uint32_t n_assign;        /* witness assignment, variable-name order                     */
+  const char *const *names;
+  const char *const *values;
+  const char *f_enclosure;  /* "[lo, hi]" as the reference prints it                       */
+  const char *g_enclosure;
+} veq_decision;
+int veq_decide(veq_ctx *ctx, uint32_t node_f, uint32_t node_g, uint64_t seed, uint64_t trials, veq_decision *out);
+
 /* ---- DAG export (host to_string / slow path / reports) -----------------
  * Exports the sub-DAG reachable from roots in canonical kid order. Nodes are
  * renumbered densely 0..n-1 in post-order (kids first); root_index maps each
@@ -335,11 +433,32 @@ int veq_render(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, const char *
  * without materialising them (digest comparison of very large forms). */
 int veq_render_digest(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, uint32_t *crc32, uint64_t *len);
 
-/* ---- multi-GPU ---------------------------------------------------------
- * Verdict counters are combined across ranks by the caller's collective
- * (torch.distributed / NCCL all-reduce); the ctx exposes them as a small
- * device-side vector so no host round trip is needed per rank. */
-int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]); /* equal, vcs, faults, missing */
+/* ---- multi-GPU (one ctx per GPU, NCCL over NVLink / NVSwitch) ----------
+ * CTA pairs, output elements and variants shard across GPUs with no data
+ * exchange; each GPU keeps its own term table. The one exchange is the
+ * verdict combine below. Rank 0 makes a unique id (veq_comm_unique_id, 128
+ * bytes), the caller broadcasts it (any channel), every rank calls
+ * veq_comm_init. NCCL is loaded at run time (libnccl.so.2). */
+int veq_comm_unique_id(void *id_out);
+int veq_comm_init(veq_ctx *ctx, const void *nccl_unique_id, int nranks, int rank);
+typedef struct veq_combined {
+  uint64_t totals[4];            /* summed over ranks: equal, vcs, faults, missing */
+  uint64_t first_fail;           /* min over ranks of the caller's first failing global VC index */
+  uint32_t n_ranks, pad;
+  const uint64_t *rank_vc_off;   /* [n_ranks + 1]: rank r's VCs are verdict[off[r] .. off[r+1]) */
+  const uint8_t *verdict;        /* per VC: 1 canonical forms equal                     */
+  const uint64_t *rank_sc_off;   /* [n_ranks + 1]                                        */
+  const uint64_t *sc_hash;       /* side-condition denominators: 64-bit Merkle hash      */
+  const uint8_t *sc_discharged;
+} veq_combined;
+/* Called by every rank after its compare: all-reduce of the counters and of
+ * the first failing index, all-gather of per-VC verdict bytes and
+ * side-condition (hash, discharged) pairs in rank order (ctx-owned output,
+ * valid until the next combine), so any rank can aggregate the report
+ * (pipeline.cpp:245-266). Without veq_comm_init: this rank's own results. */
+int veq_comm_combine(veq_ctx *ctx, uint64_t first_fail_local, veq_combined *out);
+/* This ctx's counters of the last compare / run: equal, vcs, faults, missing. */
+int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]);
 
 #ifdef __cplusplus
 }

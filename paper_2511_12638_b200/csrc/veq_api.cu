@@ -1,6 +1,8 @@
 // veq_api.cu — C-ABI implementation (include/veq.h): device memory,
 // batch preparation and the launch sequence of one check.
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <functional>
 
@@ -9,11 +11,14 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
+#include <tuple>
 #include <unordered_map>
 #include <string>
 #include <vector>
 
 #include "veq_kernels.cuh"
+#include "host/decide.hpp"
 
 using namespace veqd;
 
@@ -47,6 +52,7 @@ struct BatchDev {
   bool started = false;                   // veq_run_start enqueued, veq_run_finish pending
   bool timing_run = false;                // phase events recorded by this run
   bool no_defer = false;                  // deferral off for this batch (set after an E_DEFER fallback)
+  bool keep_regs = false;                 // this batch's runs keep final register files
   uint32_t run_launches = 0;
   unsigned long long n_work_last = 0;  // work items of the last run (read back with its results)
   uint32_t n_threads = 0;
@@ -59,6 +65,14 @@ struct BatchDev {
   // host-visible run results
   std::vector<veq_prog_result> res;
   std::vector<veq_fault> faults;
+  std::vector<uint64_t> prog_fault_off;   // faults sorted by (prog, step, sub): program p's are [off[p], off[p+1])
+  std::vector<uint64_t> locs;             // optional per-statement location keys (veq_batch_locs)
+  std::vector<veq_syncset> syncsets;      // host copies for reports (set membership)
+  std::vector<uint64_t> set_words;
+  // veq_run_report output of the last call
+  std::vector<veq_race_report> rep_races;
+  std::vector<veq_safety_report> rep_safeties;
+  std::vector<veq_thread_report> rep_threads;
   std::vector<uint8_t> th_state;
   std::vector<uint32_t> th_bset;
   std::vector<uint64_t> th_bstmt;
@@ -125,6 +139,18 @@ struct veq_ctx {
   unsigned long long *mkeys = nullptr;
   uint32_t *mvals = nullptr;
   uint64_t mslots = 0;
+  bool keep_regs = false;  // VEQ_OPT_KEEP_REGS for runs started from now on
+  // multi-GPU: NCCL communicator (veq_comm_init) and veq_comm_combine output
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  std::vector<uint8_t> all_verdict;
+  std::vector<uint64_t> all_sc_hash;
+  std::vector<uint8_t> all_sc_dis;
+  std::vector<uint64_t> rank_vc_off, rank_sc_off;
+  // veq_decide output
+  std::string dec_reason, dec_f, dec_g;
+  std::vector<std::string> dec_names, dec_values;
+  std::vector<const char *> dec_name_p, dec_value_p;
   // veq_render output
   std::string render_text;
   std::vector<uint64_t> render_offs;
@@ -206,7 +232,51 @@ int check_error_flag(veq_ctx *ctx) {
   return VEQ_OK;
 }
 
+// NCCL is resolved at run time (dlopen of libnccl.so.2): a process that
+// already loaded one (e.g. PyTorch's) shares it, and the library still loads
+// on hosts without NCCL (veq_comm_* then report VEQ_E_UNSUPPORTED).
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi &nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+    a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.AllGather && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
 }  // namespace
+
+static void veq_comm_destroy_(veq_ctx *ctx) {
+  if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+  ctx->comm = nullptr;
+  ctx->nranks = 1;
+  ctx->rank = 0;
+}
+
+#define NK(call)                                                                                      \
+  do {                                                                                                \
+    ncclResult_t r_ = (call);                                                                         \
+    if (r_ != ncclSuccess) return fail(ctx, VEQ_E_CUDA, std::string(#call ": ") + nccl().GetErrorString(r_)); \
+  } while (0)
 
 extern "C" {
 
@@ -305,6 +375,7 @@ void veq_close(veq_ctx *ctx) {
   cudaFree(ctx->pool_used);
   cudaFree(ctx->mkeys);
   cudaFree(ctx->mvals);
+  if (ctx->comm) veq_comm_destroy_(ctx);
   cudaFree(ctx->in_base);
   cudaFree(ctx->in_size);
   cudaFree(ctx->in_cache);
@@ -550,6 +621,8 @@ static int load_impl(veq_ctx *ctx, const veq_batch_desc *d, veq_stmt *dev_stmts,
     return fail(ctx, VEQ_E_UNSUPPORTED, "more than 2^32 checked memory cells in one batch");
   }
   bd->arr_cell_base = cell_base;
+  bd->syncsets.assign(d->syncsets, d->syncsets + NS);
+  bd->set_words.assign(d->set_words, d->set_words + d->n_set_words);
   bd->n_cells = cells;
   bd->n_regs = reg_off[Tn];
   // programs laid out in order (thread and statement ranges contiguous)
@@ -760,6 +833,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   {
     static const bool env_off = getenv("VEQ_NO_DEFER") && getenv("VEQ_NO_DEFER")[0] == '1';
     B.no_defer = (env_off || bd->no_defer) ? 1u : 0u;
+    B.keep_regs = ctx->keep_regs ? 1u : 0u;
+    bd->keep_regs = ctx->keep_regs;
   }
   // the tuple buffer holds every checked access; slots of accesses that
   // never execute (deadlock) keep key ~0 and sort last, so the sort needs no
@@ -869,6 +944,7 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     LAUNCH(k_resolve_all<<<blocks(S, 256), 256, 0, s>>>(B, sz));
   }
   if (bd->n_cells) LAUNCH(k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
+  if (B.keep_regs && bd->n_regs) LAUNCH(k_resolve_regs<<<blocks(bd->n_regs, 256), 256, 0, s>>>(B, bd->n_regs));
   // deferred scaling: products of a used-once sum feeding a chain (k_mark_defer)
   if (S && !B.no_defer) LAUNCH(k_mark_defer<<<blocks(S, 256), 256, 0, s>>>(B));
   PH1(VEQ_PH_RESOLVE);
@@ -1096,6 +1172,16 @@ int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
     bd->res[p].deadlocked = dead[p];
   }
   for (const veq_fault &f : bd->faults) bd->res[f.prog].n_faults++;
+  // reference order within a program: execution order (step, then the
+  // order of checks inside one statement); programs grouped
+  std::stable_sort(bd->faults.begin(), bd->faults.end(), [](const veq_fault &a, const veq_fault &b) {
+    if (a.prog != b.prog) return a.prog < b.prog;
+    if (a.step != b.step) return a.step < b.step;
+    return a.sub < b.sub;
+  });
+  bd->prog_fault_off.assign(P + 1, 0);
+  for (const veq_fault &f : bd->faults) bd->prog_fault_off[f.prog + 1]++;
+  for (uint32_t p = 0; p < P; p++) bd->prog_fault_off[p + 1] += bd->prog_fault_off[p];
   bd->ran = true;
   ctx->last_faults = nf;
   if (out) {
@@ -1662,6 +1748,407 @@ int veq_instantiate(veq_ctx *ctx, uint32_t tmpl, uint32_t n_inst, const int32_t 
   bd.syncsets = t.syncsets.data();
   bd.set_words = t.set_words.data();
   return load_impl(ctx, &bd, ds, out);
+}
+
+int veq_set_option(veq_ctx *ctx, int option, int value) {
+  if (!ctx) return VEQ_E_ARG;
+  switch (option) {
+  case VEQ_OPT_KEEP_REGS: ctx->keep_regs = value != 0; return VEQ_OK;
+  default: return fail(ctx, VEQ_E_ARG, "unknown option");
+  }
+}
+
+int veq_fetch_regs(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t tid, uint32_t *out_nodes, uint32_t n,
+                   uint32_t *n_regs) {
+  if (!ctx || !live_batch(ctx, batch) || !n_regs) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  if (!bd->ran || prog >= bd->progs.size() || tid >= bd->progs[prog].n_threads) return VEQ_E_ARG;
+  if (!bd->keep_regs) return fail(ctx, VEQ_E_ARG, "veq_fetch_regs: run without VEQ_OPT_KEEP_REGS");
+  const uint32_t g = bd->progs[prog].thread_off + tid;
+  uint64_t off[2];
+  CK(cudaMemcpy(off, bd->B.reg_off + g, 16, cudaMemcpyDeviceToHost));
+  const uint32_t nr = (uint32_t)(off[1] - off[0]);
+  *n_regs = nr;
+  if (!out_nodes) return VEQ_OK;
+  std::vector<uint32_t> v(nr);
+  if (nr) CK(cudaMemcpy(v.data(), bd->B.regfile + off[0], nr * 4, cudaMemcpyDeviceToHost));
+  for (uint32_t k = 0; k < nr && k < n; k++) {
+    uint32_t x = v[k];
+    if (x == UNSET) {
+      out_nodes[k] = UNSET;
+    } else if (x & REF_NODE) {
+      out_nodes[k] = x & ~REF_NODE;
+    } else {
+      CK(cudaMemcpy(&out_nodes[k], bd->B.canon + x, 4, cudaMemcpyDeviceToHost));
+    }
+  }
+  return VEQ_OK;
+}
+
+int veq_batch_locs(veq_ctx *ctx, uint32_t batch, const uint64_t *loc_keys) {
+  if (!ctx || !live_batch(ctx, batch)) return VEQ_E_ARG;
+  BatchDev *bd = ctx->batches[batch];
+  if (loc_keys) bd->locs.assign(loc_keys, loc_keys + bd->n_stmts);
+  else bd->locs.clear();
+  return VEQ_OK;
+}
+
+static bool set_has(const BatchDev *bd, uint32_t set, uint32_t n_threads, uint32_t tid) {
+  if (set >= bd->syncsets.size()) return tid < n_threads;  // the program's full set
+  const veq_syncset &q = bd->syncsets[set];
+  if (q.full) return tid < n_threads;
+  if (tid < q.lo || tid >= q.lo + q.n_bits) return false;
+  const uint32_t k = tid - q.lo;
+  return (bd->set_words[q.word_off + k / 64] >> (k % 64)) & 1ull;
+}
+
+int veq_set_members(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t set, uint32_t *tids, uint32_t cap,
+                    uint32_t *n) {
+  if (!ctx || !live_batch(ctx, batch) || !n) return VEQ_E_ARG;
+  BatchDev *bd = ctx->batches[batch];
+  if (prog >= bd->progs.size()) return VEQ_E_ARG;
+  const uint32_t T = bd->progs[prog].n_threads;
+  uint32_t k = 0;
+  for (uint32_t t = 0; t < T; t++)
+    if (set_has(bd, set, T, t)) {
+      if (tids && k < cap) tids[k] = t;
+      k++;
+    }
+  *n = k;
+  return VEQ_OK;
+}
+
+int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out) {
+  if (!ctx || !live_batch(ctx, batch) || !out) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  if (!bd->ran || prog >= bd->progs.size()) return fail(ctx, VEQ_E_ARG, "veq_run_report: no finished run / bad program");
+  const veq_program_meta &pm = bd->progs[prog];
+  auto loc = [&](uint32_t stmt) -> uint64_t { return bd->locs.empty() ? stmt : bd->locs[stmt]; };
+  const uint64_t f0 = bd->prog_fault_off[prog], f1 = bd->prog_fault_off[prog + 1];
+  // statements of safety faults (register operands), fetched once
+  std::map<uint32_t, veq_stmt> st;
+  for (uint64_t k = f0; k < f1; k++)
+    if (bd->faults[k].type == VEQ_FAULT_SAFETY) st.emplace(bd->faults[k].stmt, veq_stmt{});
+  for (auto &[i, v] : st) CK(cudaMemcpy(&v, bd->B.stmts + i, sizeof(veq_stmt), cudaMemcpyDeviceToHost));
+  bd->rep_races.clear();
+  bd->rep_safeties.clear();
+  bd->rep_threads.clear();
+  // Collector (proj/src/symexec.cpp:308-328): distinct reports in order of
+  // first occurrence; identity excludes step numbers
+  std::set<std::tuple<uint32_t, int32_t, uint32_t, uint32_t, uint64_t, uint32_t, uint32_t, uint64_t>> rkeys;
+  std::set<std::tuple<uint32_t, uint32_t, uint64_t, uint32_t, int32_t, uint32_t, uint32_t, uint32_t>> skeys;
+  for (uint64_t k = f0; k < f1; k++) {
+    const veq_fault &f = bd->faults[k];
+    if (f.type == VEQ_FAULT_RACE) {
+      veq_race_report r{};
+      r.arr = f.arr;
+      r.offset = f.offset;
+      r.first = veq_access{f.tid2, f.stmt2, f.step2, f.is_write2, 0};
+      r.second = veq_access{f.tid, f.stmt, f.step, f.is_write, 0};
+      if (rkeys.emplace(r.arr, r.offset, f.tid2, (uint32_t)f.is_write2, loc(f.stmt2), f.tid, (uint32_t)f.is_write,
+                        loc(f.stmt)).second)
+        bd->rep_races.push_back(r);
+      continue;
+    }
+    veq_safety_report s{};
+    s.kind = f.kind;
+    s.tid = f.tid;
+    s.stmt = f.stmt;
+    s.step = f.step;
+    s.detail = f.detail;
+    s.reg = UNSET;
+    const veq_stmt &x = st[f.stmt];
+    if (f.kind == VEQ_SAFE_UNINIT_REG) {
+      s.reg = f.reg_slot == 1 ? x.b : (x.kind == VEQ_ST_STORE ? x.dst : x.a);
+    } else if (f.kind == VEQ_SAFE_UNINIT_MEM || f.kind == VEQ_SAFE_OOB) {
+      s.has_addr = 1;
+      s.arr = f.arr;
+      s.offset = f.offset;
+      s.is_store = f.kind == VEQ_SAFE_OOB ? f.is_write : 0;
+    } else {
+      s.reg = x.dst;  // invalid arithmetic: the destination register
+    }
+    if (skeys.emplace(s.kind, s.tid, loc(s.stmt), s.has_addr ? s.arr : s.reg, s.has_addr ? s.offset : 0, s.is_store,
+                      s.detail, s.has_addr).second)
+      bd->rep_safeties.push_back(s);
+  }
+  const veq_prog_result &pr = bd->res[prog];
+  out->steps = pr.steps;
+  out->releases = pr.releases;
+  out->deadlocked = pr.deadlocked;
+  out->conflict_a = out->conflict_b = -1;
+  out->conflict_set_a = out->conflict_set_b = UNSET;
+  out->n_threads = 0;
+  if (pr.deadlocked && !bd->th_state.empty()) {
+    // make_deadlock_report (symexec.cpp:335-365): every thread's state; the
+    // first a < b blocked on different sets with a, b in both sets
+    const uint32_t T = pm.n_threads, g0 = pm.thread_off;
+    for (uint32_t t = 0; t < T; t++) {
+      const uint8_t sv = bd->th_state[g0 + t];
+      bd->rep_threads.push_back(veq_thread_report{sv, sv == TS_BLOCK ? bd->th_bset[g0 + t] : UNSET,
+                                                  sv == TS_BLOCK ? (uint32_t)bd->th_bstmt[g0 + t] : UNSET, 0});
+    }
+    for (uint32_t a = 0; a < T && out->conflict_a < 0; a++) {
+      if (bd->rep_threads[a].state != TS_BLOCK) continue;
+      const uint32_t ia = bd->rep_threads[a].set;
+      for (uint32_t b = a + 1; b < T; b++) {
+        if (bd->rep_threads[b].state != TS_BLOCK) continue;
+        const uint32_t ib = bd->rep_threads[b].set;
+        if (ia == ib) continue;  // canonical set ids: equal content <=> equal id
+        if (set_has(bd, ia, T, a) && set_has(bd, ia, T, b) && set_has(bd, ib, T, a) && set_has(bd, ib, T, b)) {
+          out->conflict_a = (int32_t)a;
+          out->conflict_b = (int32_t)b;
+          out->conflict_set_a = ia;
+          out->conflict_set_b = ib;
+          break;
+        }
+      }
+    }
+    out->n_threads = T;
+  }
+  out->n_races = bd->rep_races.size();
+  out->races = bd->rep_races.data();
+  out->n_safeties = bd->rep_safeties.size();
+  out->safeties = bd->rep_safeties.data();
+  out->threads = bd->rep_threads.data();
+  // precedence (symexec.cpp:838-845): race, else safety, else deadlock, else final
+  out->outcome = !bd->rep_races.empty() ? VEQ_OUT_RACE
+                 : !bd->rep_safeties.empty() ? VEQ_OUT_SAFETY
+                 : pr.deadlocked ? VEQ_OUT_DEADLOCK : VEQ_OUT_FINAL;
+  return VEQ_OK;
+}
+
+int veq_comm_unique_id(void *id_out) {
+  if (!id_out) return VEQ_E_ARG;
+  if (!nccl().ok) return VEQ_E_UNSUPPORTED;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return VEQ_E_CUDA;
+  memcpy(id_out, &id, sizeof(id));
+  return VEQ_OK;
+}
+
+int veq_comm_init(veq_ctx *ctx, const void *nccl_unique_id, int nranks, int rank) {
+  if (!ctx || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return VEQ_E_ARG;
+  if (!nccl().ok) return fail(ctx, VEQ_E_UNSUPPORTED, "libnccl.so.2 not available");
+  CK(cudaSetDevice(ctx->device));
+  veq_comm_destroy_(ctx);
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  NK(nccl().CommInitRank(&ctx->comm, nranks, id, rank));
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return VEQ_OK;
+}
+
+// The one exchange of a sharded check: every rank calls it
+// after its veq_compare / veq_compare_progs. Sum all-reduce of the verdict
+// counters, min all-reduce of the first failing VC index, and all-gather of
+// every rank's per-VC verdict bytes and side-condition (Merkle hash,
+// discharged) pairs in rank order, so any rank can aggregate the report as
+// check_equivalence does (proj/src/pipeline.cpp:245-266). Without a
+// communicator it returns this rank's own results.
+int veq_comm_combine(veq_ctx *ctx, uint64_t first_fail_local, veq_combined *out) {
+  if (!ctx || !out) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const uint64_t nv = ctx->vcs.size(), ns = ctx->sc_node.size();
+  // this rank's verdict bytes and side-condition hashes
+  std::vector<uint8_t> verd(nv);
+  for (uint64_t i = 0; i < nv; i++) verd[i] = ctx->vcs[i].equal ? 1 : 0;
+  std::vector<uint64_t> hs(ns);
+  for (uint64_t i = 0; i < ns; i++)
+    CK(cudaMemcpy(&hs[i], reinterpret_cast<const char *>(ctx->nodes + ctx->sc_node[i]) + 8, 8, cudaMemcpyDeviceToHost));
+  const int R = ctx->comm ? ctx->nranks : 1;
+  std::vector<unsigned long long> h(6 * (size_t)R, 0);
+  unsigned long long mine[6] = {ctx->last_equal, ctx->last_vcs, ctx->last_faults, ctx->last_missing,
+                                (unsigned long long)nv, (unsigned long long)ns};
+  ctx->rank_vc_off.assign(R + 1, 0);
+  ctx->rank_sc_off.assign(R + 1, 0);
+  unsigned long long first = first_fail_local;
+  if (!ctx->comm) {
+    for (int k = 0; k < 6; k++) h[k] = mine[k];
+  } else {
+    // sizes and counters of every rank, then the min first-failing index
+    unsigned long long *d = nullptr;
+    if (cudaMallocAsync(&d, (6 + 6 * (size_t)R + 1) * 8, s) != cudaSuccess) return fail(ctx, VEQ_E_OOM, "comm");
+    CK(cudaMemcpyAsync(d, mine, 48, cudaMemcpyHostToDevice, s));
+    NK(nccl().AllGather(d, d + 6, 6, ncclUint64, ctx->comm, s));
+    CK(cudaMemcpyAsync(d + 6 + 6 * R, &first, 8, cudaMemcpyHostToDevice, s));
+    NK(nccl().AllReduce(d + 6 + 6 * R, d + 6 + 6 * R, 1, ncclUint64, ncclMin, ctx->comm, s));
+    CK(cudaMemcpyAsync(h.data(), d + 6, 6 * R * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&first, d + 6 + 6 * R, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaFreeAsync(d, s));
+  }
+  uint64_t maxv = 0, maxs = 0;
+  for (int r = 0; r < R; r++) {
+    ctx->rank_vc_off[r + 1] = ctx->rank_vc_off[r] + h[6 * r + 4];
+    ctx->rank_sc_off[r + 1] = ctx->rank_sc_off[r] + h[6 * r + 5];
+    maxv = std::max<uint64_t>(maxv, h[6 * r + 4]);
+    maxs = std::max<uint64_t>(maxs, h[6 * r + 5]);
+  }
+  ctx->all_verdict.assign(ctx->rank_vc_off[R], 0);
+  ctx->all_sc_hash.assign(ctx->rank_sc_off[R], 0);
+  ctx->all_sc_dis.assign(ctx->rank_sc_off[R], 0);
+  if (!ctx->comm) {
+    std::copy(verd.begin(), verd.end(), ctx->all_verdict.begin());
+    std::copy(hs.begin(), hs.end(), ctx->all_sc_hash.begin());
+    std::copy(ctx->sc_dis.begin(), ctx->sc_dis.end(), ctx->all_sc_dis.begin());
+  } else if (maxv || maxs) {
+    // equal-size all-gathers of padded per-rank buffers (verdict bytes,
+    // hashes, discharged bytes), compacted to rank order on the host
+    const uint64_t rec = maxv + maxs * 9;
+    char *d = nullptr;
+    if (cudaMallocAsync(&d, rec * (R + 1) + 8, s) != cudaSuccess) return fail(ctx, VEQ_E_OOM, "comm");
+    std::vector<char> me(rec, 0);
+    memcpy(me.data(), verd.data(), nv);
+    memcpy(me.data() + maxv, hs.data(), ns * 8);
+    memcpy(me.data() + maxv + maxs * 8, ctx->sc_dis.data(), ns);
+    CK(cudaMemcpyAsync(d, me.data(), rec, cudaMemcpyHostToDevice, s));
+    NK(nccl().AllGather(d, d + rec, rec, ncclChar, ctx->comm, s));
+    std::vector<char> all(rec * R);
+    CK(cudaMemcpyAsync(all.data(), d + rec, rec * R, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaFreeAsync(d, s));
+    for (int r = 0; r < R; r++) {
+      const char *b = all.data() + rec * r;
+      const uint64_t v0 = ctx->rank_vc_off[r], s0 = ctx->rank_sc_off[r];
+      memcpy(ctx->all_verdict.data() + v0, b, h[6 * r + 4]);
+      memcpy(ctx->all_sc_hash.data() + s0, b + maxv, h[6 * r + 5] * 8);
+      memcpy(ctx->all_sc_dis.data() + s0, b + maxv + maxs * 8, h[6 * r + 5]);
+    }
+  }
+  for (int k = 0; k < 4; k++) {
+    out->totals[k] = 0;
+    for (int r = 0; r < R; r++) out->totals[k] += h[6 * r + k];
+  }
+  out->first_fail = first;
+  out->n_ranks = (uint32_t)R;
+  out->rank_vc_off = ctx->rank_vc_off.data();
+  out->verdict = ctx->all_verdict.data();
+  out->rank_sc_off = ctx->rank_sc_off.data();
+  out->sc_hash = ctx->all_sc_hash.data();
+  out->sc_discharged = ctx->all_sc_dis.data();
+  return VEQ_OK;
+}
+
+int veq_decide(veq_ctx *ctx, uint32_t f, uint32_t g, uint64_t seed, uint64_t trials, veq_decision *out) {
+  if (!ctx || !out) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  using veqdec::DecideError;
+  veqdec::Result res;
+  ctx->dec_reason.clear();
+  auto finish = [&](veqdec::Kind k) {
+    out->kind = k == veqdec::Kind::Equal ? VEQ_EQUAL : k == veqdec::Kind::NotEqual ? VEQ_NOT_EQUAL : VEQ_UNKNOWN;
+    ctx->dec_reason = res.reason;
+    ctx->dec_f = res.f_enclosure;
+    ctx->dec_g = res.g_enclosure;
+    ctx->dec_names.clear();
+    ctx->dec_values.clear();
+    for (auto &[n, v] : res.assignment) {
+      ctx->dec_names.push_back(n);
+      ctx->dec_values.push_back(v);
+    }
+    ctx->dec_name_p.clear();
+    ctx->dec_value_p.clear();
+    for (size_t i = 0; i < ctx->dec_names.size(); i++) {
+      ctx->dec_name_p.push_back(ctx->dec_names[i].c_str());
+      ctx->dec_value_p.push_back(ctx->dec_values[i].c_str());
+    }
+    out->reason = ctx->dec_reason.c_str();
+    out->n_assign = (uint32_t)ctx->dec_names.size();
+    out->names = ctx->dec_name_p.data();
+    out->values = ctx->dec_value_p.data();
+    out->f_enclosure = ctx->dec_f.c_str();
+    out->g_enclosure = ctx->dec_g.c_str();
+    out->precision = res.precision;
+    return VEQ_OK;
+  };
+  if (f == g) return finish(veqdec::Kind::Equal);
+  // d = canon(f - g) on the device (decide.cpp:779-787)
+  uint32_t *dd = nullptr;
+  { int r_ = ws_get(ctx, 27, (void **)&dd, 16); if (r_) return r_; }
+  CK(cudaMemsetAsync(ctx->pool_used, 0, 8, s));
+  k_canon_sub<<<1, 32, 0, s>>>(ctx->T, f, g, dd, ctx->pool, ctx->pool_used, ctx->pool_cap);
+  CK(cudaGetLastError());
+  uint32_t d = 0;
+  CK(cudaMemcpyAsync(&d, dd, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (int er = check_error_flag(ctx)) return er;
+  // the three DAGs on the host
+  veqdec::Dag dag;
+  std::vector<uint32_t> roots{f, g};
+  const bool have_d = d != ~0u && d != ~1u;
+  if (have_d) roots.push_back(d);
+  else res.reason = std::string("cannot form the difference: -inf is not a valid operand of ") + (d == ~0u ? "Neg" : "Add");
+  {
+    veq_dag_buf buf{};
+    if (int r = veq_export_dag(ctx, roots.data(), roots.size(), &buf)) return r;
+    std::vector<veq_dag_node> nodes(buf.n_nodes);
+    std::vector<uint32_t> kids(buf.n_kids), ridx(roots.size());
+    buf.cap_nodes = buf.n_nodes;
+    buf.cap_kids = buf.n_kids;
+    buf.nodes = nodes.data();
+    buf.kids = kids.data();
+    buf.root_index = ridx.data();
+    if (int r = veq_export_dag(ctx, roots.data(), roots.size(), &buf)) return r;
+    dag.nodes.resize(nodes.size());
+    for (size_t i = 0; i < nodes.size(); i++) {
+      const veq_dag_node &n = nodes[i];
+      veqdec::DNode &o = dag.nodes[i];
+      o.kind = (uint8_t)n.kind;
+      o.num = n.num;
+      o.den = n.den;
+      for (uint32_t k = 0; k < n.nkids; k++) o.kids.push_back(kids[n.kid_off + k]);
+      if (n.kind == VEQ_K_VAR) {
+        char hx[32];
+        snprintf(hx, sizeof hx, "%llx", (unsigned long long)n.var_index);
+        o.name = n.var_input >= 0 ? ctx->input_names[n.var_input] + "_" + std::to_string(n.var_index)
+                                  : std::string("!undef<") + hx + ">";
+      }
+    }
+    f = ridx[0];
+    g = ridx[1];
+    if (have_d) d = ridx[2];
+  }
+  if (have_d) {
+    const veqdec::DNode &dn = dag.nodes[d];
+    if (dn.kind == VEQ_K_CONST && dn.num == 0) return finish(veqdec::Kind::Equal);
+    // opaque-max pass: Max subtrees are atoms (decide.cpp:789-813)
+    const bool has_max = veqdec::contains_max(dag, d);
+    bool opaque_done = false;
+    try {
+      if (veqdec::zero_by_exp_poly(dag, d)) return finish(veqdec::Kind::Equal);
+      opaque_done = true;
+      if (!has_max) res.reason = "difference is a nonzero exp-polynomial";
+    } catch (const DecideError &e) {
+      res.reason = e.what();
+    }
+    if (has_max && (opaque_done || res.reason.empty())) {
+      // the full max case split (split_max, decide.cpp:677-681) is not
+      // restated: such VCs stay undecided rather than guessed
+      res.reason = "max case analysis not available";
+      out->kind = VEQ_UNDECIDED;
+      ctx->dec_reason = res.reason;
+      out->reason = ctx->dec_reason.c_str();
+      out->n_assign = 0;
+      out->precision = 0;
+      return VEQ_OK;
+    }
+  }
+  // no proof of equality: a rigorous separating point (refute_random)
+  if (!veqdec::mpfr_available()) return fail(ctx, VEQ_E_UNSUPPORTED, "libmpfr.so.6 not available for witnesses");
+  try {
+    if (veqdec::refute_random(dag, f, g, trials, seed, res)) return finish(veqdec::Kind::NotEqual);
+  } catch (const DecideError &e) {
+    res.reason = e.what();
+  }
+  if (res.reason.empty()) res.reason = "no decision within budget";
+  res.reason += "; no separating point found in " + std::to_string(trials) + " trials";
+  return finish(veqdec::Kind::Unknown);
 }
 
 int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]) {

@@ -75,6 +75,7 @@ struct Batch {
   uint32_t *user;
   uint8_t *defer;
   uint32_t no_defer;  // 1: deferral disabled (VEQ_NO_DEFER, or the -inf fallback)
+  uint32_t keep_regs; // 1: final register files are kept and canonicalised (veq_fetch_regs)
   unsigned long long *tup_key, *tup_val;
   unsigned long long *n_tup;
 
@@ -1123,6 +1124,11 @@ __global__ void k_exec(Batch B, Table T) {
       }
     }
   }
+  // the Final register file (Outcome::regs, symexec.hpp:155-156) when asked
+  if (B.keep_regs && regs == lregs) {
+    uint32_t *out = B.regfile + B.reg_off[g];
+    for (uint32_t k = 0; k < nregs && k < LREG; k++) out[k] = lregs[k];
+  }
 }
 #endif
 
@@ -1590,6 +1596,23 @@ __global__ void k_resolve_finals(Batch B) {
 }
 #endif
 
+
+// Final registers count as uses (and are never deferred) when kept: every
+// register value is canonicalised like a final memory cell.
+#ifndef VEQ_TU_EVAL
+__global__ void k_resolve_regs(Batch B, uint64_t n_regs) {
+  const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_regs) return;
+  uint32_t v = B.regfile[k];
+  if (v == UNSET) return;
+  v = chase(B, v);
+  B.regfile[k] = v;
+  if (is_stmt_ref(v)) {
+    atomicAdd(B.uses + v, 1u);
+    B.user[v] = USER_FINAL;
+  }
+}
+#endif
 
 // Input symbols read by direct loads (never-stored input arrays) are
 // interned in one parallel pass before execution; the executors read the
@@ -2369,6 +2392,37 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
 #endif  // VEQ_TU_EVAL
 
 #ifndef VEQ_TU_EVAL
+// canon(a - b) for the verdict API's slow path (decide.cpp:779-787):
+// canon_add_kids(a, canon_mul_kids(-1, b)). out[0] = node, or ~0 / ~1 when
+// b / a is -inf (sub() raises on Neg / Add respectively).
+#ifndef VEQ_TU_EVAL
+__global__ void k_canon_sub(Table T, uint32_t a, uint32_t b, uint32_t *out, char *pool,
+                            unsigned long long *pool_used, uint64_t pool_cap) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (b == T.id_neginf) {
+    out[0] = ~0u;
+    return;
+  }
+  if (a == T.id_neginf) {
+    out[0] = ~1u;
+    return;
+  }
+  Arena A{pool, pool_used, pool_cap, &T, nullptr, 0, 0, 1ull << 20, 0};
+  const Node nb = ld_node(T, b);
+  uint32_t mb;
+  if (nb.kind == K_CONST) {
+    Rat v = const_val(nb);
+    v.n = -v.n;
+    mb = intern_const(T, v);
+  } else {
+    uint32_t ops[2] = {T.id_mone, b};
+    mb = mul_canon(T, A, ops, 2);
+  }
+  uint32_t leaves[2] = {a, mb};
+  out[0] = add_nary(T, A, leaves, 2);
+}
+#endif
+
 __global__ void k_final_nodes(Batch B) {
   uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= B.n_cells) return;

@@ -84,13 +84,15 @@ class RunResult:
     deadlock: Optional[Deadlock]
     outcome: str
     shared: Dict[str, str] = field(default_factory=dict)       # addr -> to_string (Final only)
+    regs: List[Dict[str, str]] = field(default_factory=list)   # per thread: register -> to_string (keep_regs)
     cell_nodes: Dict[Tuple[int, int], int] = field(default_factory=dict)  # (array idx, offset) -> node
 
 
 class Session:
     """One veq_ctx: a term table on one GPU plus its loaded batches."""
 
-    def __init__(self, device: int = 0, max_nodes: int = 0, max_kid_words: int = 0, scratch_bytes: int = 0):
+    def __init__(self, device: int = 0, max_nodes: int = 0, max_kid_words: int = 0, scratch_bytes: int = 0,
+                 keep_regs: bool = False):
         L = N.lib()
         lim = N.veq_limits(max_nodes, max_kid_words, scratch_bytes)
         h = C.c_void_p()
@@ -98,6 +100,9 @@ class Session:
         if st != 0:
             raise N.VeqError(st, L.veq_strerror(st).decode())
         self.ctx = h
+        self.keep_regs = keep_regs
+        if keep_regs:
+            _check(self.ctx, L.veq_set_option(self.ctx, N.OPT_KEEP_REGS, 1))
         self.inputs: List[Tuple[str, int]] = []
         self._batches: List[Optional[Batch]] = []
         self._templates: List[Batch] = []
@@ -199,6 +204,32 @@ class Session:
         out = N.veq_vc_out()
         _check(self.ctx, N.lib().veq_compare(self.ctx, ba, bb, A, B, n, C.byref(out)))
         return out
+
+    def decide(self, f: int, g: int, seed: int, trials: int = 64) -> dict:
+        """The verdict API's slow path for one VC (veq_decide): the reference
+        eq() result as report_to_json renders a VC (verdict, witness or
+        reason)."""
+        out = N.veq_decision()
+        _check(self.ctx, N.lib().veq_decide(self.ctx, f, g, seed, trials, C.byref(out)))
+        v = {"verdict": N.VERDICT_KIND[out.kind]}
+        if out.kind == 1:
+            v["witness"] = {"assignment": {out.names[i].decode(): out.values[i].decode() for i in range(out.n_assign)},
+                            "f": out.f_enclosure.decode(), "g": out.g_enclosure.decode(),
+                            "precision": int(out.precision)}
+        elif out.kind in (2, 3):
+            v["reason"] = out.reason.decode()
+        return v
+
+    def fetch_regs(self, bid: int, prog: int, tid: int) -> np.ndarray:
+        """Final register file of one thread (canonical node per register
+        id, UNSET = never assigned); needs keep_regs."""
+        L = N.lib()
+        n = C.c_uint32()
+        _check(self.ctx, L.veq_fetch_regs(self.ctx, bid, prog, tid, None, 0, C.byref(n)))
+        out = np.empty(max(1, n.value), dtype=np.uint32)
+        _check(self.ctx, L.veq_fetch_regs(self.ctx, bid, prog, tid, out.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                          n.value, C.byref(n)))
+        return out[:n.value]
 
     def fetch_cells(self, bid: int, prog: int, array: int, n: int) -> np.ndarray:
         out = np.empty(max(n, 1), dtype=np.uint32)
@@ -304,95 +335,75 @@ def render(nodes, kids, roots: List[int], inputs: Sequence[Tuple[str, int]]) -> 
     return [pr(r, 0) for r in roots]
 
 
-def _set_tids(b: Batch, s: int, n_threads: int) -> List[int]:
-    if s >= len(b.syncsets):  # the device's full-set id (veq.h: n_syncsets)
-        return list(range(n_threads))
-    q = b.syncsets[s]
-    if q["full"]:
-        return list(range(n_threads))
-    out = []
-    for k in range(int(q["n_bits"])):
-        if (int(b.set_words[int(q["word_off"]) + k // 64]) >> (k % 64)) & 1:
-            out.append(int(q["lo"]) + k)
-    return out
+def _set_tids(sess: "Session", bid: int, p: int, s: int) -> List[int]:
+    L = N.lib()
+    n = C.c_uint32()
+    _check(sess.ctx, L.veq_set_members(sess.ctx, bid, p, s, None, 0, C.byref(n)))
+    buf = (C.c_uint32 * max(1, n.value))()
+    _check(sess.ctx, L.veq_set_members(sess.ctx, bid, p, s, buf, n.value, C.byref(n)))
+    return [buf[i] for i in range(n.value)]
+
+
+def _locs_key(b: Batch) -> np.ndarray:
+    """Per-statement location keys (line << 32 | col) for report identity."""
+    if b.locs is None or len(b.locs) == 0:
+        return None
+    return (b.locs["line"].astype(np.uint64) << np.uint64(32)) | b.locs["col"].astype(np.uint64)
 
 
 def build_results(sess: Session, bid: int, b: Batch, out: N.veq_run_out, with_shared: bool) -> List[RunResult]:
-    nf = out.n_faults
-    faults = np.ctypeslib.as_array(out.faults, shape=(nf,)).copy() if nf else []
-    per_prog: Dict[int, list] = {}
-    for f in faults:
-        per_prog.setdefault(int(f["prog"]), []).append(f)
+    """RunResult per program from the C-ABI's assembled reports
+    (veq_run_report: Collector order and identity, deadlock conflict pair,
+    outcome precedence); this layer maps statements to source locations and
+    register ids to names."""
+    L = N.lib()
+    keys = _locs_key(b)
+    if keys is not None:
+        keys = np.ascontiguousarray(keys)
+        _check(sess.ctx, L.veq_batch_locs(sess.ctx, bid, keys.ctypes.data_as(C.POINTER(C.c_uint64))))
     results = []
-    T = out.n_threads_total
-    th_state = np.ctypeslib.as_array(out.thread_state, shape=(T,)).copy() if T else np.zeros(0, np.uint8)
-    th_set = np.ctypeslib.as_array(out.thread_block_set, shape=(T,)).copy() if T else np.zeros(0, np.uint32)
-    th_stmt = np.ctypeslib.as_array(out.thread_block_stmt, shape=(T,)).copy() if T else np.zeros(0, np.uint64)
+    kinds = {N.OUT_FINAL: "final", N.OUT_RACE: "race", N.OUT_DEADLOCK: "deadlock", N.OUT_SAFETY: "safety"}
     for p in range(out.n_progs):
-        pr = out.progs[p]
         pm = b.progs[p]
         t_off, a_off = int(pm["thread_off"]), int(pm["array_off"])
         nthr = int(pm["n_threads"])
         aname = lambda a: b.array_names[a_off + int(a)]
-        fl = sorted(per_prog.get(p, []), key=lambda f: (int(f["step"]), int(f["sub"])))
+        rep = N.veq_report()
+        _check(sess.ctx, L.veq_run_report(sess.ctx, bid, p, C.byref(rep)))
         races, safeties = [], []
-        rkeys, skeys = set(), set()
-        for f in fl:
-            stmt = int(f["stmt"])
-            if f["type"] == N.FAULT_RACE:
-                first = Access(int(f["tid2"]), "write" if f["is_write2"] else "read", b.loc(int(f["stmt2"])),
-                               int(f["step2"]))
-                second = Access(int(f["tid"]), "write" if f["is_write"] else "read", b.loc(stmt), int(f["step"]))
-                r = Race(aname(f["arr"]), int(f["offset"]), first, second)
-                key = (r.array, r.offset, first.tid, first.access, first.loc, second.tid, second.access, second.loc)
-                if key not in rkeys:
-                    rkeys.add(key)
-                    races.append(r)
+        for k in range(rep.n_races):
+            r = rep.races[k]
+            acc = lambda x: Access(int(x.tid), "write" if x.is_write else "read", b.loc(int(x.stmt)), int(x.step))
+            races.append(Race(aname(r.arr), int(r.offset), acc(r.first), acc(r.second)))
+        for k in range(rep.n_safeties):
+            f = rep.safeties[k]
+            kind = int(f.kind)
+            s = Safety(SAFETY_KIND[kind], int(f.tid), b.loc(int(f.stmt)), step=int(f.step))
+            if f.has_addr:
+                s.array, s.offset = aname(f.arr), int(f.offset)
+                s.is_store = bool(f.is_store)
             else:
-                kind = int(f["kind"])
-                st = b.stmts[stmt]
-                gt = t_off + int(f["tid"])
-                s = Safety(SAFETY_KIND[kind], int(f["tid"]), b.loc(stmt), step=int(f["step"]))
-                if kind == N.SAFE_UNINIT_REG:
-                    reg = int(st["b"]) if f["reg_slot"] == 1 else (int(st["dst"]) if st["kind"] == N.ST_STORE
-                                                                     else int(st["a"]))
-                    s.reg = b.reg_name(gt, reg)
-                elif kind in (N.SAFE_UNINIT_MEM, N.SAFE_OOB):
-                    s.array, s.offset = aname(f["arr"]), int(f["offset"])
-                    s.is_store = bool(f["is_write"]) if kind == N.SAFE_OOB else False
-                else:
-                    s.reg = b.reg_name(gt, int(st["dst"]))
-                    s.detail = DETAIL[int(f["detail"])]
-                key = (s.kind, s.tid, s.loc, (s.array, s.offset) if s.array is not None else s.reg, s.is_store,
-                       s.detail)
-                if key not in skeys:
-                    skeys.add(key)
-                    safeties.append(s)
+                s.reg = b.reg_name(t_off + int(f.tid), int(f.reg))
+            s.detail = DETAIL[int(f.detail)]
+            safeties.append(s)
         dl = None
-        if pr.deadlocked:
+        if rep.deadlocked:
             threads = []
-            for t in range(nthr):
-                g = t_off + t
-                state = {0: "runnable", 1: "blocked", 2: "returned"}[int(th_state[g])]
+            for t in range(rep.n_threads):
+                th = rep.threads[t]
+                state = {N.TS_RUNNABLE: "runnable", N.TS_BLOCKED: "blocked", N.TS_RETURNED: "returned"}[int(th.state)]
                 tj = {"tid": t, "state": state}
                 if state == "blocked":
-                    tj["waiting"] = _set_tids(b, int(th_set[g]), nthr)
-                    tj["loc"] = b.loc(int(th_stmt[g]))
+                    tj["waiting"] = _set_tids(sess, bid, p, int(th.set))
+                    tj["loc"] = b.loc(int(th.stmt))
                 threads.append(tj)
             dl = Deadlock(threads)
-            for a in range(nthr):
-                if threads[a]["state"] != "blocked" or dl.conflict_tids:
-                    continue
-                for c in range(a + 1, nthr):
-                    if threads[c]["state"] != "blocked":
-                        continue
-                    ia, ic = set(threads[a]["waiting"]), set(threads[c]["waiting"])
-                    if ia != ic and a in ia and a in ic and c in ia and c in ic:
-                        dl.conflict_tids = (a, c)
-                        dl.conflict_sets = (sorted(ia), sorted(ic))
-                        break
-        outcome = "race" if races else ("safety" if safeties else ("deadlock" if dl else "final"))
-        rr = RunResult(int(pr.steps), int(pr.releases), races, safeties, dl, outcome)
+            if rep.conflict_a >= 0:
+                dl.conflict_tids = (int(rep.conflict_a), int(rep.conflict_b))
+                dl.conflict_sets = (_set_tids(sess, bid, p, int(rep.conflict_set_a)),
+                                    _set_tids(sess, bid, p, int(rep.conflict_set_b)))
+        outcome = kinds[int(rep.outcome)]
+        rr = RunResult(int(rep.steps), int(rep.releases), races, safeties, dl, outcome)
         if outcome == "final" and with_shared:
             cells: List[Tuple[str, int, int]] = []
             input_cells: List[Tuple[str, str]] = []
@@ -411,5 +422,14 @@ def build_results(sess: Session, bid: int, b: Batch, out: N.veq_run_out, with_sh
                 rr.shared[f"{an}[{i}]"] = s
             for k, v in input_cells:
                 rr.shared[k] = v
+            if sess.keep_regs:
+                per, roots = [], []
+                for t in range(nthr):
+                    nodes = sess.fetch_regs(bid, p, t)
+                    names = [(b.reg_name(t_off + t, k), int(x)) for k, x in enumerate(nodes) if x != N.UNSET]
+                    per.append(names)
+                    roots += [x for _, x in names]
+                strs = iter(sess.to_strings(roots))
+                rr.regs = [{nm: next(strs) for nm, _ in names} for names in per]
         results.append(rr)
     return results

@@ -82,6 +82,50 @@ class veq_run_out(C.Structure):
                 ("n_launches", u32), ("n_phases", u32), ("phase_ms", C.c_float * 9)]
 
 
+class veq_access(C.Structure):
+    _fields_ = [("tid", u32), ("stmt", u32), ("step", u64), ("is_write", u32), ("pad", u32)]
+
+
+class veq_race_report(C.Structure):
+    _fields_ = [("arr", u32), ("offset", i32), ("first", veq_access), ("second", veq_access)]
+
+
+class veq_safety_report(C.Structure):
+    _fields_ = [("kind", u32), ("tid", u32), ("stmt", u32), ("detail", u32), ("step", u64), ("has_addr", u32),
+                ("arr", u32), ("offset", i32), ("reg", u32), ("is_store", u32), ("pad", u32)]
+
+
+class veq_thread_report(C.Structure):
+    _fields_ = [("state", u32), ("set", u32), ("stmt", u32), ("pad", u32)]
+
+
+class veq_report(C.Structure):
+    _fields_ = [("outcome", u32), ("releases", u32), ("steps", u64), ("n_races", u64),
+                ("races", P(veq_race_report)), ("n_safeties", u64), ("safeties", P(veq_safety_report)),
+                ("deadlocked", u32), ("n_threads", u32), ("threads", P(veq_thread_report)),
+                ("conflict_a", i32), ("conflict_b", i32), ("conflict_set_a", u32), ("conflict_set_b", u32)]
+
+
+OUT_FINAL, OUT_RACE, OUT_DEADLOCK, OUT_SAFETY = range(4)
+TS_RUNNABLE, TS_BLOCKED, TS_RETURNED = range(3)
+OPT_KEEP_REGS = 1
+
+
+class veq_combined(C.Structure):
+    _fields_ = [("totals", u64 * 4), ("first_fail", u64), ("n_ranks", u32), ("pad", u32),
+                ("rank_vc_off", P(u64)), ("verdict", P(u8)), ("rank_sc_off", P(u64)), ("sc_hash", P(u64)),
+                ("sc_discharged", P(u8))]
+
+
+class veq_decision(C.Structure):
+    _fields_ = [("kind", u32), ("precision", u32), ("reason", C.c_char_p), ("n_assign", u32),
+                ("names", P(C.c_char_p)), ("values", P(C.c_char_p)), ("f_enclosure", C.c_char_p),
+                ("g_enclosure", C.c_char_p)]
+
+
+VERDICT_KIND = ["equal", "not_equal", "unknown", "undecided"]
+
+
 class veq_vc(C.Structure):
     _fields_ = [("node_a", u32), ("node_b", u32), ("equal", u32), ("sc_off", u32), ("sc_n", u32), ("pad", u32)]
 
@@ -146,6 +190,15 @@ def lib() -> C.CDLL:
     L.veq_drop_template.argtypes = [vp, u32]
     L.veq_render.argtypes = [vp, P(u32), C.c_size_t, P(C.c_char_p), P(P(u64))]
     L.veq_render_digest.argtypes = [vp, P(u32), C.c_size_t, P(u32), P(u64)]
+    L.veq_batch_locs.argtypes = [vp, u32, P(u64)]
+    L.veq_run_report.argtypes = [vp, u32, u32, P(veq_report)]
+    L.veq_set_members.argtypes = [vp, u32, u32, u32, P(u32), u32, P(u32)]
+    L.veq_set_option.argtypes = [vp, C.c_int, C.c_int]
+    L.veq_fetch_regs.argtypes = [vp, u32, u32, u32, P(u32), u32, P(u32)]
+    L.veq_comm_unique_id.argtypes = [C.c_char_p]
+    L.veq_comm_init.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
+    L.veq_comm_combine.argtypes = [vp, u64, P(veq_combined)]
+    L.veq_decide.argtypes = [vp, u32, u32, u64, u64, P(veq_decision)]
     for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_run_start", "veq_run_finish",
               "veq_fetch_cells", "veq_compare", "veq_compare_progs",
               "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
@@ -157,5 +210,7 @@ def lib() -> C.CDLL:
 EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_declare_inputs", "veq_load_batch",
             "veq_run", "veq_run_start", "veq_run_finish", "veq_fetch_cells", "veq_compare", "veq_compare_progs", "veq_export_dag", "veq_verdict_counters",
             "veq_set_timing", "veq_clear_terms", "veq_stream", "veq_drop_batch", "veq_load_template",
-            "veq_instantiate", "veq_drop_template", "veq_render", "veq_render_digest"]
+            "veq_instantiate", "veq_drop_template", "veq_render", "veq_render_digest", "veq_batch_locs",
+            "veq_run_report", "veq_set_members", "veq_set_option", "veq_fetch_regs", "veq_comm_unique_id",
+            "veq_comm_init", "veq_comm_combine", "veq_decide"]
 PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]

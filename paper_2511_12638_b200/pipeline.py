@@ -8,9 +8,14 @@ with their race/safety/deadlock payloads (harvest_errors, missing_output,
 pipeline.cpp:62-87, 185-212), per-VC verdicts and the side-condition union
 de-duplicated in VC order (pipeline.cpp:245-265).
 
-Decision scope: the canonical fast path (decide.cpp:765-768). A VC whose
-canonical forms differ is reported as "undecided" — the exp-polynomial slow
-path and the MPFR witness search stay with the reference host code.
+Decision: the canonical fast path on the device (decide.cpp:765-768); a VC
+whose canonical forms differ goes to the slow path (veq_decide: canonical
+difference on the device, exp-polynomial zero test with opaque Max atoms,
+MPFR witness search — decide.cpp:728-859), seeded with fnv1a of
+"array[index]" as pipeline.cpp:18-25, 226 does. `report_to_json` renders a
+report in the reference's JSON schema (pipeline.cpp:305-381, timings
+omitted). The one verdict the reference cannot produce is "undecided": a VC
+whose difference still needs the max case split (not restated).
 """
 from __future__ import annotations
 
@@ -87,7 +92,16 @@ def _failed(rr: RunResult) -> bool:
     return not (rr.outcome == "final" and not rr.races and not rr.safeties)
 
 
-def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: bool = True) -> List[PairReport]:
+def fnv1a(text: str) -> int:
+    """The VC seed of check_equivalence (pipeline.cpp:18-25)."""
+    h = 14695981039346656037
+    for c in text.encode():
+        h = ((h ^ c) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: bool = True, slow_path: bool = True,
+                  trials: int = 64) -> List[PairReport]:
     ba = sess.load(a)
     bb = sess.load(b)
     out_a, out_b = sess.run_pair_raw(ba, bb)
@@ -157,15 +171,22 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
             reports.append(rep)
             continue
         seen = set()
-        any_undecided = False
+        any_undecided = any_ne = any_unknown = False
         residual = False
         off = 0
         for name, sz in zip(names, sizes):
             for i in range(sz):
                 v = vc.vcs[base + off + i]
-                verdict = "equal" if v.equal else "undecided"
-                any_undecided |= not v.equal
-                rep.vcs.append({"array": name, "index": i, "verdict": verdict})
+                entry = {"array": name, "index": i, "verdict": "equal"}
+                if not v.equal:
+                    if slow_path:
+                        entry.update(sess.decide(v.node_a, v.node_b, fnv1a(f"{name}[{i}]"), trials))
+                    else:
+                        entry.update({"verdict": "undecided", "reason": "slow path not run"})
+                any_undecided |= entry["verdict"] == "undecided"
+                any_ne |= entry["verdict"] == "not_equal"
+                any_unknown |= entry["verdict"] == "unknown"
+                rep.vcs.append(entry)
                 for q in range(v.sc_off, v.sc_off + v.sc_n):
                     node = vc.sc_node[q]
                     key = sc_strs.get(node, node)
@@ -175,6 +196,56 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
                         rep.side_conditions.append({"denominator": sc_strs.get(node, f"#{node}"), "discharged": dis})
                         residual |= not dis
             off += sz
-        rep.verdict = "undecided" if any_undecided else ("unknown" if residual else "equivalent")
+        # aggregation (pipeline.cpp:259-265)
+        rep.verdict = ("not-equivalent" if any_ne else "undecided" if any_undecided
+                       else "unknown" if (any_unknown or residual) else "equivalent")
         reports.append(rep)
     return reports
+
+
+def _loc_j(loc):
+    return {"line": loc[0], "col": loc[1]}
+
+
+def report_to_json(rep: PairReport, kernel_a: str = "a", kernel_b: str = "b") -> dict:
+    """The reference's JSON report (report_to_json, pipeline.cpp:305-381)
+    without the timings block; dict key order matches, so json.dumps gives
+    the reference's text."""
+    j = {"verdict": rep.verdict, "kernels": {"a": kernel_a, "b": kernel_b}, "vcs": [dict(v) for v in rep.vcs]}
+    if rep.error_detail:
+        j["error"] = {"kernel": rep.error_kernel, "detail": rep.error_detail}
+    if rep.races:
+        acc = lambda x: {"tid": x.tid, "access": x.access, "loc": _loc_j(x.loc), "step": x.step}
+        j["race"] = {"pairs": [{"array": r.array, "offset": r.offset, "first": acc(r.first), "second": acc(r.second)}
+                               for r in rep.races]}
+    if rep.deadlock is not None:
+        d = {"threads": []}
+        for t in rep.deadlock.threads:
+            tj = {"tid": t["tid"], "state": t["state"]}
+            if "waiting" in t:
+                tj["waiting"] = t["waiting"]
+            if t["state"] == "blocked":
+                tj["loc"] = _loc_j(t["loc"])
+            d["threads"].append(tj)
+        if rep.deadlock.conflict_tids is not None:
+            d["conflict_tids"] = list(rep.deadlock.conflict_tids)
+            d["conflict_sets"] = [list(x) for x in rep.deadlock.conflict_sets]
+        j["deadlock"] = d
+    if rep.safeties:
+        faults = []
+        for s in rep.safeties:
+            f = {"kind": s.kind, "tid": s.tid, "loc": _loc_j(s.loc)}
+            if s.array is not None:
+                f["array"], f["offset"] = s.array, s.offset
+            if s.reg:
+                f["reg"] = s.reg
+            if s.kind == "out-of-bounds":
+                f["is_store"] = s.is_store
+            if s.detail:
+                f["detail"] = s.detail
+            f["step"] = s.step
+            faults.append(f)
+        j["safety"] = {"faults": faults}
+    j["side_conditions"] = [{"denominator": c["denominator"], "discharged": c["discharged"]}
+                            for c in rep.side_conditions]
+    return j

@@ -30,6 +30,6 @@ def gen_dirs():
 @pytest.fixture(scope="session")
 def session():
     from paper_2511_12638_b200.engine import Session
-    s = Session(0, max_nodes=1 << 20, max_kid_words=1 << 22, scratch_bytes=256 << 20)
+    s = Session(0, max_nodes=1 << 20, max_kid_words=1 << 22, scratch_bytes=256 << 20, keep_regs=True)
     yield s
     s.close()

@@ -5,7 +5,8 @@ oracle/_ref/ref_harness from the reference sources — tests/golden/make_golden.
 Compared exactly: steps, releases, outcome class, the ordered de-duplicated
 race list (addresses, tids, access kinds, source locations, step numbers),
 the safety list, the deadlock report, and — for fault-free runs — every
-final shared-memory cell rendered by to_string of the canonical form.
+final shared-memory cell and every thread's final register file
+(VEQ_OPT_KEEP_REGS) rendered by to_string of the canonical form.
 """
 import json
 import os
@@ -66,6 +67,10 @@ def check_run(got, want, where):
     assert got.outcome == want["outcome"], where
     if want["outcome"] == "final":
         assert got.shared == want["shared"], where
+        # Final register files (Outcome::regs, symexec.hpp:155-156), fixtures
+        # of at most 256 threads
+        if want.get("regs") and got.regs:
+            assert got.regs == want["regs"], where
 
 
 def _run_dir(session, d, sides):

@@ -40,13 +40,11 @@ def test_c5_variant_batch(session):
     for rep, d in zip(reps, dirs):
         want = json.load(open(os.path.join(d, "golden.json")))
         rv = want["report"]["verdict"]
+        # not-equivalent mutants are settled by the slow path (veq_decide:
+        # witnesses at the reference's own seeds and precisions)
+        assert rep.verdict == rv, d
         if rv == "not-equivalent":
-            # decided on the reference's host slow path; the device reports
-            # which VCs differ canonically
-            assert rep.verdict == "undecided", d
-            assert [v["verdict"] == "equal" for v in rep.vcs] == [v["fast_equal"] for v in want["fast_path"]], d
-        else:
-            assert rep.verdict == rv, d
+            assert [v["verdict"] for v in rep.vcs] == [v["verdict"] for v in want["report"]["vcs"]], d
         if rv == "kernel-B-error":
             assert [_race_j(r) for r in rep.races] == want["report"].get("race", {}).get("pairs", []), d
 
