@@ -14,6 +14,9 @@
 // non-zero on any difference.
 //   usage: integration_check KERNELS_DIR [pair-index ...]
 #include <dlfcn.h>
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
 
 #include <cstring>
 #include <fstream>
@@ -73,7 +76,15 @@ std::vector<Expr> import_exprs(veq_ctx *ctx, const std::vector<uint32_t> &roots,
     std::vector<Expr> k;
     for (uint32_t j = 0; j < n.nkids; j++) k.push_back(ex[kids[n.kid_off + j]]);
     switch (n.kind) {
-    case VEQ_K_CONST: ex[i] = cst(Rat(mpz_class((long)n.num), mpz_class((long)n.den))); break;
+    case VEQ_K_CONST:
+      if (n.den == 0) {
+        std::cerr << "import: Const with zero denominator at dag node " << i << " of " << nodes.size() << " (roots";
+        for (uint32_t r : roots) std::cerr << " " << r;
+        std::cerr << ")\n";
+        throw std::runtime_error("bad Const");
+      }
+      ex[i] = cst(Rat(mpz_class((long)n.num), mpz_class((long)n.den)));
+      break;
     case VEQ_K_NEGINF: ex[i] = neg_inf(); break;
     case VEQ_K_VAR:
       ex[i] = var(n.var_input >= 0 ? input_names[n.var_input] + "_" + std::to_string(n.var_index)
@@ -330,7 +341,7 @@ Report check_programs_gpu(veq_ctx *ctx, const Program &pa, const Program &pb, co
       } else {
         // canonically different: the host verdict API (slow path) decides
         const std::string key = a->name + "[" + std::to_string(i) + "]";
-        uint64_t seed = 14695981039346656037ull;  // fnv1a (pipeline.cpp:18-25)
+        uint64_t seed = 1469598103934665603ull;  // fnv1a as pipeline.cpp:18-25 seeds it
         for (unsigned char c : key) {
           seed ^= c;
           seed *= 1099511628211ull;
@@ -407,7 +418,17 @@ int golden_main(int n, char **dirs) {
 
 }  // namespace
 
+void on_fault(int sig) {
+  void *bt[64];
+  const int n = backtrace(bt, 64);
+  fprintf(stderr, "integration_check: signal %d\n", sig);
+  backtrace_symbols_fd(bt, n, 2);
+  _exit(128 + sig);
+}
+
 int main(int argc, char **argv) {
+  signal(SIGFPE, on_fault);
+  signal(SIGSEGV, on_fault);
   if (argc < 2) {
     std::cerr << "usage: integration_check KERNELS_DIR [pair-index ...]\n";
     return 2;

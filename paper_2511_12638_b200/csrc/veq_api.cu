@@ -147,6 +147,10 @@ struct veq_ctx {
   std::vector<uint64_t> all_sc_hash;
   std::vector<uint8_t> all_sc_dis;
   std::vector<uint64_t> rank_vc_off, rank_sc_off;
+  // host snapshot of the term table (append-only between clears): later
+  // exports copy only what was created since the previous one
+  std::vector<Node> hnodes;
+  std::vector<uint32_t> hkids;
   // veq_decide output
   std::string dec_reason, dec_f, dec_g;
   std::vector<std::string> dec_names, dec_values;
@@ -459,6 +463,8 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
 int veq_clear_terms(veq_ctx *ctx) {
   if (!ctx) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
+  ctx->hnodes.clear();
+  ctx->hkids.clear();
   Table &T = ctx->T;
   CK(cudaMemsetAsync(ctx->slots, 0xff, ctx->n_slots * sizeof(uint32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(unsigned long long), ctx->stream));
@@ -1300,22 +1306,37 @@ int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint
   return VEQ_OK;
 }
 
-int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_buf *buf) {
-  if (!ctx || !buf || (n_roots && !roots)) return VEQ_E_ARG;
-  CK(cudaSetDevice(ctx->device));
+// Host snapshot of the term table: nodes and kid words are append-only
+// between veq_clear_terms calls and complete whenever no run is in flight,
+// so each sync copies only the ranges created since the previous one.
+static int sync_table(veq_ctx *ctx) {
   cudaStream_t s = ctx->stream;
   unsigned long long nn[2];
   CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  uint64_t NN = std::min<uint64_t>(nn[0], ctx->lim.max_nodes), NK = std::min<uint64_t>(nn[1], ctx->lim.max_kid_words);
-  std::vector<Node> nodes(NN);
-  std::vector<uint32_t> kids(NK);
-  if (NN) CK(cudaMemcpyAsync(nodes.data(), ctx->nodes, NN * sizeof(Node), cudaMemcpyDeviceToHost, s));
-  if (NK) CK(cudaMemcpyAsync(kids.data(), ctx->kids, NK * 4, cudaMemcpyDeviceToHost, s));
+  const uint64_t NN = std::min<uint64_t>(nn[0], ctx->lim.max_nodes), NK = std::min<uint64_t>(nn[1], ctx->lim.max_kid_words);
+  const uint64_t n0 = std::min<uint64_t>(ctx->hnodes.size(), NN), k0 = std::min<uint64_t>(ctx->hkids.size(), NK);
+  ctx->hnodes.resize(NN);
+  ctx->hkids.resize(NK);
+  if (NN > n0)
+    CK(cudaMemcpyAsync(ctx->hnodes.data() + n0, ctx->nodes + n0, (NN - n0) * sizeof(Node), cudaMemcpyDeviceToHost, s));
+  if (NK > k0) CK(cudaMemcpyAsync(ctx->hkids.data() + k0, ctx->kids + k0, (NK - k0) * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  // iterative post-order DFS, dense renumbering
-  // dense renumbering through a flat table (no per-node map lookups)
-  std::vector<uint32_t> idx(NN, UNSET);
+  return VEQ_OK;
+}
+
+int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_buf *buf) {
+  if (!ctx || !buf || (n_roots && !roots)) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (int r = sync_table(ctx)) return r;
+  const std::vector<Node> &nodes = ctx->hnodes;
+  const std::vector<uint32_t> &kids = ctx->hkids;
+  const uint64_t NN = nodes.size();
+  // iterative post-order DFS over the reachable nodes, dense renumbering
+  struct Idx {
+    std::unordered_map<uint32_t, uint32_t> m;
+    uint32_t &operator[](uint32_t x) { return m.try_emplace(x, UNSET).first->second; }
+  } idx;
   std::vector<uint32_t> order;
   for (size_t r = 0; r < n_roots; r++) {
     if (roots[r] >= NN) return fail(ctx, VEQ_E_ARG, "root id out of range");
@@ -1348,8 +1369,10 @@ int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_
   uint64_t cap_n = buf->cap_nodes, cap_k = buf->cap_kids;
   buf->n_nodes = order.size();
   buf->n_kids = total_kids;
-  if (cap_n < order.size() || cap_k < total_kids || !buf->nodes || !buf->kids || !buf->root_index)
-    return VEQ_OK;  // sizing call
+  // sizing call: capacities too small or no node buffer (the kid buffer may
+  // be null when there are no kids)
+  if (cap_n < order.size() || cap_k < total_kids || !buf->nodes || !buf->root_index || (total_kids && !buf->kids))
+    return VEQ_OK;
   uint64_t ko = 0;
   for (size_t i = 0; i < order.size(); i++) {
     const Node &n = nodes[order[i]];
@@ -1385,21 +1408,6 @@ int veq_export_dag(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, veq_dag_
 
 // ---- to_string of device terms (proj/src/expr.cpp:735-822) ----------------
 namespace {
-
-// Host copy of the term table (nodes and kid arena as created so far).
-int copy_table(veq_ctx *ctx, std::vector<Node> &nodes, std::vector<uint32_t> &kids) {
-  cudaStream_t s = ctx->stream;
-  unsigned long long nn[2];
-  CK(cudaMemcpyAsync(nn, ctx->counters, 16, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const uint64_t NN = std::min<uint64_t>(nn[0], ctx->lim.max_nodes), NK = std::min<uint64_t>(nn[1], ctx->lim.max_kid_words);
-  nodes.resize(NN);
-  kids.resize(NK);
-  if (NN) CK(cudaMemcpyAsync(nodes.data(), ctx->nodes, NN * sizeof(Node), cudaMemcpyDeviceToHost, s));
-  if (NK) CK(cudaMemcpyAsync(kids.data(), ctx->kids, NK * 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  return VEQ_OK;
-}
 
 // Byte sinks: a string, or CRC-32 (IEEE, zlib.crc32) + length.
 struct StrSink {
@@ -1542,10 +1550,9 @@ extern "C" {
 int veq_render(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, const char **text, const uint64_t **offs) {
   if (!ctx || (n_roots && !roots) || !text || !offs) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
-  std::vector<Node> nodes;
-  std::vector<uint32_t> kids;
-  if (int r = copy_table(ctx, nodes, kids)) return r;
-  Printer P{nodes, kids, ctx->input_names};
+  if (int r = sync_table(ctx)) return r;
+  const std::vector<Node> &nodes = ctx->hnodes;
+  Printer P{ctx->hnodes, ctx->hkids, ctx->input_names};
   ctx->render_text.clear();
   ctx->render_offs.assign(1, 0);
   StrSink sink{&ctx->render_text};
@@ -1562,10 +1569,10 @@ int veq_render(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, const char *
 int veq_render_digest(veq_ctx *ctx, const uint32_t *roots, size_t n_roots, uint32_t *crc32, uint64_t *len) {
   if (!ctx || (n_roots && (!roots || !crc32 || !len))) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
-  std::vector<Node> nodes;
-  std::vector<uint32_t> kids;
-  if (int r = copy_table(ctx, nodes, kids)) return r;
-  Printer P{nodes, kids, ctx->input_names};
+  if (int r = sync_table(ctx)) return r;
+  const std::vector<Node> &nodes = ctx->hnodes;
+  const std::vector<uint32_t> &kids = ctx->hkids;
+  Printer P{ctx->hnodes, ctx->hkids, ctx->input_names};
   static const CrcCat C;
   using D = CrcCat::D;
   // memo of each node's unparenthesised text digest; atoms are printed
@@ -2128,14 +2135,19 @@ int veq_decide(veq_ctx *ctx, uint32_t f, uint32_t g, uint64_t seed, uint64_t tri
       res.reason = e.what();
     }
     if (has_max && (opaque_done || res.reason.empty())) {
-      // the full max case split (split_max, decide.cpp:677-681) is not
-      // restated: such VCs stay undecided rather than guessed
+      // The reference now runs the max case split (split_max,
+      // decide.cpp:677-681), which is not restated. A rigorous witness
+      // settles NotEqual regardless of its outcome (it could not have
+      // proved equality); without one the VC stays undecided, not guessed.
+      if (!veqdec::mpfr_available()) return fail(ctx, VEQ_E_UNSUPPORTED, "libmpfr.so.6 not available for witnesses");
+      try {
+        if (veqdec::refute_random(dag, f, g, trials, seed, res)) return finish(veqdec::Kind::NotEqual);
+      } catch (const DecideError &) {
+      }
       res.reason = "max case analysis not available";
+      res.assignment.clear();
+      finish(veqdec::Kind::Unknown);
       out->kind = VEQ_UNDECIDED;
-      ctx->dec_reason = res.reason;
-      out->reason = ctx->dec_reason.c_str();
-      out->n_assign = 0;
-      out->precision = 0;
       return VEQ_OK;
     }
   }
