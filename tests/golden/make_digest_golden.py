@@ -55,5 +55,38 @@ def main(prefixes):
         print(f"{name} ok ({time.time() - t0:.1f} s)", flush=True)
 
 
+
+
+def c5_cases(n_variants: int = 1000, n: int = 32):
+    """C5 at full size: one digest golden per distinct (variant source,
+    config) of the seeded 1,000-variant generator at N = 32."""
+    seen = {}
+    for kind, src, cfg in workloads.c5_variants(n_variants, n):
+        key = (src, cfg)
+        if key not in seen:
+            tk = cfg.split("params.TK = ")[1].split()[0]
+            seen[key] = f"dg_c5_{kind}_tk{tk}"
+    return [(name, src, cfg) for (src, cfg), name in seen.items()]
+
+
+def main_c5():
+    ref = workloads.c5_reference(32)
+    for name, src, cfg in c5_cases():
+        d = os.path.join(HERE, name)
+        if os.path.exists(os.path.join(d, "golden.json")):
+            continue
+        os.makedirs(d, exist_ok=True)
+        for fn, text in (("a.mk", ref), ("b.mk", src), ("cfg.cfg", cfg)):
+            with open(os.path.join(d, fn), "w") as f:
+                f.write(text)
+        t0 = time.time()
+        subprocess.check_call([H, "digest", d, os.path.join(d, "a.mk"), os.path.join(d, "b.mk"),
+                               os.path.join(d, "cfg.cfg")])
+        print(f"{name} ok ({time.time() - t0:.1f} s)", flush=True)
+
+
 if __name__ == "__main__":
-    main(sys.argv[1:])
+    if sys.argv[1:] == ["c5"]:
+        main_c5()
+    else:
+        main(sys.argv[1:])
