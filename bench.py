@@ -67,7 +67,7 @@ class ClockSampler:
         self.gpu, self.samples, self.proc = gpu, [], None
 
     def __enter__(self):
-        if shutil.which("nvidia-smi"):
+        if shutil.which("nvidia-smi") and os.environ.get("VEQ_NO_CLOCKS") != "1":
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
@@ -254,7 +254,9 @@ def main():
     deltas = np.ascontiguousarray(np.concatenate([da, db], axis=1), dtype=np.int32)
     S_pair = len(ta.stmts) + len(tb.stmts)
     S_step = S_pair * cps
-    sess = Session(local, max_nodes=min((1 << 31) - 1, max(1 << 22, 4 * S_step // 10)),
+    # created nodes per step run at ~S/8 (C3) to ~S/5.3 (C4): S/5 keeps the
+    # slot table (cleared every step) at load <= 0.5 with headroom
+    sess = Session(local, max_nodes=min((1 << 31) - 1, max(1 << 22, int(S_step * float(os.environ.get("VEQ_NODES_PER_STMT", "0.2"))))),
                    max_kid_words=min((1 << 32) - 1, (1 << 24) + 4 * S_step),
                    scratch_bytes=wl.get("scratch_gb", 8) << 30)
     L = N.lib()
@@ -283,20 +285,36 @@ def main():
 
     state = {"k": 0, "equal": 0, "vcs": 0, "faults": 0, "launches": 0}
 
+    step_prof = os.environ.get("VEQ_STEP_PROF") == "1"
+
     def step(th_use=None, e2e=False):
         k = state["k"]
         state["k"] += 1
         blk = blocks_of(k)
+        tt = [time.perf_counter()]
+
+        def lap():
+            if step_prof:
+                torch.cuda.synchronize()
+                tt.append(time.perf_counter())
         assert L.veq_clear_terms(sess.ctx) == 0
+        lap()
         tu = th_use if th_use is not None else th
         h = sess.instantiate(tu, deltas[blk])
+        lap()
         r = sess.run_raw(h)
+        lap()
         vc = sess.compare_progs_raw(h, 0, h, cps, cps, oa, ob)
+        lap()
         n_eq, n_vcs, nf = int(vc.n_equal), int(vc.n_vcs), int(r.n_faults)
         if e2e:  # every VC's verdict to the host (d2h counted in e2e)
             eqs = np.ctypeslib.as_array(C.cast(vc.vcs, C.POINTER(C.c_uint32)), shape=(n_vcs * 6,))[2::6].copy()
             n_eq = int(eqs.sum())
         sess.drop(h)
+        lap()
+        if step_prof:
+            print("[step] clear %.1f instantiate %.1f run %.1f compare %.1f drop %.1f ms" %
+                  tuple(1000 * (tt[i + 1] - tt[i]) for i in range(5)), file=sys.stderr)
         state["equal"] += n_eq
         state["vcs"] += n_vcs
         state["faults"] += nf

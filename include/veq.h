@@ -375,6 +375,14 @@ int veq_compare_progs(veq_ctx *ctx, uint32_t batch_a, uint32_t prog_a0, uint32_t
                       uint32_t n_pairs, const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
                       uint32_t n_out_per_pair, veq_vc_out *out);
 
+/* One reference program against many: program prog_a of batch_a against
+ * program prog_b0 + i of batch_b, i < n_pairs (a batch of candidate kernels
+ * checked against one reference kernel that ran once). VCs are laid out
+ * pair-major as in veq_compare_progs. */
+int veq_compare_fan(veq_ctx *ctx, uint32_t batch_a, uint32_t prog_a, uint32_t batch_b, uint32_t prog_b0,
+                    uint32_t n_pairs, const uint32_t *out_arrays_a, const uint32_t *out_arrays_b,
+                    uint32_t n_out_per_pair, veq_vc_out *out);
+
 /* ---- slow path of the verdict API (ctaeq::eq, proj/src/decide.cpp:728-859)
  * For a VC whose canonical forms differ: d = canon(f - g) on the device; if
  * d is 0, or the exp-polynomial normal form of d's rationalized numerator

@@ -460,17 +460,33 @@ int veq_declare_inputs(veq_ctx *ctx, const veq_input_desc *inputs, uint32_t n) {
   return VEQ_OK;
 }
 
+// Fills n 32-bit words with a value, 16 bytes per thread per iteration
+// (grid-stride over all SMs): the per-step table clear.
+__global__ void k_fill_u32(uint32_t *p, uint64_t n, uint32_t v) {
+  const uint64_t n4 = n / 4;
+  uint4 *q = reinterpret_cast<uint4 *>(p);
+  const uint4 w = make_uint4(v, v, v, v);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x)
+    q[i] = w;
+  if (blockIdx.x == 0 && threadIdx.x < n - 4 * n4) p[4 * n4 + threadIdx.x] = v;
+}
+
 int veq_clear_terms(veq_ctx *ctx) {
   if (!ctx) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   ctx->hnodes.clear();
   ctx->hkids.clear();
   Table &T = ctx->T;
-  CK(cudaMemsetAsync(ctx->slots, 0xff, ctx->n_slots * sizeof(uint32_t), ctx->stream));
+  {
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    k_fill_u32<<<nsm * 8, 256, 0, ctx->stream>>>(ctx->slots, ctx->n_slots, 0xFFFFFFFFu);
+    ctx->launches++;
+  }
   CK(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(unsigned long long), ctx->stream));
   CK(cudaMemsetAsync(ctx->error, 0, sizeof(int), ctx->stream));
   CK(cudaMemsetAsync(ctx->dbg, 0, 4 * sizeof(unsigned long long), ctx->stream));
-  if (T.in_cache) CK(cudaMemsetAsync(T.in_cache, 0xff, ctx->in_cells * 4, ctx->stream));
+  if (T.in_cache) k_fill_u32<<<148, 256, 0, ctx->stream>>>(T.in_cache, ctx->in_cells, 0xFFFFFFFFu);
   // a single thread interns -inf, 0, 1, -1 first into an empty table, so
   // their ids are 0..3 without a host round trip
   k_session_init<<<1, 32, 0, ctx->stream>>>(T, ctx->session_ids);
@@ -952,7 +968,13 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   if (bd->n_cells) LAUNCH(k_resolve_finals<<<blocks(bd->n_cells, 256), 256, 0, s>>>(B));
   if (B.keep_regs && bd->n_regs) LAUNCH(k_resolve_regs<<<blocks(bd->n_regs, 256), 256, 0, s>>>(B, bd->n_regs));
   // deferred scaling: products of a used-once sum feeding a chain (k_mark_defer)
-  if (S && !B.no_defer) LAUNCH(k_mark_defer<<<blocks(S, 256), 256, 0, s>>>(B));
+  B.prog_split = nullptr;
+  if (S && !B.no_defer) {
+    LAUNCH(k_mark_defer<<<blocks(S, 256), 256, 0, s>>>(B));
+    { int r_ = ws_get(ctx, 28, (void **)&B.prog_split, (uint64_t)B.n_progs * 4); if (r_) return r_; }
+    CK(cudaMemsetAsync(B.prog_split, 0xff, (uint64_t)B.n_progs * 4, s));
+    LAUNCH(k_defer_split<<<blocks(S, 256), 256, 0, s>>>(B));
+  }
   PH1(VEQ_PH_RESOLVE);
   CK(cudaGetLastError());
   // chain logs
@@ -981,15 +1003,17 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     { int r_ = ws_get(ctx, 13, (void **)&wk2, U * 8); if (r_) return r_; }
     { int r_ = ws_get(ctx, 14, (void **)&wv, U * 4); if (r_) return r_; }
     { int r_ = ws_get(ctx, 15, (void **)&wv2, U * 4); if (r_) return r_; }
-    { int r_ = ws_get(ctx, 16, (void **)&nw, 8); if (r_) return r_; }
-    CK(cudaMemsetAsync(nw, 0, 8, s));
+    // nw = {items, pass-2 items}
+    { int r_ = ws_get(ctx, 16, (void **)&nw, 16); if (r_) return r_; }
+    CK(cudaMemsetAsync(nw, 0, 16, s));
     CK(cudaMemsetAsync(wk, 0xff, U * 8, s));
     LAUNCH(k_scatter_work<<<blocks(S, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
     void *tmp2 = nullptr;
     n_work = bd->n_arith;
     if (n_work) {
-      // key = step << prog_bits | program: sort only the bits in use
-      const int end_bit = (int)(B.prog_bits + B.step_bits);
+      // key = pass << (step_bits + prog_bits) | step << prog_bits | program:
+      // sort only the bits in use
+      const int end_bit = (int)(B.prog_bits + B.step_bits) + (B.prog_split ? 1 : 0);
       size_t tb2 = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
       { int r_ = ws_get(ctx, 17, (void **)&tmp2, tb2); if (r_) return r_; }
@@ -1000,8 +1024,8 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     PH0(VEQ_PH_EVAL);
     if (n_work) {
       unsigned long long *cursor = nullptr;
-      { int r_ = ws_get(ctx, 18, (void **)&cursor, 8); if (r_) return r_; }
-      CK(cudaMemsetAsync(cursor, 0, 8, s));
+      { int r_ = ws_get(ctx, 18, (void **)&cursor, 16); if (r_) return r_; }
+      CK(cudaMemsetAsync(cursor, 0, 16, s));
       static const bool prof_on = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
       unsigned long long *prof = nullptr;
       if (prof_on) {
@@ -1052,7 +1076,11 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
       }
       uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * threads)));
       LAUNCH(launch_eval_warp(blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s, B, ctx->T, E, desc, nw, cursor,
-                              ctx->pool, ctx->pool_used, ctx->pool_cap, chunk));
+                              ctx->pool, ctx->pool_used, ctx->pool_cap, chunk, false));
+      // pass 2: items from each program's first deferred expansion on
+      if (B.prog_split)
+        LAUNCH(launch_eval_warp(blocks(threads, EVAL_BLOCK), EVAL_BLOCK, smem, s, B, ctx->T, E, desc, nw, cursor + 1,
+                                ctx->pool, ctx->pool_used, ctx->pool_cap, chunk, true));
       CK(cudaGetLastError());
       if (prof) {
         unsigned long long hp[256], nwh = 0;
@@ -1229,18 +1257,21 @@ int veq_compare(veq_ctx *ctx, uint32_t ba, uint32_t bb, const uint32_t *out_a, c
   return veq_compare_progs(ctx, ba, 0, bb, 0, (uint32_t)A->progs.size(), out_a, out_b, n_out, out);
 }
 
-int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint32_t pb0, uint32_t n_pairs,
-                      const uint32_t *out_a, const uint32_t *out_b, uint32_t n_out, veq_vc_out *out) {
+// Pair q compares program pa0 + q * a_stride of batch a with pb0 + q of b.
+static int compare_impl(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t a_stride, uint32_t bb, uint32_t pb0,
+                        uint32_t n_pairs, const uint32_t *out_a, const uint32_t *out_b, uint32_t n_out,
+                        veq_vc_out *out) {
   if (!ctx || !live_batch(ctx, ba) || !live_batch(ctx, bb)) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   BatchDev *A = ctx->batches[ba], *Bd = ctx->batches[bb];
   if (!A->ran || !Bd->ran) return fail(ctx, VEQ_E_ARG, "compare before run");
-  if ((uint64_t)pa0 + n_pairs > A->progs.size() || (uint64_t)pb0 + n_pairs > Bd->progs.size())
+  if ((uint64_t)pa0 + (uint64_t)(n_pairs ? n_pairs - 1 : 0) * a_stride + (n_pairs ? 1 : 0) > A->progs.size() ||
+      (uint64_t)pb0 + n_pairs > Bd->progs.size())
     return fail(ctx, VEQ_E_ARG, "program range out of the batch");
   std::vector<uint32_t> ca, cb;
   for (size_t q = 0; q < n_pairs; q++)
     for (uint32_t k = 0; k < n_out; k++) {
-      const size_t p = pa0 + q, pb = pb0 + q;
+      const size_t p = pa0 + q * a_stride, pb = pb0 + q;
       uint32_t ga = A->progs[p].array_off + out_a[k], gb = Bd->progs[pb].array_off + out_b[k];
       if (out_a[k] >= A->progs[p].n_arrays || out_b[k] >= Bd->progs[pb].n_arrays)
         return fail(ctx, VEQ_E_ARG, "out array index out of range");
@@ -1304,6 +1335,16 @@ int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint
     out->n_missing = h[2];
   }
   return VEQ_OK;
+}
+
+int veq_compare_progs(veq_ctx *ctx, uint32_t ba, uint32_t pa0, uint32_t bb, uint32_t pb0, uint32_t n_pairs,
+                      const uint32_t *out_a, const uint32_t *out_b, uint32_t n_out, veq_vc_out *out) {
+  return compare_impl(ctx, ba, pa0, 1, bb, pb0, n_pairs, out_a, out_b, n_out, out);
+}
+
+int veq_compare_fan(veq_ctx *ctx, uint32_t ba, uint32_t pa, uint32_t bb, uint32_t pb0, uint32_t n_pairs,
+                    const uint32_t *out_a, const uint32_t *out_b, uint32_t n_out, veq_vc_out *out) {
+  return compare_impl(ctx, ba, pa, 0, bb, pb0, n_pairs, out_a, out_b, n_out, out);
 }
 
 // Host snapshot of the term table: nodes and kid words are append-only

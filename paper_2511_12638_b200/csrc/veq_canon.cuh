@@ -57,6 +57,17 @@ struct Arena {
   template <class X> __device__ X *get(uint64_t n) { return reinterpret_cast<X *>(alloc(n * sizeof(X))); }
 };
 
+// Calls into the out-of-line routines go through a copy of the caller's
+// arena: only the copy's address escapes, so a kernel's own arena stays in
+// registers on its hot paths (the out-of-line call is the rare path).
+template <class F>
+__device__ __forceinline__ uint32_t arena_call(Arena &A, F f) {
+  Arena a2 = A;
+  const uint32_t r = f(a2);
+  A = a2;
+  return r;
+}
+
 // A term coeff * f[0] * ... * f[nf-1] (expr.cpp:296-300). Factors live in
 // the kid arena of an existing Mul (read-only) or in scratch; a single
 // factor is held inline.
@@ -211,7 +222,7 @@ __device__ inline uint32_t finish_term(const Table &T, Arena &A, Rat c, const Te
 
 // Group like terms, drop zero coefficients, rebuild and add()
 // (canon_add_kids tail + rebuild, expr.cpp:402-424).
-VEQ_NOINLINE uint32_t collect_terms(const Table &T, Arena &A, Term *ts, uint32_t n) {
+__device__ inline uint32_t collect_terms(const Table &T, Arena &A, Term *ts, uint32_t n) {
   if (n == 0) return T.id_zero;
   uint32_t *idx = A.get<uint32_t>(n), *tmp = A.get<uint32_t>(n);
   if (!idx || !tmp) return T.id_zero;
@@ -243,7 +254,7 @@ VEQ_NOINLINE uint32_t collect_terms(const Table &T, Arena &A, Term *ts, uint32_t
 }
 
 // canon_add_kids over canonical leaves (expr.cpp:415-424).
-VEQ_NOINLINE uint32_t add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
+__device__ inline uint32_t add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
   uint32_t total = 0;
   for (uint32_t i = 0; i < n; i++) total += n_terms_of(T, leaves[i]);
   Term *ts = A.get<Term>(total ? total : 1);
@@ -278,7 +289,7 @@ __device__ inline uint32_t merge_exp_factors(const Table &T, Arena &A, uint32_t 
 }
 
 // canon_mul_kids over canonical operands (expr.cpp:426-481).
-VEQ_NOINLINE uint32_t mul_canon(const Table &T, Arena &A, const uint32_t *ops, uint32_t n) {
+__device__ inline uint32_t mul_canon(const Table &T, Arena &A, const uint32_t *ops, uint32_t n) {
   Rat coeff{1, 1};
   uint32_t nfac = 0, nsum = 0;
   for (uint32_t i = 0; i < n; i++) {
@@ -438,7 +449,7 @@ __device__ inline uint32_t split_coeff(const Table &T, Arena &A, uint32_t e, Rat
 }
 
 // canon_div (expr.cpp:543-559); den is not the literal 0 (checked by div()).
-VEQ_NOINLINE uint32_t canon_div(const Table &T, Arena &A, uint32_t num, uint32_t den) {
+__device__ inline uint32_t canon_div(const Table &T, Arena &A, uint32_t num, uint32_t den) {
   Node dn = ld_node(T, den);
   if (dn.kind == K_CONST) {
     uint32_t ops[2] = {intern_const(T, rat_div(T, Rat{1, 1}, const_val(dn))), num};
@@ -477,7 +488,7 @@ __device__ inline uint32_t mx_lower(const Table &T, const uint32_t *run, uint32_
   }
   return lo;
 }
-VEQ_NOINLINE uint32_t max_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
+__device__ inline uint32_t max_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
   uint32_t total = 0, nloose = 0;
   for (uint32_t i = 0; i < n; i++) {
     Node k = ld_node(T, leaves[i]);

@@ -11,9 +11,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-// Heavy canonicalisation routines stay out-of-line: smaller kernels, much
-// shorter builds (static: one private copy per translation unit that uses it).
+// Routines of the rare paths (deferred-scaling expansion). Measured on C3:
+// any out-of-line call in k_eval_warp costs the whole kernel ~2.7x (eval
+// 31 ms -> 85 ms per 4 CTA pairs), so they are inlined like everything else;
+// define VEQ_FAST_BUILD to outline them for quick development builds.
+#ifdef VEQ_FAST_BUILD
 #define VEQ_NOINLINE static __device__ __noinline__
+#else
+#define VEQ_NOINLINE static __device__ inline
+#endif
 
 namespace veqd {
 

@@ -75,6 +75,9 @@ struct Batch {
   uint32_t *user;
   uint8_t *defer;
   uint32_t no_defer;  // 1: deferral disabled (VEQ_NO_DEFER, or the -inf fallback)
+  // per program: the first step of an item that expands deferred leaves
+  // (k_defer_split); items at or after it form the second eval pass
+  uint32_t *prog_split;
   uint32_t keep_regs; // 1: final register files are kept and canonicalised (veq_fetch_regs)
   unsigned long long *tup_key, *tup_val;
   unsigned long long *n_tup;
@@ -1724,9 +1727,30 @@ __global__ void k_mark_defer(Batch B) {
 }
 #endif
 
-// One pass after the log scan: chain-log entries and the work list (every
-// executed BinOp/UnOp except chain links absorbed by their successor, and
-// deferred products and sums).
+// A work item: every executed BinOp/UnOp except chain links absorbed by
+// their successor, and deferred products and sums.
+__device__ __forceinline__ bool is_work_item(const Batch &B, uint64_t i, const veq_stmt &st) {
+  if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) return false;
+  if (is_chain_op(st) && B.continued[i] && B.uses[i] == 1) return false;
+  return !(B.defer[i] & (DF_LEAF | DF_SUM));
+}
+
+// Two-pass evaluation: the deferred expansion (eval_add_deferred) needs a
+// deep call stack that slows the whole evaluator down, so only the items
+// from each program's first expanding chain onwards run in the kernel that
+// carries it. Every dependency of an item is in its program at a smaller
+// step, so pass 1 (steps below the split) never waits on pass 2.
+#ifndef VEQ_TU_EVAL
+__global__ void k_defer_split(Batch B) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B.n_stmts || B.st_step[i] == UNSET) return;
+  const veq_stmt st = B.stmts[i];
+  if (!is_chain_op(st) || !(B.defer[B.chain_head[i]] & DF_CHAIN) || !is_work_item(B, i, st)) return;
+  atomicMin(B.prog_split + prog_of_stmt(B, i), B.st_step[i]);
+}
+#endif
+
+// One pass after the log scan: chain-log entries and the work list.
 #ifndef VEQ_TU_EVAL
 __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t *base, uint32_t *log,
                                                         uint32_t *log_stmt, unsigned long long *wkey, uint32_t *wval,
@@ -1741,7 +1765,6 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
     const uint64_t i = b0 + (uint64_t)k * APP_NT;
     if (i >= B.n_stmts || B.st_step[i] == UNSET) continue;
     const veq_stmt st = B.stmts[i];
-    if (st.kind != VEQ_ST_BINOP && st.kind != VEQ_ST_UNOP) continue;
     if (is_chain_op(st)) {
       const uint32_t h = B.chain_head[i], pos = B.chain_pos[i];
       const uint32_t b = base[h];
@@ -1754,10 +1777,8 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
         log[b + pos + 1] = B.ref_b[i];
         log_stmt[b + pos + 1] = (uint32_t)i;
       }
-      if (B.continued[i] && B.uses[i] == 1) continue;  // absorbed by its successor
     }
-    if (B.defer[i] & (DF_LEAF | DF_SUM)) continue;  // expanded by the consuming chain
-    mask |= 1u << k;
+    if (is_work_item(B, i, st)) mask |= 1u << k;
   }
   unsigned long long o = block_append<APP_NT>(n_work, __popc(mask));
 #pragma unroll
@@ -1766,7 +1787,10 @@ __global__ void __launch_bounds__(APP_NT) k_scatter_work(Batch B, const uint32_t
     const uint64_t i = b0 + (uint64_t)k * APP_NT;
     // (step, program): every dependency of an item has a smaller step in the
     // same program, hence a smaller key, and all CTAs advance together
-    wkey[o] = ((unsigned long long)B.st_step[i] << B.prog_bits) | prog_walk(B, s_p0, i);
+    const uint32_t p = prog_walk(B, s_p0, i);
+    const unsigned long long pass2 = B.prog_split && B.st_step[i] >= B.prog_split[p];
+    if (pass2) atomicAdd(n_work + 1, 1ull);
+    wkey[o] = (pass2 << (B.prog_bits + B.step_bits)) | ((unsigned long long)B.st_step[i] << B.prog_bits) | p;
     wval[o] = (uint32_t)i;
     o++;
   }
@@ -1823,7 +1847,7 @@ __device__ inline void arith_fault(const Batch &B, uint32_t stmt, uint8_t detail
   emit_fault(B, f);
 }
 
-VEQ_NOINLINE uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, const EvalCtx &E, uint32_t i) {
+__device__ inline uint32_t eval_stmt(const Batch &B, const Table &T, Arena &A, const EvalCtx &E, uint32_t i) {
   const veq_stmt st = B.stmts[i];
   auto undef_of = [&](uint32_t s) { return intern_undef(T, 3, s >> 29, s); };
   if (st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX)) {
@@ -1961,12 +1985,12 @@ void eval_warp_config(int smem, int *per_sm);
 void launch_eval_warp(uint32_t grid, uint32_t block, int smem, cudaStream_t s, const Batch &B, const Table &T,
                       const EvalCtx &E, const uint4 *desc, const unsigned long long *n_work_dev,
                       unsigned long long *cursor, char *pool, unsigned long long *pool_used, uint64_t pool_cap,
-                      uint64_t chunk);
+                      uint64_t chunk, bool defer);
 #ifdef VEQ_TU_EVAL
 // One fused Add chain, whole warp (lg: the chain's first 32 log entries,
 // lane-indexed). Returns the canonical sum; `created` when this warp
 // published a new node (its fence already ran).
-VEQ_NOINLINE uint32_t eval_add_warp(const Batch &B, const Table &T, const EvalCtx &E, Arena &A, WarpAlloc &W,
+__device__ inline uint32_t eval_add_warp(const Batch &B, const Table &T, const EvalCtx &E, Arena &A, WarpAlloc &W,
                                          const SmemPool &SP, const uint4 d, const uint32_t lg, bool &created,
                                          int &path, unsigned long long *prof_lean, unsigned long long *prof_smem,
                                          unsigned long long &prof_pool, unsigned long long &prof_pages) {
@@ -2145,7 +2169,7 @@ VEQ_NOINLINE uint32_t scaled_term(const Table &T, const EvalCtx &E, Arena &A, ui
 // leaves are expanded (X's chain leaves, each under the scale c times the
 // enclosing scale, recursively), every leaf is scaled lane-parallel, and the
 // scaled terms are summed (canon_add_kids). Whole warp.
-VEQ_NOINLINE uint32_t eval_add_deferred(const Batch &B, const Table &T, const EvalCtx &E, Arena &A,
+static __device__ __noinline__ uint32_t eval_add_deferred(const Batch &B, const Table &T, const EvalCtx &E, Arena &A,
                                              const uint4 d) {
   const uint32_t lane = lane_id();
   const long long c0 = E.prof ? clock64() : 0;
@@ -2263,6 +2287,10 @@ VEQ_NOINLINE uint32_t eval_add_deferred(const Batch &B, const Table &T, const Ev
   return r;
 }
 
+// DEFER selects the pass (k_defer_split): n_work_dev = {items, pass-2 items};
+// the sorted list holds pass 1 then pass 2, and only the pass-2 kernel
+// carries the deferred expansion.
+template <bool DEFER>
 __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, EvalCtx E, const uint4 *desc,
                                                              const unsigned long long *n_work_dev,
                                                              unsigned long long *cursor, char *pool,
@@ -2270,7 +2298,9 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
                                                              uint64_t chunk) {
   // work-list length and window size from the device (no host read-back): a
   // short list is claimed in small windows so it spreads over all warps
-  const uint64_t n_work = *n_work_dev;
+  const uint64_t n_all = n_work_dev[0], n_p2 = n_work_dev[1];
+  const uint64_t n_work = DEFER ? n_p2 : n_all - n_p2;
+  if (DEFER) desc += n_all - n_p2;
   const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t G = n_work >= warps_total * 128 ? 32 : (n_work >= warps_total * 16 ? 8 : 1);
   extern __shared__ __align__(16) char eval_smem[];
@@ -2317,7 +2347,12 @@ __global__ void __launch_bounds__(EVAL_BLOCK, 1) k_eval_warp(Batch B, Table T, E
         int path = 0;
         uint32_t r;
         if (d.w & DESC_DEFER) {
-          r = eval_add_deferred(B, T, E, A, d);
+          if constexpr (DEFER) {
+            r = arena_call(A, [&](Arena &a) { return eval_add_deferred(B, T, E, a, d); });
+          } else {
+            set_error(T, E_INTERNAL);  // k_defer_split puts every such chain in pass 2
+            r = UNSET;
+          }
           path = 4;
         } else {
           r = eval_add_warp(B, T, E, A, W, SP, d, lg, created, path, E.prof ? prof_lean : nullptr,

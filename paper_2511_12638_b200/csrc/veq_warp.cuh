@@ -707,7 +707,7 @@ __device__ __forceinline__ bool pref_less(const Table &T, uint64_t pa, uint32_t 
 // the result's kids are the terms themselves plus at most one folded Const,
 // and canonical order (Expr::compare) is produced by merging the leaves'
 // already-sorted kid runs with warp-parallel merge-path passes.
-VEQ_NOINLINE uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint32_t m, WarpAlloc *W,
+__device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint32_t m, WarpAlloc *W,
                                        unsigned long long *ph = nullptr, bool coef_room = true) {
   const uint32_t lane = lane_id();
   const long long c0 = ph ? clock64() : 0;
@@ -901,7 +901,7 @@ VEQ_NOINLINE uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, uint3
 }
 
 // canon_add_kids over n canonical leaves (scratch), warp-cooperative.
-VEQ_NOINLINE uint32_t warp_add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
+__device__ inline uint32_t warp_add_nary(const Table &T, Arena &A, const uint32_t *leaves, uint32_t n) {
   const uint32_t lane = lane_id();
   // 1. term offsets per leaf
   uint32_t *off = warp_get<uint32_t>(A, n + 1);

@@ -197,6 +197,17 @@ class Session:
         _check(self.ctx, N.lib().veq_compare_progs(self.ctx, ba, pa0, bb, pb0, n_pairs, A, B, n, C.byref(out)))
         return out
 
+    def compare_fan_raw(self, ba: int, pa: int, bb: int, pb0: int, n_pairs: int, out_a: Sequence[int],
+                        out_b: Sequence[int]) -> N.veq_vc_out:
+        """Program pa of batch ba against programs pb0 .. pb0 + n_pairs - 1 of
+        bb (veq_compare_fan)."""
+        n = len(out_a)
+        A = (C.c_uint32 * max(1, n))(*out_a)
+        B = (C.c_uint32 * max(1, n))(*out_b)
+        out = N.veq_vc_out()
+        _check(self.ctx, N.lib().veq_compare_fan(self.ctx, ba, pa, bb, pb0, n_pairs, A, B, n, C.byref(out)))
+        return out
+
     def compare_raw(self, ba: int, bb: int, out_a: Sequence[int], out_b: Sequence[int]) -> N.veq_vc_out:
         n = len(out_a)
         A = (C.c_uint32 * max(1, n))(*out_a)

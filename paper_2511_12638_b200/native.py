@@ -178,6 +178,7 @@ def lib() -> C.CDLL:
     L.veq_fetch_cells.argtypes = [vp, u32, u32, u32, P(u32), u64]
     L.veq_compare.argtypes = [vp, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
     L.veq_compare_progs.argtypes = [vp, u32, u32, u32, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
+    L.veq_compare_fan.argtypes = [vp, u32, u32, u32, u32, u32, P(u32), P(u32), u32, P(veq_vc_out)]
     L.veq_export_dag.argtypes = [vp, P(u32), C.c_size_t, P(veq_dag_buf)]
     L.veq_verdict_counters.argtypes = [vp, P(u64)]
     L.veq_set_timing.argtypes = [vp, C.c_int]
@@ -200,7 +201,7 @@ def lib() -> C.CDLL:
     L.veq_comm_combine.argtypes = [vp, u64, P(veq_combined)]
     L.veq_decide.argtypes = [vp, u32, u32, u64, u64, P(veq_decision)]
     for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_run_start", "veq_run_finish",
-              "veq_fetch_cells", "veq_compare", "veq_compare_progs",
+              "veq_fetch_cells", "veq_compare", "veq_compare_progs", "veq_compare_fan",
               "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -212,5 +213,5 @@ EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_decl
             "veq_set_timing", "veq_clear_terms", "veq_stream", "veq_drop_batch", "veq_load_template",
             "veq_instantiate", "veq_drop_template", "veq_render", "veq_render_digest", "veq_batch_locs",
             "veq_run_report", "veq_set_members", "veq_set_option", "veq_fetch_regs", "veq_comm_unique_id",
-            "veq_comm_init", "veq_comm_combine", "veq_decide"]
+            "veq_comm_init", "veq_comm_combine", "veq_decide", "veq_compare_fan"]
 PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]

@@ -1,3 +1,5 @@
+import gzip
+import json
 import os
 import sys
 
@@ -17,9 +19,19 @@ def golden_dirs(prefix=""):
     out = []
     for d in sorted(os.listdir(GOLDEN)):
         p = os.path.join(GOLDEN, d)
-        if os.path.isdir(p) and d.startswith(prefix) and os.path.exists(os.path.join(p, "golden.json")):
+        if os.path.isdir(p) and d.startswith(prefix) and (
+                os.path.exists(os.path.join(p, "golden.json")) or os.path.exists(os.path.join(p, "golden.json.gz"))):
             out.append(p)
     return out
+
+
+def load_golden(d):
+    """A fixture's golden.json (or its gzipped form, golden.json.gz)."""
+    p = os.path.join(d, "golden.json")
+    if os.path.exists(p):
+        return json.load(open(p))
+    with gzip.open(p + ".gz", "rt") as f:
+        return json.load(f)
 
 
 def gen_dirs():

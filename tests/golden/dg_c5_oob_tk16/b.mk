@@ -1,0 +1,15 @@
+kernel mm_oob {
+  param N;
+  param TK;
+  in a[N * N];
+  in b[N * N];
+  out c[N * N];
+
+  let i = tid / N;
+  let j = tid % N;
+  s = 0;
+  for (k = 0; k < N; k++) {
+    s += a[i * N + k + 1] * b[k * N + j];
+  }
+  c[i * N + j] = s;
+}
