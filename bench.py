@@ -19,7 +19,9 @@ walk the grid. `value` starts each step from the template resident in HBM;
 `e2e` re-uploads the template from pinned host memory every step
 (veq_load_template) and reads every VC back.
 
-  python bench.py [--workload c3|c2|c4] [--gpus N] [--steps K] [--warmup W]
+  c5  1,000 generated kernel variants vs one reference (matmul N=32), one
+      batch per GPU: run, compare (veq_compare_fan), batched slow path
+  python bench.py [--workload c3|c2|c4|c5] [--gpus N] [--steps K] [--warmup W]
                   [--impl ours|reference]
 Multi-GPU: torchrun, one rank per GPU, weak scaling (every rank checks
 `--ctas` CTA pairs per step; rank r takes the grid's CTA ranges r, r + N, ...)
@@ -156,14 +158,62 @@ WORKLOADS = {
 }
 
 
+# C5: a batch of generated kernel variants against one reference kernel
+# (workloads.c5_variants, seeded), each rank taking variants rank, rank + N, ..
+C5_VARIANTS, C5_N = 1000, 32
+# the reference's verdict per variant kind (pinned by tests/test_c5_variants
+# against the reference checker's reports)
+C5_EXPECT = {"tiled": "equivalent", "colmajor": "equivalent", "reverse_k": "equivalent", "unroll2": "equivalent",
+             "nosync": "kernel-B-error", "oob": "kernel-B-error", "index_bug": "not-equivalent",
+             "wrong_guard": "not-equivalent"}
+WORKLOADS["c5"] = dict(
+    fan=True, name=f"C5 batch of {C5_VARIANTS} generated kernel variants vs one reference (matmul N={C5_N}), "
+                   "sharded across GPUs",
+    kernel_a=f"matmul naive (N*N = {C5_N * C5_N} threads)",
+    kernel_b="variants: tiled / column-major / reversed k / unrolled (70%), dropped barrier, index bug, "
+             "wrong guard, out-of-bounds read",
+    ref_what=f"C5 variant pairs in generator order (N={C5_N}), no scaling")
+
+
+def ref_bench_c5(indices, seconds, threads):
+    """The reference checker on variant pairs of the C5 batch (oracle/_ref
+    ref_harness bench with a per-line kernel B)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+    if not os.path.exists(exe):
+        return None, "oracle/_ref/ref_harness not built"
+    variants = workloads.c5_variants(C5_VARIANTS, C5_N)
+    d = tempfile.mkdtemp(prefix="veq_ref_c5_")
+    open(os.path.join(d, "a.mk"), "w").write(workloads.c5_reference(C5_N))
+    lst = []
+    for j in indices:
+        _, src, cfg = variants[j]
+        pc, pb = os.path.join(d, f"cfg_{j}.cfg"), os.path.join(d, f"b_{j}.mk")
+        open(pc, "w").write(cfg)
+        open(pb, "w").write(src)
+        lst.append(f"{pc}\t{pb}")
+    open(os.path.join(d, "list.txt"), "w").write("\n".join(lst) + "\n")
+    out = subprocess.run([exe, "bench", os.path.join(d, "a.mk"), os.path.join(d, "a.mk"),
+                          os.path.join(d, "list.txt"), str(threads), str(seconds)],
+                         capture_output=True, text=True, timeout=seconds * 10 + 120)
+    shutil.rmtree(d, ignore_errors=True)
+    if out.returncode != 0:
+        return None, out.stderr.strip()[-300:]
+    return json.loads(out.stdout.strip().splitlines()[-1]), None
+
+
 def ref_sample(wl, ncpu, seconds, blocks):
-    r, err = ref_bench(wl["ref"](), blocks, seconds, ncpu)
+    if wl.get("fan"):
+        r, err = ref_bench_c5(range(min(C5_VARIANTS, 4 * ncpu)), seconds, ncpu)
+        scale = 1.0
+    else:
+        r, err = ref_bench(wl["ref"](), blocks, seconds, ncpu)
+        scale = wl["ref_scale"]
     if r is None:
         return None, err
     busy = r["busy_s"] / ncpu
     measured = r["elements"] / busy if busy else 0.0
-    return {"value": measured * wl["ref_scale"], "unit": "elements/s", "cores": ncpu, "kind": "reference",
-            "cpu": cpu_model(), "measured_sample_value": measured, "scale_to_config": wl["ref_scale"],
+    return {"value": measured * scale, "unit": "elements/s", "cores": ncpu, "kind": "reference",
+            "cpu": cpu_model(), "measured_sample_value": measured, "scale_to_config": scale,
             "sample": f"{r['pairs']} {wl['ref_what']}; {seconds:.0f}s bound, exec+decide span, all host threads"}, None
 
 
@@ -191,17 +241,27 @@ def main():
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     wl = WORKLOADS[args.workload]
-    W = wl["make"]()
-    cps = args.ctas or wl["ctas"]
-    n_grid = W.n_blocks
-    # default: one pass over the grid (C4: two steps of four full-size CTA
-    # pairs, ~7.5 s each; the whole 256-pair grid takes ~8 min)
-    steps = args.steps or wl.get("steps") or max(1, -(-n_grid // (cps * world)))
-    cfg_json = {"workload": wl["name"], "kernel_a": wl["kernel_a"], "kernel_b": wl["kernel_b"],
-                "cta_pairs_in_grid": n_grid, "cta_pairs_per_step_per_gpu": cps,
-                "elements_per_cta_pair": W.elements_per_block,
-                "parallelism": f"dp{world} (CTA pairs sharded; verdicts combined by the C-ABI NCCL collective)",
-                "l2": "working set re-generated every step (term table cleared, fresh batch; IR > 126 MB L2)"}
+    if wl.get("fan"):
+        W = None
+        steps = args.steps or 3
+        cfg_json = {"workload": wl["name"], "kernel_a": wl["kernel_a"], "kernel_b": wl["kernel_b"],
+                    "variants": C5_VARIANTS, "variants_per_gpu": -(-C5_VARIANTS // world),
+                    "elements_per_variant": C5_N * C5_N,
+                    "parallelism": f"dp{world} (variants sharded; the batch is fixed, so scaling is strong; "
+                                   "verdicts combined by the C-ABI NCCL collective)",
+                    "l2": "working set re-generated every step (term table cleared; IR > 126 MB L2)"}
+    else:
+        W = wl["make"]()
+        cps = args.ctas or wl["ctas"]
+        n_grid = W.n_blocks
+        # default: one pass over the grid (C4: two steps of four full-size CTA
+        # pairs, ~7.5 s each; the whole 256-pair grid takes ~8 min)
+        steps = args.steps or wl.get("steps") or max(1, -(-n_grid // (cps * world)))
+        cfg_json = {"workload": wl["name"], "kernel_a": wl["kernel_a"], "kernel_b": wl["kernel_b"],
+                    "cta_pairs_in_grid": n_grid, "cta_pairs_per_step_per_gpu": cps,
+                    "elements_per_cta_pair": W.elements_per_block,
+                    "parallelism": f"dp{world} (CTA pairs sharded; verdicts combined by the C-ABI NCCL collective)",
+                    "l2": "working set re-generated every step (term table cleared, fresh batch; IR > 126 MB L2)"}
     ncpu = os.cpu_count() or 1
 
     if args.impl == "reference":
@@ -209,10 +269,16 @@ def main():
             return
         per = max(1, min(steps, 5))
         samples = []
-        nb = wl["ref"]().n_blocks
+        nb = C5_VARIANTS if wl.get("fan") else wl["ref"]().n_blocks
+        ref_scale = 1.0 if wl.get("fan") else wl["ref_scale"]
         for st in range(args.warmup + per):
-            blocks = [(st * 8 + k) % nb for k in range(8)]
-            r, err = ref_bench(wl["ref"](), blocks, max(2.0, args.cpu_seconds / per), ncpu)
+            if wl.get("fan"):
+                # C5 pairs take ~10 s each: a window of the generator order
+                r, err = ref_bench_c5([(st * 2 * ncpu + k) % nb for k in range(2 * ncpu)],
+                                      max(2.0, args.cpu_seconds / per), ncpu)
+            else:
+                blocks = [(st * 8 + k) % nb for k in range(8)]
+                r, err = ref_bench(wl["ref"](), blocks, max(2.0, args.cpu_seconds / per), ncpu)
             if r is None:
                 print(json.dumps({"impl": "reference", "unavailable": err}))
                 return
@@ -221,17 +287,21 @@ def main():
         el = sum(r["elements"] for r in samples)
         busy = sum(r["busy_s"] for r in samples) / ncpu
         measured = el / busy if busy > 0 else 0.0
-        v = measured * wl["ref_scale"]
+        v = measured * ref_scale
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": world,
             "steps": per, "warmup": args.warmup, "ms_per_step": 1000.0 * busy / per if per else None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "exact rational (GMP)",
+            "higher_is_better": True, "scaling": "strong" if wl.get("fan") else "weak", "vs_baseline": None,
+            "dtype": "exact rational (GMP)",
             "data": "synthetic", "config": cfg_json,
             "cpu_baseline": {"value": v, "unit": "elements/s", "cores": ncpu, "kind": "reference", "cpu": cpu_model(),
-                             "measured_sample_value": measured, "scale_to_config": wl["ref_scale"],
+                             "measured_sample_value": measured, "scale_to_config": ref_scale,
                              "sample": f"{sum(r['pairs'] for r in samples)} {wl['ref_what']}"},
             "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
+
+    if wl.get("fan"):
+        return main_fan(args, wl, steps, cfg_json, rank, world, local, ncpu)
 
     import numpy as np
     import torch
@@ -430,6 +500,173 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, err = ref_sample(wl, ncpu, args.cpu_seconds, list(range(8)))
+        line["cpu_baseline"] = cb if cb is not None else {
+            "value": None, "unit": "elements/s", "cores": ncpu, "kind": "reference", "sample": f"unavailable: {err}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    sess.close()
+    del pinned
+
+
+def main_fan(args, wl, steps, cfg_json, rank, world, local, ncpu):
+    """C5: every variant of this rank as one batch with the reference kernel
+    (program 0, run once per step), checked by veq_compare_fan and the
+    batched slow path (pipeline.fan_verdicts). A step = run + every
+    variant's verdict; `value` starts from the batch resident in HBM, `e2e`
+    uploads it from pinned host memory every step."""
+    import numpy as np
+    import torch
+    from paper_2511_12638_b200 import dist as D
+    from paper_2511_12638_b200 import frontend, ir, native as N
+    from paper_2511_12638_b200.engine import Session
+    from paper_2511_12638_b200.pipeline import fan_verdicts, out_array_pairs
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    variants = workloads.c5_variants(C5_VARIANTS, C5_N)
+    ref = workloads.c5_reference(C5_N)
+    mine = list(range(rank, C5_VARIANTS, world))
+    m = len(mine)
+    # host frontend, outside the timed region (identical variant sources are
+    # elaborated once; the device batch holds every variant)
+    t0 = time.time()
+    cache, a0, inputs = {}, None, None
+    for j in mine:
+        _, src, cfg = variants[j]
+        if (src, cfg) not in cache:
+            a, b, inp = frontend.elaborate_pair(ref, src, cfg, want_names=False)
+            if a0 is None:
+                a0, inputs = a, inp
+            elif bytes(a.image) != bytes(a0.image) or inp != inputs:
+                raise SystemExit("[bench] C5: the reference kernel must elaborate identically for every variant")
+            cache[(src, cfg)] = b
+    batch = ir.concat([a0] + [cache[(variants[j][1], variants[j][2])] for j in mine])
+    t_elab = time.time() - t0
+    expect = [C5_EXPECT[variants[j][0]] for j in mine]
+    S = len(batch.stmts)
+    sess = Session(local, max_nodes=min((1 << 31) - 1, max(1 << 22, S // 5)),
+                   max_kid_words=min((1 << 32) - 1, (1 << 24) + 4 * S), scratch_bytes=8 << 30)
+    L = N.lib()
+    sess.declare_inputs(inputs)
+    first_b = cache[(variants[mine[0]][1], variants[mine[0]][2])]
+    oa, ob, names = out_array_pairs(a0, first_b, 0)
+    o0 = int(a0.progs[0]["array_off"])
+    sizes = [int(a0.arrays[o0 + k]["size"]) for k in oa]
+    elements_var = sum(sizes)
+    pinned = []
+    for f in ("progs", "thread_stmt", "thread_nregs", "stmts", "arrays", "consts", "syncsets", "set_words"):
+        arr = getattr(batch, f)
+        t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8)).pin_memory()
+        pinned.append(t)
+        setattr(batch, f, t.numpy().view(arr.dtype))
+    h = sess.load(batch)
+    stream = torch.cuda.ExternalStream(L.veq_stream(sess.ctx))
+    use_comm = world > 1 and D.comm_init(sess, rank, world)
+    state = {"bad": 0, "tally": {}}
+
+    step_prof = os.environ.get("VEQ_STEP_PROF") == "1"
+
+    def step(e2e=False):
+        assert L.veq_clear_terms(sess.ctx) == 0
+        t_0 = time.perf_counter()
+        hh = sess.load(batch) if e2e else h
+        r = sess.run_raw(hh)
+        t_1 = time.perf_counter()
+        v = fan_verdicts(sess, hh, 0, 1, m, oa, ob, names, sizes, r, prof=step_prof)
+        if step_prof:
+            print("[step] load+run %.1f ms, verdicts %.1f ms" % (1000 * (t_1 - t_0), 1000 * (time.perf_counter() - t_1)),
+                  file=sys.stderr)
+        launches = r.n_launches + 2
+        if e2e:
+            sess.drop(hh)
+        bad = sum(x != y for x, y in zip(v, expect))
+        state["bad"] += bad
+        for x in v:
+            state["tally"][x] = state["tally"].get(x, 0) + 1
+        if use_comm:
+            D.comm_combine(sess, None if bad == 0 else rank)
+        return launches
+
+    step()  # correctness gate (untimed)
+    if state["bad"]:
+        print(f"[bench] rank {rank}: C5 verdicts differ from the reference's: {state}", file=sys.stderr)
+        sys.exit(1)
+    L.veq_set_timing(sess.ctx, 1)
+    assert L.veq_clear_terms(sess.ctx) == 0
+    r_t = sess.run_raw(h)
+    L.veq_set_timing(sess.ctx, 0)
+    phases = {name: float(r_t.phase_ms[i]) for i, name in enumerate(N.PHASES)}
+    stats = {"S": int(r_t.n_stmts_executed), "R": int(r_t.n_access), "new_nodes": int(r_t.n_new_nodes),
+             "new_kid_words": int(r_t.n_new_kid_words), "work_items": int(r_t.n_work)}
+    for _ in range(args.warmup):
+        step()
+    state.update(bad=0, tally={})
+
+    def timed(fn, k):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launches = 0
+        for _ in range(k):
+            launches += fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, launches
+
+    with ClockSampler(local) as clk:
+        ms, launches = timed(step, steps)
+    tally = dict(state["tally"])
+    if state["bad"]:
+        print(f"[bench] rank {rank}: timed steps: verdicts differ from the reference's: {state}", file=sys.stderr)
+        sys.exit(1)
+    ms_step = ms / steps
+    elements_step = C5_VARIANTS * elements_var  # the whole batch, all ranks
+    value = elements_step / (ms_step / 1000.0)
+    e2e_k = max(1, min(steps, 3))
+    ms_e2e, _ = timed(lambda: step(e2e=True) + 1, e2e_k)
+    e2e_value = elements_step / (ms_e2e / e2e_k / 1000.0)
+    h2d = batch.nbytes()
+    d2h = m * elements_var * 24
+    peak, peak_kind = peaks()
+    U_bytes = 16 * stats["new_nodes"] + 4 * stats["new_kid_words"]
+    alg = {"exec": 16 * stats["S"], "sort": 16 * stats["R"], "memscan": 16 * stats["R"], "eval": 2 * U_bytes}
+    dom = max(phases, key=lambda k: phases[k])
+    dom_bytes = alg.get(dom, 0)
+    achieved = dom_bytes / (phases[dom] / 1000.0) / 1e9 if phases[dom] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "exact rational (int64 num/den), u32 term ids", "data": "synthetic",
+        "config": cfg_json,
+        "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "peak_kind": peak_kind, "alg_bytes_per_launch": dom_bytes},
+        "phases_ms": phases,
+        "counts": dict(stats, t_frontend_s=t_elab, variants_this_rank=m, distinct_sources=len(cache),
+                       verdicts_per_step_rank0={k: v // steps for k, v in tally.items()}),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, err = ref_sample(wl, ncpu, args.cpu_seconds, None)
         line["cpu_baseline"] = cb if cb is not None else {
             "value": None, "unit": "elements/s", "cores": ncpu, "kind": "reference", "sample": f"unavailable: {err}"}
     if rank == 0:

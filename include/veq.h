@@ -322,6 +322,10 @@ typedef struct veq_report {
 } veq_report;
 int veq_batch_locs(veq_ctx *ctx, uint32_t batch, const uint64_t *loc_keys); /* [n_stmts] or NULL */
 int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out);
+/* The same for n programs at once, assembled in parallel on host threads:
+ * outs[q] describes progs[q]; valid until the next veq_run_reports call on
+ * the batch. */
+int veq_run_reports(veq_ctx *ctx, uint32_t batch, const uint32_t *progs, uint32_t n, veq_report *outs);
 /* Members (program-local tids, ascending) of a sync-set id of a report. */
 int veq_set_members(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t set, uint32_t *tids, uint32_t cap,
                     uint32_t *n);
@@ -405,6 +409,16 @@ typedef struct veq_decision {
   const char *g_enclosure;
 } veq_decision;
 int veq_decide(veq_ctx *ctx, uint32_t node_f, uint32_t node_g, uint64_t seed, uint64_t trials, veq_decision *out);
+
+/* veq_decide over n VCs at once (the decide loop of check_equivalence,
+ * pipeline.cpp:222-243, with its OpenMP jobs): every difference canon(f - g)
+ * in one device launch, one DAG export for all of them, then the host
+ * decisions on n_threads threads (0: every hardware thread). kinds[i] is the
+ * kind veq_decide returns for (f[i], g[i], seeds[i], trials); reasons and
+ * witnesses are not kept — call veq_decide for a VC whose payload is
+ * wanted. */
+int veq_decide_batch(veq_ctx *ctx, uint64_t n, const uint32_t *node_f, const uint32_t *node_g, const uint64_t *seeds,
+                     uint64_t trials, uint32_t n_threads, uint32_t *kinds);
 
 /* ---- DAG export (host to_string / slow path / reports) -----------------
  * Exports the sub-DAG reachable from roots in canonical kid order. Nodes are

@@ -9,7 +9,7 @@
 //                                   its full check_equivalence report.
 //   gen   OUTDIR SEED               same for the reference's property-test
 //                                   program generator (tests/prog_gen.hpp).
-//   bench A.mk B.mk CFGLIST THREADS SECONDS
+//   bench A.mk B.mk CFGLIST THREADS SECONDS   (CFGLIST line: cfg [TAB b.mk])
 //                                   CPU baseline: times the reference's own
 //                                   run(A) + run(B) + eq() per CTA pair (the
 //                                   t_exec_a + t_exec_b + t_decide span of
@@ -22,6 +22,7 @@
 #include <fstream>
 #include <iostream>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -330,12 +331,20 @@ int cmd_bench(const std::string &pa_path, const std::string &pb_path, const std:
               unsigned threads, double seconds) {
   std::string sa = read_file(pa_path), sb = read_file(pb_path);
   KernelAst ka = parse_kernel(sa), kb = parse_kernel(sb);
+  // CFGLIST lines: "cfg_path" or "cfg_path<TAB>b_kernel_path" (a batch of
+  // candidate kernels against one reference kernel A, config C5)
   std::vector<std::string> cfgs;
+  std::vector<std::shared_ptr<KernelAst>> kbs;
   {
     std::ifstream in(list_path);
     std::string line;
-    while (std::getline(in, line))
-      if (!line.empty()) cfgs.push_back(read_file(line));
+    while (std::getline(in, line)) {
+      if (line.empty()) continue;
+      const size_t tab = line.find('\t');
+      cfgs.push_back(read_file(line.substr(0, tab)));
+      kbs.push_back(tab == std::string::npos ? nullptr
+                                             : std::make_shared<KernelAst>(parse_kernel(read_file(line.substr(tab + 1)))));
+    }
   }
   struct Job {
     Program pa, pb;
@@ -363,7 +372,7 @@ int cmd_bench(const std::string &pa_path, const std::string &pb_path, const std:
       {
         LaunchConfig c = parse_config(cfgs[i]);
         j.pa = elaborate(ka, c, c.for_a());
-        j.pb = elaborate(kb, c, c.for_b());
+        j.pb = elaborate(kbs[i] ? *kbs[i] : kb, c, c.for_b());
         j.init = make_symbolic_inputs(c, j.pa.arrays);
         for (auto &a : j.pa.arrays)
           if (a.role == Role::Out) j.n_out += a.size;

@@ -7,6 +7,8 @@
 #include <functional>
 #include <random>
 #include <set>
+#include <unordered_map>
+#include <memory>
 #include <stdexcept>
 
 namespace veqdec {
@@ -147,7 +149,7 @@ struct EPS {
     if (c.zero()) return;
     auto [it, ins] = t.try_emplace(k, c);
     if (!ins) {
-      it->second = padd(it->second, c);
+      for (auto &[m, q] : c.t) it->second.add_term(m, q);  // padd in place
       if (it->second.zero()) t.erase(it);
     }
   }
@@ -214,7 +216,15 @@ struct Conv {
   std::map<std::string, uint32_t> vars;
   std::map<uint32_t, std::pair<EPS, EPS>> memo;
   uint32_t var_id(const std::string &n) { return vars.emplace(n, (uint32_t)vars.size()).first->second; }
-  std::pair<EPS, EPS> ratio(uint32_t id) {
+  // a * b; a product with the unit is the other factor (the accumulation in
+  // eps_mul would rebuild it term by term and hit the same budget check)
+  EPS mul(const EPS &a, const EPS &b) {
+    const EPS *x = is_one(a) ? &b : is_one(b) ? &a : nullptr;
+    if (!x) return eps_mul(a, b, budget);
+    if (x->monomials() > budget) throw DecideError("monomial budget exceeded");
+    return *x;
+  }
+  const std::pair<EPS, EPS> &ratio(uint32_t id) {
     if (auto it = memo.find(id); it != memo.end()) return it->second;
     const DNode &n = g.nodes[id];
     std::pair<EPS, EPS> r;
@@ -232,19 +242,19 @@ struct Conv {
       break;
     }
     case K_NEG: {
-      auto k = ratio(n.kids[0]);
+      const auto &k = ratio(n.kids[0]);
       r = {eps_neg(k.first), k.second};
       break;
     }
     case K_ADD: {
       r = {eps_const(Q(0)), one};
       for (uint32_t k : n.kids) {
-        auto x = ratio(k);
+        const auto &x = ratio(k);
         if (is_one(r.second) && is_one(x.second)) {
-          r.first = eps_add(r.first, x.first);
+          for (auto &[key, c] : x.first.t) r.first.add_term(key, c);  // eps_add in place
         } else {
-          r.first = eps_add(eps_mul(r.first, x.second, budget), eps_mul(x.first, r.second, budget));
-          r.second = eps_mul(r.second, x.second, budget);
+          r.first = eps_add(mul(r.first, x.second), mul(x.first, r.second));
+          r.second = mul(r.second, x.second);
         }
       }
       break;
@@ -252,19 +262,20 @@ struct Conv {
     case K_MUL: {
       r = {one, one};
       for (uint32_t k : n.kids) {
-        auto x = ratio(k);
-        r.first = eps_mul(r.first, x.first, budget);
-        r.second = eps_mul(r.second, x.second, budget);
+        const auto &x = ratio(k);
+        r.first = mul(r.first, x.first);
+        r.second = mul(r.second, x.second);
       }
       break;
     }
     case K_DIV: {
-      auto a = ratio(n.kids[0]), b = ratio(n.kids[1]);
-      r = {eps_mul(a.first, b.second, budget), eps_mul(a.second, b.first, budget)};
+      const auto &a = ratio(n.kids[0]);
+      const auto &b = ratio(n.kids[1]);
+      r = {mul(a.first, b.second), mul(a.second, b.first)};
       break;
     }
     case K_EXP: {
-      auto k = ratio(n.kids[0]);
+      const auto &k = ratio(n.kids[0]);
       Q c;
       EPS arg = k.first;
       if (!is_one(k.second)) {
@@ -286,8 +297,7 @@ struct Conv {
     }
     default: throw DecideError("unsupported expression");
     }
-    memo.emplace(id, r);
-    return r;
+    return memo.emplace(id, std::move(r)).first->second;
   }
 };
 
@@ -356,176 +366,6 @@ const Mpfr &mp() {
   return m;
 }
 
-// Closed interval with directed-rounding endpoints; indeterminate absorbs.
-struct Iv {
-  unsigned prec = 64;
-  bool indet = true;
-  mpfr_s lo{}, hi{};
-  bool init = false;
-  Iv() = default;
-  explicit Iv(unsigned p) : prec(p), indet(false), init(true) {
-    mp().init2(&lo, p);
-    mp().init2(&hi, p);
-  }
-  Iv(const Iv &o) : prec(o.prec), indet(o.indet), init(o.init) {
-    if (init) {
-      mp().init2(&lo, prec);
-      mp().init2(&hi, prec);
-      mp().set(&lo, &o.lo, RNDD);
-      mp().set(&hi, &o.hi, RNDU);
-    }
-  }
-  Iv &operator=(const Iv &o) {
-    if (this == &o) return *this;
-    if (init) {
-      mp().clear(&lo);
-      mp().clear(&hi);
-    }
-    prec = o.prec;
-    indet = o.indet;
-    init = o.init;
-    if (init) {
-      mp().init2(&lo, prec);
-      mp().init2(&hi, prec);
-      mp().set(&lo, &o.lo, RNDD);
-      mp().set(&hi, &o.hi, RNDU);
-    }
-    return *this;
-  }
-  ~Iv() {
-    if (init) {
-      mp().clear(&lo);
-      mp().clear(&hi);
-    }
-  }
-  static Iv of_rat(int64_t n, int64_t d, unsigned p) {
-    Iv r(p);
-    // n is exact at >= 64 bits; one correctly rounded division = set_q
-    mp().set_si(&r.lo, (long)n, RNDD);
-    mp().set_si(&r.hi, (long)n, RNDU);
-    if (d != 1) {
-      mp().div_si(&r.lo, &r.lo, (long)d, RNDD);
-      mp().div_si(&r.hi, &r.hi, (long)d, RNDU);
-    }
-    return r;
-  }
-  bool contains_zero() const { return indet || (mp().sgn(&lo) <= 0 && mp().sgn(&hi) >= 0); }
-};
-Iv iv_add(const Iv &a, const Iv &b) {
-  if (a.indet || b.indet) return Iv();
-  Iv r(std::max(a.prec, b.prec));
-  mp().add(&r.lo, &a.lo, &b.lo, RNDD);
-  mp().add(&r.hi, &a.hi, &b.hi, RNDU);
-  if (mp().nan_p(&r.lo) || mp().nan_p(&r.hi)) return Iv();
-  return r;
-}
-template <class Op>
-Iv iv_corners(const Iv &a, const Iv &b, Op op) {
-  Iv r(std::max(a.prec, b.prec));
-  mpfr_s t{};
-  mp().init2(&t, r.prec);
-  const mpfr_s *as[2] = {&a.lo, &a.hi}, *bs[2] = {&b.lo, &b.hi};
-  bool first = true, nan = false;
-  for (int i = 0; i < 2; i++)
-    for (int j = 0; j < 2; j++) {
-      op(&t, as[i], bs[j], RNDD);
-      if (mp().nan_p(&t)) nan = true;
-      if (first || mp().less_p(&t, &r.lo)) mp().set(&r.lo, &t, RNDD);
-      op(&t, as[i], bs[j], RNDU);
-      if (mp().nan_p(&t)) nan = true;
-      if (first || mp().greater_p(&t, &r.hi)) mp().set(&r.hi, &t, RNDU);
-      first = false;
-    }
-  mp().clear(&t);
-  if (nan) return Iv();
-  return r;
-}
-Iv iv_mul(const Iv &a, const Iv &b) {
-  if (a.indet || b.indet) return Iv();
-  return iv_corners(a, b, mp().mul);
-}
-Iv iv_div(const Iv &a, const Iv &b) {
-  if (a.indet || b.indet || b.contains_zero()) return Iv();
-  return iv_corners(a, b, mp().div);
-}
-Iv iv_neg(const Iv &a) {
-  if (a.indet) return Iv();
-  Iv r(a.prec);
-  mp().neg(&r.lo, &a.hi, RNDD);
-  mp().neg(&r.hi, &a.lo, RNDU);
-  return r;
-}
-Iv iv_exp(const Iv &a) {
-  if (a.indet) return Iv();
-  Iv r(a.prec);
-  mp().exp(&r.lo, &a.lo, RNDD);
-  mp().exp(&r.hi, &a.hi, RNDU);
-  return r;
-}
-Iv iv_max(const Iv &a, const Iv &b) {
-  if (a.indet || b.indet) return Iv();
-  Iv r(std::max(a.prec, b.prec));
-  mp().max(&r.lo, &a.lo, &b.lo, RNDD);
-  mp().max(&r.hi, &a.hi, &b.hi, RNDU);
-  return r;
-}
-bool iv_disjoint(const Iv &a, const Iv &b) {
-  if (a.indet || b.indet) return false;
-  return mp().less_p(&a.hi, &b.lo) || mp().less_p(&b.hi, &a.lo);
-}
-std::string iv_str(const Iv &a) {
-  if (a.indet) return "[indeterminate]";
-  char *s = nullptr;
-  mp().asprintf(&s, "[%.17Rg, %.17Rg]", &a.lo, &a.hi);
-  std::string o(s);
-  mp().free_str(s);
-  return o;
-}
-
-// eval_numeric (interval.cpp:221-280): kids folded left to right, memoised
-Iv eval(const Dag &g, uint32_t id, const std::map<std::string, int64_t> &as, unsigned prec,
-        std::map<uint32_t, Iv> &memo) {
-  if (auto it = memo.find(id); it != memo.end()) return it->second;
-  const DNode &n = g.nodes[id];
-  Iv r;
-  switch (n.kind) {
-  case K_CONST: r = Iv::of_rat(n.num, n.den, prec); break;
-  case K_NEGINF:
-    r = Iv(prec);
-    mp().set_inf(&r.lo, -1);
-    mp().set_inf(&r.hi, -1);
-    break;
-  case K_VAR: {
-    auto it = as.find(n.name);
-    if (it == as.end()) throw DecideError("eval_numeric: unassigned variable " + n.name);
-    r = Iv::of_rat(it->second, 1, prec);
-    break;
-  }
-  case K_ADD:
-  case K_MUL:
-  case K_MAX:
-    r = eval(g, n.kids[0], as, prec, memo);
-    for (size_t i = 1; i < n.kids.size(); i++) {
-      const Iv k = eval(g, n.kids[i], as, prec, memo);
-      r = n.kind == K_ADD ? iv_add(r, k) : n.kind == K_MUL ? iv_mul(r, k) : iv_max(r, k);
-    }
-    break;
-  case K_NEG: r = iv_neg(eval(g, n.kids[0], as, prec, memo)); break;
-  case K_DIV: r = iv_div(eval(g, n.kids[0], as, prec, memo), eval(g, n.kids[1], as, prec, memo)); break;
-  case K_EXP: r = iv_exp(eval(g, n.kids[0], as, prec, memo)); break;
-  default: break;
-  }
-  memo.emplace(id, r);
-  return r;
-}
-
-void free_vars(const Dag &g, uint32_t id, std::set<std::string> &out, std::set<uint32_t> &seen) {
-  if (!seen.insert(id).second) return;
-  const DNode &n = g.nodes[id];
-  if (n.kind == K_VAR) out.insert(n.name);
-  for (uint32_t k : n.kids) free_vars(g, k, out, seen);
-}
-
 }  // namespace
 
 bool mpfr_available() { return mp().ok; }
@@ -542,41 +382,358 @@ bool contains_max(const Dag &dag, uint32_t d) {
   return rec(d);
 }
 
+// d a sum of monomials (Add of Const / Var / Mul of Var and Const kids, or
+// one such term): its expansion is those monomials with like terms
+// collected, which is what the exp-polynomial conversion computes for this
+// shape. handled = false for any other shape.
+bool monomial_sum_zero(const Dag &dag, uint32_t d, bool &handled) {
+  handled = false;
+  const DNode &root = dag.nodes[d];
+  std::vector<uint32_t> terms = root.kind == K_ADD ? root.kids : std::vector<uint32_t>{d};
+  std::vector<std::pair<std::vector<uint32_t>, Q>> mono;
+  mono.reserve(terms.size());
+  for (uint32_t t : terms) {
+    const DNode &n = dag.nodes[t];
+    std::vector<uint32_t> vars;
+    Q c(1);
+    auto factor = [&](uint32_t x) {
+      const DNode &k = dag.nodes[x];
+      if (k.kind == K_VAR) vars.push_back(x);
+      else if (k.kind == K_CONST) c = c * Q(k.num, k.den);
+      else return false;
+      return true;
+    };
+    if (n.kind == K_MUL) {
+      for (uint32_t x : n.kids)
+        if (!factor(x)) return false;
+    } else if (!factor(t)) {
+      return false;
+    }
+    std::sort(vars.begin(), vars.end());
+    mono.emplace_back(std::move(vars), c);
+  }
+  handled = true;
+  std::sort(mono.begin(), mono.end(), [](const auto &a, const auto &b) { return a.first < b.first; });
+  for (size_t i = 0; i < mono.size();) {
+    size_t j = i;
+    Q sum(0);
+    for (; j < mono.size() && mono[j].first == mono[i].first; j++) sum = sum + mono[j].second;
+    if (!sum.zero()) return false;
+    i = j;
+  }
+  return true;
+}
+
 bool zero_by_exp_poly(const Dag &dag, uint32_t d, uint64_t max_monomials) {
+  bool handled = false;
+  const bool z = monomial_sum_zero(dag, d, handled);
+  if (handled) return z;
   Conv c{dag, max_monomials, {}, {}};
   return c.ratio(d).first.zero();
 }
 
-bool refute_random(const Dag &dag, uint32_t f, uint32_t g, uint64_t trials, uint64_t seed, Result &w) {
+namespace {
+
+// eval_numeric (interval.cpp:221-280) over closed intervals with directed-
+// rounding MPFR endpoints, indeterminate absorbing: the sub-DAG under f and
+// g in topological (index) order, kids folded left to right, evaluated into
+// per-precision slot buffers without per-operation allocation. f and g share
+// the memo (a node's enclosure depends only on the node).
+struct SubDag {
+  std::vector<uint32_t> ids;                 // reachable node ids, ascending
+  std::vector<std::vector<uint32_t>> kids;   // local kid indices
+  std::vector<int32_t> var;                  // Var: index into the sorted names
+  uint32_t lf = 0, lg = 0;                   // local indices of f and g
+  std::vector<std::string> names;            // free variables, sorted
+};
+
+SubDag make_sub(const Dag &g, uint32_t f, uint32_t h) {
+  SubDag S;
+  // per-thread node marks (generation stamps) instead of per-call sets
+  thread_local std::vector<uint32_t> stamp, pos;
+  thread_local uint32_t gen = 0;
+  if (stamp.size() < g.nodes.size()) {
+    stamp.assign(g.nodes.size(), 0);
+    pos.resize(g.nodes.size());
+    gen = 0;
+  }
+  if (++gen == 0) {
+    std::fill(stamp.begin(), stamp.end(), 0);
+    gen = 1;
+  }
+  std::vector<uint32_t> st{f, h}, seen;
+  while (!st.empty()) {
+    const uint32_t x = st.back();
+    st.pop_back();
+    if (stamp[x] == gen) continue;
+    stamp[x] = gen;
+    seen.push_back(x);
+    for (uint32_t k : g.nodes[x].kids) st.push_back(k);
+  }
+  std::sort(seen.begin(), seen.end());  // post-order export: kids first
+  S.ids = seen;
+  for (uint32_t i = 0; i < seen.size(); i++) pos[seen[i]] = i;
+  for (uint32_t x : seen)
+    if (g.nodes[x].kind == K_VAR) S.names.push_back(g.nodes[x].name);
+  std::sort(S.names.begin(), S.names.end());
+  S.names.erase(std::unique(S.names.begin(), S.names.end()), S.names.end());
+  S.kids.resize(seen.size());
+  S.var.assign(seen.size(), -1);
+  for (uint32_t i = 0; i < seen.size(); i++) {
+    const DNode &n = g.nodes[seen[i]];
+    S.kids[i].reserve(n.kids.size());
+    for (uint32_t k : n.kids) S.kids[i].push_back(pos[k]);
+    if (n.kind == K_VAR)
+      S.var[i] = (int32_t)(std::lower_bound(S.names.begin(), S.names.end(), n.name) - S.names.begin());
+  }
+  S.lf = pos[f];
+  S.lg = pos[h];
+  return S;
+}
+
+// Integer polynomial sub-DAGs (integer Const, Var, Add, Mul, Neg) at an
+// integer point: exact values while every intermediate stays below 2^63 in
+// magnitude. Such values are exact at 64-bit MPFR precision, so the interval
+// evaluation would return exactly these points: the exact evaluation is a
+// shortcut with the same outcome. False: the sub-DAG is not of that shape,
+// or a value left the range (the interval path then runs).
+bool int_poly(const Dag &g, const SubDag &S) {
+  for (uint32_t x : S.ids) {
+    const DNode &n = g.nodes[x];
+    if (!(n.kind == K_VAR || n.kind == K_ADD || n.kind == K_MUL || n.kind == K_NEG ||
+          (n.kind == K_CONST && n.den == 1)))
+      return false;
+  }
+  return true;
+}
+bool eval_int(const Dag &g, const SubDag &S, const std::vector<int64_t> &vals, std::vector<int64_t> &v) {
+  const size_t n = S.ids.size();
+  v.resize(n);
+  const i128 lim = ((i128)1 << 63) - 1;
+  for (size_t i = 0; i < n; i++) {
+    const DNode &nd = g.nodes[S.ids[i]];
+    const std::vector<uint32_t> &k = S.kids[i];
+    i128 r;
+    switch (nd.kind) {
+    case K_CONST: r = nd.num; break;
+    case K_VAR: r = vals[S.var[i]]; break;
+    case K_NEG: r = -(i128)v[k[0]]; break;
+    case K_ADD:
+      r = v[k[0]];
+      for (size_t q = 1; q < k.size(); q++) {
+        r += v[k[q]];
+        if (r > lim || r < -lim) return false;
+      }
+      break;
+    default:  // K_MUL
+      r = v[k[0]];
+      for (size_t q = 1; q < k.size(); q++) {
+        r *= v[k[q]];
+        if (r > lim || r < -lim) return false;
+      }
+      break;
+    }
+    if (r > lim || r < -lim) return false;
+    v[i] = (int64_t)r;
+  }
+  return true;
+}
+
+
+// Interval slots at one precision, grown on demand and reused by a thread.
+struct IvBuf {
+  unsigned prec = 0;
+  std::vector<mpfr_s> lo, hi;
+  std::vector<uint8_t> indet;
+  mpfr_s t{}, nlo{}, nhi{};
+  explicit IvBuf(unsigned p) : prec(p) {
+    mp().init2(&t, p);
+    mp().init2(&nlo, p);
+    mp().init2(&nhi, p);
+  }
+  ~IvBuf() {
+    for (auto &x : lo) mp().clear(&x);
+    for (auto &x : hi) mp().clear(&x);
+    mp().clear(&t);
+    mp().clear(&nlo);
+    mp().clear(&nhi);
+  }
+  void reserve(size_t n) {
+    while (lo.size() < n) {
+      lo.emplace_back();
+      hi.emplace_back();
+      mp().init2(&lo.back(), prec);
+      mp().init2(&hi.back(), prec);
+    }
+    if (indet.size() < n) indet.resize(n);
+  }
+};
+
+IvBuf &iv_buf(unsigned prec) {
+  thread_local std::vector<std::unique_ptr<IvBuf>> bufs;
+  for (auto &b : bufs)
+    if (b->prec == prec) return *b;
+  bufs.push_back(std::make_unique<IvBuf>(prec));
+  return *bufs.back();
+}
+
+// iv_corners into (nlo, nhi) from slots a and b (r may alias a)
+template <class Op>
+bool corners(IvBuf &B, mpfr_s *alo, mpfr_s *ahi, const mpfr_s *blo, const mpfr_s *bhi, Op op) {
+  const mpfr_s *as[2] = {alo, ahi}, *bs[2] = {blo, bhi};
+  bool first = true, nan = false;
+  for (int i = 0; i < 2; i++)
+    for (int j = 0; j < 2; j++) {
+      op(&B.t, as[i], bs[j], RNDD);
+      if (mp().nan_p(&B.t)) nan = true;
+      if (first || mp().less_p(&B.t, &B.nlo)) mp().set(&B.nlo, &B.t, RNDD);
+      op(&B.t, as[i], bs[j], RNDU);
+      if (mp().nan_p(&B.t)) nan = true;
+      if (first || mp().greater_p(&B.t, &B.nhi)) mp().set(&B.nhi, &B.t, RNDU);
+      first = false;
+    }
+  if (nan) return false;
+  mp().set(alo, &B.nlo, RNDD);
+  mp().set(ahi, &B.nhi, RNDU);
+  return true;
+}
+
+void eval_sub(const Dag &g, const SubDag &S, const std::vector<int64_t> &vals, IvBuf &B) {
+  const size_t n = S.ids.size();
+  B.reserve(n);
+  for (size_t i = 0; i < n; i++) {
+    const DNode &nd = g.nodes[S.ids[i]];
+    mpfr_s *lo = &B.lo[i], *hi = &B.hi[i];
+    uint8_t &ind = B.indet[i];
+    ind = 0;
+    auto of_rat = [&](int64_t num, int64_t den) {
+      mp().set_si(lo, (long)num, RNDD);
+      mp().set_si(hi, (long)num, RNDU);
+      if (den != 1) {
+        mp().div_si(lo, lo, (long)den, RNDD);
+        mp().div_si(hi, hi, (long)den, RNDU);
+      }
+    };
+    const std::vector<uint32_t> &k = S.kids[i];
+    switch (nd.kind) {
+    case K_CONST: of_rat(nd.num, nd.den); break;
+    case K_NEGINF:
+      mp().set_inf(lo, -1);
+      mp().set_inf(hi, -1);
+      break;
+    case K_VAR: of_rat(vals[S.var[i]], 1); break;
+    case K_ADD:
+    case K_MUL:
+    case K_MAX: {
+      ind = B.indet[k[0]];
+      mp().set(lo, &B.lo[k[0]], RNDD);
+      mp().set(hi, &B.hi[k[0]], RNDU);
+      for (size_t q = 1; q < k.size() && !ind; q++) {
+        const uint32_t c = k[q];
+        if (B.indet[c]) {
+          ind = 1;
+          break;
+        }
+        if (nd.kind == K_ADD) {
+          mp().add(lo, lo, &B.lo[c], RNDD);
+          mp().add(hi, hi, &B.hi[c], RNDU);
+          if (mp().nan_p(lo) || mp().nan_p(hi)) ind = 1;
+        } else if (nd.kind == K_MUL) {
+          if (!corners(B, lo, hi, &B.lo[c], &B.hi[c], mp().mul)) ind = 1;
+        } else {
+          mp().max(lo, lo, &B.lo[c], RNDD);
+          mp().max(hi, hi, &B.hi[c], RNDU);
+        }
+      }
+      break;
+    }
+    case K_NEG:
+      ind = B.indet[k[0]];
+      if (!ind) {
+        mp().neg(lo, &B.hi[k[0]], RNDD);
+        mp().neg(hi, &B.lo[k[0]], RNDU);
+      }
+      break;
+    case K_DIV: {
+      const uint32_t a = k[0], b = k[1];
+      const bool bz = B.indet[b] || (mp().sgn(&B.lo[b]) <= 0 && mp().sgn(&B.hi[b]) >= 0);
+      ind = B.indet[a] || bz;
+      if (!ind) {
+        mp().set(lo, &B.lo[a], RNDD);
+        mp().set(hi, &B.hi[a], RNDU);
+        if (!corners(B, lo, hi, &B.lo[b], &B.hi[b], mp().div)) ind = 1;
+      }
+      break;
+    }
+    case K_EXP:
+      ind = B.indet[k[0]];
+      if (!ind) {
+        mp().exp(lo, &B.lo[k[0]], RNDD);
+        mp().exp(hi, &B.hi[k[0]], RNDU);
+      }
+      break;
+    default: ind = 1; break;
+    }
+  }
+}
+
+std::string slot_str(IvBuf &B, uint32_t i) {
+  if (B.indet[i]) return "[indeterminate]";
+  char *s = nullptr;
+  mp().asprintf(&s, "[%.17Rg, %.17Rg]", &B.lo[i], &B.hi[i]);
+  std::string o(s);
+  mp().free_str(s);
+  return o;
+}
+
+}  // namespace
+
+bool refute_random(const Dag &dag, uint32_t f, uint32_t g, uint64_t trials, uint64_t seed, Result &w,
+                   bool want_witness) {
   if (!mp().ok) return false;
-  std::set<std::string> names;
-  std::set<uint32_t> seen;
-  free_vars(dag, f, names, seen);
-  free_vars(dag, g, names, seen);
+  const SubDag S = make_sub(dag, f, g);
+  const bool ipoly = int_poly(dag, S);
+  std::vector<int64_t> vals(S.names.size()), iv;
   std::mt19937_64 rng(seed);
   for (uint64_t t = 0; t < trials; ++t) {
-    std::map<std::string, int64_t> a;
     const long box = 1 + (long)(t / 8);
-    for (const std::string &n : names) {
+    for (size_t v = 0; v < vals.size(); v++) {
       if (t == 0) {
-        a[n] = 0;
+        vals[v] = 0;
       } else {
         const unsigned long span = (unsigned long)(2 * box + 1);
-        a[n] = (long)(rng() % span) - box;
+        vals[v] = (long)(rng() % span) - box;
+      }
+    }
+    if (ipoly && eval_int(dag, S, vals, iv)) {
+      // exact values: equal ones are never separated at any precision;
+      // different ones are separated at 64 bits (see int_poly). The interval
+      // pass below still prints a witness (its points carry MPFR's signed
+      // zeros).
+      if (iv[S.lf] == iv[S.lg]) continue;
+      if (!want_witness) {
+        w.precision = 64;
+        return true;
       }
     }
     for (unsigned prec : {64u, 128u, 192u, 256u}) {
-      std::map<uint32_t, Iv> mf, mg;
-      const Iv fi = eval(dag, f, a, prec, mf), gi = eval(dag, g, a, prec, mg);
-      if (fi.indet || gi.indet) continue;
-      if (iv_disjoint(fi, gi)) {
-        w.assignment.clear();
-        for (auto &[n, v] : a) w.assignment.emplace_back(n, std::to_string(v));
-        w.f_enclosure = iv_str(fi);
-        w.g_enclosure = iv_str(gi);
+      IvBuf &B = iv_buf(prec);
+      eval_sub(dag, S, vals, B);
+      const uint32_t a = S.lf, b = S.lg;
+      if (B.indet[a] || B.indet[b]) continue;
+      if (mp().less_p(&B.hi[a], &B.lo[b]) || mp().less_p(&B.hi[b], &B.lo[a])) {
         w.precision = prec;
+        if (!want_witness) return true;
+        w.assignment.clear();
+        for (size_t v = 0; v < vals.size(); v++) w.assignment.emplace_back(S.names[v], std::to_string(vals[v]));
+        w.f_enclosure = slot_str(B, a);
+        w.g_enclosure = slot_str(B, b);
         return true;
       }
+      // both enclosures are the same point: the true values are equal and
+      // no higher precision can separate them
+      auto point = [&](uint32_t x) { return !mp().less_p(&B.lo[x], &B.hi[x]); };
+      if (point(a) && point(b) && !mp().less_p(&B.lo[a], &B.lo[b]) && !mp().less_p(&B.lo[b], &B.lo[a])) break;
     }
   }
   return false;

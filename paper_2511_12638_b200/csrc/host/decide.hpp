@@ -46,7 +46,9 @@ bool contains_max(const Dag &dag, uint32_t d);
 
 // refute_random (decide.cpp:686-718) on f and g; false when MPFR is
 // unavailable or no separating point was found.
-bool refute_random(const Dag &dag, uint32_t f, uint32_t g, uint64_t trials, uint64_t seed, Result &w);
+// want_witness false: only the outcome (and w.precision) is filled.
+bool refute_random(const Dag &dag, uint32_t f, uint32_t g, uint64_t trials, uint64_t seed, Result &w,
+                   bool want_witness = true);
 bool mpfr_available();
 
 }  // namespace veqdec

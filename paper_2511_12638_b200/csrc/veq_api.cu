@@ -7,6 +7,7 @@
 #include <functional>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -14,11 +15,44 @@
 #include <set>
 #include <tuple>
 #include <unordered_map>
+#include <unordered_set>
 #include <string>
 #include <vector>
+#include <atomic>
+#include <thread>
 
-#include "veq_kernels.cuh"
+#include "veq_pipeline.cuh"
 #include "host/decide.hpp"
+
+// Open-addressing set of W-word keys (report identities in veq_run_report):
+// sized once for the number of inserts, no per-key allocation.
+template <int W> struct FlatSet {
+  std::vector<std::array<uint64_t, W>> keys;
+  std::vector<uint8_t> used;
+  uint64_t mask = 0;
+  void init(uint64_t n) {
+    uint64_t cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    keys.assign(cap, {});
+    used.assign(cap, 0);
+    mask = cap - 1;
+  }
+  bool insert(const std::array<uint64_t, W> &k) {
+    uint64_t h = 0x9e3779b97f4a7c15ull;
+    for (int i = 0; i < W; i++) {
+      h = (h ^ k[i]) * 0xff51afd7ed558ccdull;
+      h ^= h >> 32;
+    }
+    for (uint64_t j = h & mask;; j = (j + 1) & mask) {
+      if (!used[j]) {
+        used[j] = 1;
+        keys[j] = k;
+        return true;
+      }
+      if (keys[j] == k) return false;
+    }
+  }
+};
 
 using namespace veqd;
 
@@ -70,9 +104,14 @@ struct BatchDev {
   std::vector<veq_syncset> syncsets;      // host copies for reports (set membership)
   std::vector<uint64_t> set_words;
   // veq_run_report output of the last call
-  std::vector<veq_race_report> rep_races;
-  std::vector<veq_safety_report> rep_safeties;
-  std::vector<veq_thread_report> rep_threads;
+  // veq_run_report / veq_run_reports output (ctx-owned, per call)
+  struct RepStore {
+    std::vector<veq_race_report> races;
+    std::vector<veq_safety_report> safeties;
+    std::vector<veq_thread_report> threads;
+  };
+  RepStore rep;
+  std::vector<RepStore> rep_many;
   std::vector<uint8_t> th_state;
   std::vector<uint32_t> th_bset;
   std::vector<uint64_t> th_bstmt;
@@ -1169,7 +1208,29 @@ int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   if (er) return er;
   if (nf > B.fault_cap) return fail(ctx, VEQ_E_BUDGET, "fault buffer overflow");
   bd->faults.resize(nf);
-  if (nf) CK(cudaMemcpyAsync(bd->faults.data(), B.faults, nf * sizeof(veq_fault), cudaMemcpyDeviceToHost, s));
+  // many faults (racy kernels): ordered on the device before the copy
+  const bool dev_order = nf >= (1u << 14) && B.n_progs < (1u << 23);
+  if (dev_order) {
+    unsigned long long *k1 = nullptr, *k2 = nullptr;
+    uint32_t *i1 = nullptr, *i2 = nullptr;
+    veq_fault *sorted = nullptr;
+    { int r_ = ws_get(ctx, 32, (void **)&k1, nf * 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 33, (void **)&k2, nf * 8); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 34, (void **)&i1, nf * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 35, (void **)&i2, nf * 4); if (r_) return r_; }
+    { int r_ = ws_get(ctx, 36, (void **)&sorted, nf * sizeof(veq_fault)); if (r_) return r_; }
+    k_fault_keys<<<blocks(nf, 256), 256, 0, s>>>(B.faults, nf, k1, i1);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, i1, i2, (int64_t)nf, 0, 63, s);
+    void *tmp = nullptr;
+    { int r_ = ws_get(ctx, 37, &tmp, tb); if (r_) return r_; }
+    cub::DeviceRadixSort::SortPairs(tmp, tb, k1, k2, i1, i2, (int64_t)nf, 0, 63, s);
+    k_fault_gather<<<blocks(nf, 256), 256, 0, s>>>(B.faults, i2, nf, sorted);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(bd->faults.data(), sorted, nf * sizeof(veq_fault), cudaMemcpyDeviceToHost, s));
+  } else if (nf) {
+    CK(cudaMemcpyAsync(bd->faults.data(), B.faults, nf * sizeof(veq_fault), cudaMemcpyDeviceToHost, s));
+  }
   bool any_dead = false;
   for (uint32_t p = 0; p < P; p++) any_dead |= dead[p] != 0;
   // final thread states are per-thread only after a deadlock; otherwise every
@@ -1207,15 +1268,40 @@ int veq_run_finish(veq_ctx *ctx, uint32_t batch, veq_run_out *out) {
   }
   for (const veq_fault &f : bd->faults) bd->res[f.prog].n_faults++;
   // reference order within a program: execution order (step, then the
-  // order of checks inside one statement); programs grouped
-  std::stable_sort(bd->faults.begin(), bd->faults.end(), [](const veq_fault &a, const veq_fault &b) {
-    if (a.prog != b.prog) return a.prog < b.prog;
-    if (a.step != b.step) return a.step < b.step;
-    return a.sub < b.sub;
-  });
+  // order of checks inside one statement); programs grouped. A stable
+  // counting pass by program, then each program's range stable-sorted on
+  // its own (threads when there are many faults): the order of one global
+  // stable sort by (prog, step, sub)
+  const auto tf0 = std::chrono::steady_clock::now();
   bd->prog_fault_off.assign(P + 1, 0);
   for (const veq_fault &f : bd->faults) bd->prog_fault_off[f.prog + 1]++;
   for (uint32_t p = 0; p < P; p++) bd->prog_fault_off[p + 1] += bd->prog_fault_off[p];
+  if (nf && !dev_order) {
+    std::vector<veq_fault> by_prog(nf);
+    std::vector<uint64_t> at(bd->prog_fault_off.begin(), bd->prog_fault_off.end() - 1);
+    for (const veq_fault &f : bd->faults) by_prog[at[f.prog]++] = f;
+    bd->faults.swap(by_prog);
+    auto sort_prog = [&](uint32_t p) {
+      std::stable_sort(bd->faults.begin() + bd->prog_fault_off[p], bd->faults.begin() + bd->prog_fault_off[p + 1],
+                       [](const veq_fault &a, const veq_fault &b) {
+                         if (a.step != b.step) return a.step < b.step;
+                         return a.sub < b.sub;
+                       });
+    };
+    const unsigned nt = nf < (1u << 16) ? 1u : std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::atomic<uint32_t> next{0};
+    auto work = [&]() {
+      for (uint32_t p; (p = next.fetch_add(1)) < P;) sort_prog(p);
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; t++) th.emplace_back(work);
+    work();
+    for (auto &t : th) t.join();
+  }
+  static const bool prof_f = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
+  if (prof_f)
+    fprintf(stderr, "[veq run_finish] faults %llu, order %.1f ms\n", nf,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tf0).count());
   bd->ran = true;
   ctx->last_faults = nf;
   if (out) {
@@ -1867,26 +1953,23 @@ int veq_set_members(veq_ctx *ctx, uint32_t batch, uint32_t prog, uint32_t set, u
   return VEQ_OK;
 }
 
-int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out) {
-  if (!ctx || !live_batch(ctx, batch) || !out) return VEQ_E_ARG;
-  CK(cudaSetDevice(ctx->device));
-  BatchDev *bd = ctx->batches[batch];
-  if (!bd->ran || prog >= bd->progs.size()) return fail(ctx, VEQ_E_ARG, "veq_run_report: no finished run / bad program");
+// One program's RunResult from the ordered raw faults (Collector,
+// symexec.cpp:308-328; make_deadlock_report, 335-365; precedence, 838-845).
+// `st`: the statements of the batch's safety faults (register operands).
+static void assemble_report(BatchDev *bd, uint32_t prog, const std::unordered_map<uint32_t, veq_stmt> &st,
+                            BatchDev::RepStore &R, veq_report *out) {
   const veq_program_meta &pm = bd->progs[prog];
   auto loc = [&](uint32_t stmt) -> uint64_t { return bd->locs.empty() ? stmt : bd->locs[stmt]; };
   const uint64_t f0 = bd->prog_fault_off[prog], f1 = bd->prog_fault_off[prog + 1];
-  // statements of safety faults (register operands), fetched once
-  std::map<uint32_t, veq_stmt> st;
-  for (uint64_t k = f0; k < f1; k++)
-    if (bd->faults[k].type == VEQ_FAULT_SAFETY) st.emplace(bd->faults[k].stmt, veq_stmt{});
-  for (auto &[i, v] : st) CK(cudaMemcpy(&v, bd->B.stmts + i, sizeof(veq_stmt), cudaMemcpyDeviceToHost));
-  bd->rep_races.clear();
-  bd->rep_safeties.clear();
-  bd->rep_threads.clear();
+  R.races.clear();
+  R.safeties.clear();
+  R.threads.clear();
   // Collector (proj/src/symexec.cpp:308-328): distinct reports in order of
   // first occurrence; identity excludes step numbers
-  std::set<std::tuple<uint32_t, int32_t, uint32_t, uint32_t, uint64_t, uint32_t, uint32_t, uint64_t>> rkeys;
-  std::set<std::tuple<uint32_t, uint32_t, uint64_t, uint32_t, int32_t, uint32_t, uint32_t, uint32_t>> skeys;
+  FlatSet<5> rkeys;
+  FlatSet<3> skeys;
+  rkeys.init(f1 - f0);
+  skeys.init(f1 - f0);
   for (uint64_t k = f0; k < f1; k++) {
     const veq_fault &f = bd->faults[k];
     if (f.type == VEQ_FAULT_RACE) {
@@ -1895,9 +1978,10 @@ int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out)
       r.offset = f.offset;
       r.first = veq_access{f.tid2, f.stmt2, f.step2, f.is_write2, 0};
       r.second = veq_access{f.tid, f.stmt, f.step, f.is_write, 0};
-      if (rkeys.emplace(r.arr, r.offset, f.tid2, (uint32_t)f.is_write2, loc(f.stmt2), f.tid, (uint32_t)f.is_write,
-                        loc(f.stmt)).second)
-        bd->rep_races.push_back(r);
+      if (rkeys.insert({((uint64_t)r.arr << 32) | (uint32_t)r.offset,
+                        ((uint64_t)f.tid2 << 32) | ((uint64_t)f.is_write2 << 1) | f.is_write, loc(f.stmt2),
+                        (uint64_t)f.tid, loc(f.stmt)}))
+        R.races.push_back(r);
       continue;
     }
     veq_safety_report s{};
@@ -1907,7 +1991,7 @@ int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out)
     s.step = f.step;
     s.detail = f.detail;
     s.reg = UNSET;
-    const veq_stmt &x = st[f.stmt];
+    const veq_stmt &x = st.at(f.stmt);
     if (f.kind == VEQ_SAFE_UNINIT_REG) {
       s.reg = f.reg_slot == 1 ? x.b : (x.kind == VEQ_ST_STORE ? x.dst : x.a);
     } else if (f.kind == VEQ_SAFE_UNINIT_MEM || f.kind == VEQ_SAFE_OOB) {
@@ -1918,9 +2002,11 @@ int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out)
     } else {
       s.reg = x.dst;  // invalid arithmetic: the destination register
     }
-    if (skeys.emplace(s.kind, s.tid, loc(s.stmt), s.has_addr ? s.arr : s.reg, s.has_addr ? s.offset : 0, s.is_store,
-                      s.detail, s.has_addr).second)
-      bd->rep_safeties.push_back(s);
+    if (skeys.insert({((uint64_t)s.kind << 56) | ((uint64_t)s.detail << 48) | ((uint64_t)s.is_store << 40) |
+                          ((uint64_t)s.has_addr << 32) | s.tid,
+                      loc(s.stmt),
+                      ((uint64_t)(s.has_addr ? s.arr : s.reg) << 32) | (uint32_t)(s.has_addr ? s.offset : 0)}))
+      R.safeties.push_back(s);
   }
   const veq_prog_result &pr = bd->res[prog];
   out->steps = pr.steps;
@@ -1935,15 +2021,15 @@ int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out)
     const uint32_t T = pm.n_threads, g0 = pm.thread_off;
     for (uint32_t t = 0; t < T; t++) {
       const uint8_t sv = bd->th_state[g0 + t];
-      bd->rep_threads.push_back(veq_thread_report{sv, sv == TS_BLOCK ? bd->th_bset[g0 + t] : UNSET,
+      R.threads.push_back(veq_thread_report{sv, sv == TS_BLOCK ? bd->th_bset[g0 + t] : UNSET,
                                                   sv == TS_BLOCK ? (uint32_t)bd->th_bstmt[g0 + t] : UNSET, 0});
     }
     for (uint32_t a = 0; a < T && out->conflict_a < 0; a++) {
-      if (bd->rep_threads[a].state != TS_BLOCK) continue;
-      const uint32_t ia = bd->rep_threads[a].set;
+      if (R.threads[a].state != TS_BLOCK) continue;
+      const uint32_t ia = R.threads[a].set;
       for (uint32_t b = a + 1; b < T; b++) {
-        if (bd->rep_threads[b].state != TS_BLOCK) continue;
-        const uint32_t ib = bd->rep_threads[b].set;
+        if (R.threads[b].state != TS_BLOCK) continue;
+        const uint32_t ib = R.threads[b].set;
         if (ia == ib) continue;  // canonical set ids: equal content <=> equal id
         if (set_has(bd, ia, T, a) && set_has(bd, ia, T, b) && set_has(bd, ib, T, a) && set_has(bd, ib, T, b)) {
           out->conflict_a = (int32_t)a;
@@ -1956,15 +2042,72 @@ int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out)
     }
     out->n_threads = T;
   }
-  out->n_races = bd->rep_races.size();
-  out->races = bd->rep_races.data();
-  out->n_safeties = bd->rep_safeties.size();
-  out->safeties = bd->rep_safeties.data();
-  out->threads = bd->rep_threads.data();
+  out->n_races = R.races.size();
+  out->races = R.races.data();
+  out->n_safeties = R.safeties.size();
+  out->safeties = R.safeties.data();
+  out->threads = R.threads.data();
   // precedence (symexec.cpp:838-845): race, else safety, else deadlock, else final
-  out->outcome = !bd->rep_races.empty() ? VEQ_OUT_RACE
-                 : !bd->rep_safeties.empty() ? VEQ_OUT_SAFETY
+  out->outcome = !R.races.empty() ? VEQ_OUT_RACE
+                 : !R.safeties.empty() ? VEQ_OUT_SAFETY
                  : pr.deadlocked ? VEQ_OUT_DEADLOCK : VEQ_OUT_FINAL;
+}
+
+// The statements of the safety faults of some programs, in one gather.
+static int fetch_fault_stmts(veq_ctx *ctx, BatchDev *bd, const uint32_t *progs, uint32_t n,
+                             std::unordered_map<uint32_t, veq_stmt> &st) {
+  std::vector<uint32_t> ids;
+  for (uint32_t q = 0; q < n; q++)
+    for (uint64_t k = bd->prog_fault_off[progs[q]]; k < bd->prog_fault_off[progs[q] + 1]; k++)
+      if (bd->faults[k].type == VEQ_FAULT_SAFETY && st.emplace(bd->faults[k].stmt, veq_stmt{}).second)
+        ids.push_back(bd->faults[k].stmt);
+  if (ids.empty()) return VEQ_OK;
+  cudaStream_t s = ctx->stream;
+  uint32_t *di = nullptr;
+  veq_stmt *dst = nullptr;
+  { int r_ = ws_get(ctx, 38, (void **)&di, ids.size() * 4); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 39, (void **)&dst, ids.size() * sizeof(veq_stmt)); if (r_) return r_; }
+  CK(cudaMemcpyAsync(di, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, s));
+  k_gather_stmts<<<blocks(ids.size(), 256), 256, 0, s>>>(bd->B.stmts, di, ids.size(), dst);
+  CK(cudaGetLastError());
+  std::vector<veq_stmt> h(ids.size());
+  CK(cudaMemcpyAsync(h.data(), dst, ids.size() * sizeof(veq_stmt), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (size_t k = 0; k < ids.size(); k++) st[ids[k]] = h[k];
+  return VEQ_OK;
+}
+
+int veq_run_report(veq_ctx *ctx, uint32_t batch, uint32_t prog, veq_report *out) {
+  if (!ctx || !live_batch(ctx, batch) || !out) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  if (!bd->ran || prog >= bd->progs.size()) return fail(ctx, VEQ_E_ARG, "veq_run_report: no finished run / bad program");
+  std::unordered_map<uint32_t, veq_stmt> st;
+  if (int r = fetch_fault_stmts(ctx, bd, &prog, 1, st)) return r;
+  assemble_report(bd, prog, st, bd->rep, out);
+  return VEQ_OK;
+}
+
+int veq_run_reports(veq_ctx *ctx, uint32_t batch, const uint32_t *progs, uint32_t n, veq_report *outs) {
+  if (!ctx || !live_batch(ctx, batch) || (n && (!progs || !outs))) return VEQ_E_ARG;
+  CK(cudaSetDevice(ctx->device));
+  BatchDev *bd = ctx->batches[batch];
+  if (!bd->ran) return fail(ctx, VEQ_E_ARG, "veq_run_reports: no finished run");
+  for (uint32_t q = 0; q < n; q++)
+    if (progs[q] >= bd->progs.size()) return fail(ctx, VEQ_E_ARG, "veq_run_reports: bad program");
+  std::unordered_map<uint32_t, veq_stmt> st;
+  if (int r = fetch_fault_stmts(ctx, bd, progs, n, st)) return r;
+  bd->rep_many.resize(n);
+  // programs are independent: assembled on a thread pool
+  const unsigned nt = (unsigned)std::min<uint64_t>(n, std::max(1u, std::thread::hardware_concurrency()));
+  std::atomic<uint32_t> next{0};
+  auto work = [&]() {
+    for (uint32_t q; (q = next.fetch_add(1)) < n;) assemble_report(bd, progs[q], st, bd->rep_many[q], outs + q);
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; t++) th.emplace_back(work);
+  work();
+  for (auto &t : th) t.join();
   return VEQ_OK;
 }
 
@@ -2082,15 +2225,99 @@ int veq_comm_combine(veq_ctx *ctx, uint64_t first_fail_local, veq_combined *out)
   return VEQ_OK;
 }
 
+// The roots' DAG on the host (veq_export_dag, size call then fill) as the
+// decision procedure's Dag; ridx[k] = index of roots[k].
+static int export_to_dag(veq_ctx *ctx, const std::vector<uint32_t> &roots, veqdec::Dag &dag,
+                         std::vector<uint32_t> &ridx) {
+  veq_dag_buf buf{};
+  if (int r = veq_export_dag(ctx, roots.data(), roots.size(), &buf)) return r;
+  std::vector<veq_dag_node> nodes(buf.n_nodes);
+  std::vector<uint32_t> kids(buf.n_kids);
+  ridx.assign(roots.size(), 0);
+  buf.cap_nodes = buf.n_nodes;
+  buf.cap_kids = buf.n_kids;
+  buf.nodes = nodes.data();
+  buf.kids = kids.data();
+  buf.root_index = ridx.data();
+  if (int r = veq_export_dag(ctx, roots.data(), roots.size(), &buf)) return r;
+  dag.nodes.resize(nodes.size());
+  for (size_t i = 0; i < nodes.size(); i++) {
+    const veq_dag_node &n = nodes[i];
+    veqdec::DNode &o = dag.nodes[i];
+    o.kind = (uint8_t)n.kind;
+    o.num = n.num;
+    o.den = n.den;
+    o.kids.assign(kids.begin() + n.kid_off, kids.begin() + n.kid_off + n.nkids);
+    if (n.kind == VEQ_K_VAR) {
+      char hx[32];
+      snprintf(hx, sizeof hx, "%llx", (unsigned long long)n.var_index);
+      o.name = n.var_input >= 0 ? ctx->input_names[n.var_input] + "_" + std::to_string(n.var_index)
+                                : std::string("!undef<") + hx + ">";
+    }
+  }
+  return VEQ_OK;
+}
+
+// Host half of one decision (decide.cpp:749-859 after the fast path) on an
+// exported DAG: f, g, and d = canon(f - g) as DAG indices (have_d false when
+// the difference could not be formed; res.reason then says why). Returns
+// VEQ_EQUAL .. VEQ_UNDECIDED, or -1 when MPFR is missing for a witness.
+static int decide_on_dag(const veqdec::Dag &dag, uint32_t f, uint32_t g, uint32_t d, bool have_d, uint64_t trials,
+                         uint64_t seed, veqdec::Result &res, bool want_witness = true) {
+  using veqdec::DecideError;
+  if (have_d) {
+    const veqdec::DNode &dn = dag.nodes[d];
+    if (dn.kind == VEQ_K_CONST && dn.num == 0) return VEQ_EQUAL;
+    // opaque-max pass: Max subtrees are atoms (decide.cpp:789-813)
+    const bool has_max = veqdec::contains_max(dag, d);
+    bool opaque_done = false;
+    try {
+      if (veqdec::zero_by_exp_poly(dag, d)) return VEQ_EQUAL;
+      opaque_done = true;
+      if (!has_max) res.reason = "difference is a nonzero exp-polynomial";
+    } catch (const DecideError &e) {
+      res.reason = e.what();
+    }
+    if (has_max && (opaque_done || res.reason.empty())) {
+      // The reference now runs the max case split (split_max,
+      // decide.cpp:677-681), which is not restated. A rigorous witness
+      // settles NotEqual regardless of its outcome (it could not have
+      // proved equality); without one the VC stays undecided, not guessed.
+      if (!veqdec::mpfr_available()) return -1;
+      try {
+        if (veqdec::refute_random(dag, f, g, trials, seed, res, want_witness)) return VEQ_NOT_EQUAL;
+      } catch (const DecideError &) {
+      }
+      res.reason = "max case analysis not available";
+      res.assignment.clear();
+      return VEQ_UNDECIDED;
+    }
+  }
+  // no proof of equality: a rigorous separating point (refute_random)
+  if (!veqdec::mpfr_available()) return -1;
+  try {
+    if (veqdec::refute_random(dag, f, g, trials, seed, res, want_witness)) return VEQ_NOT_EQUAL;
+  } catch (const DecideError &e) {
+    res.reason = e.what();
+  }
+  if (res.reason.empty()) res.reason = "no decision within budget";
+  res.reason += "; no separating point found in " + std::to_string(trials) + " trials";
+  return VEQ_UNKNOWN;
+}
+
+static const char *no_diff_reason(uint32_t d) {
+  return d == ~0u ? "cannot form the difference: -inf is not a valid operand of Neg"
+                  : "cannot form the difference: -inf is not a valid operand of Add";
+}
+
 int veq_decide(veq_ctx *ctx, uint32_t f, uint32_t g, uint64_t seed, uint64_t trials, veq_decision *out) {
   if (!ctx || !out) return VEQ_E_ARG;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
-  using veqdec::DecideError;
   veqdec::Result res;
   ctx->dec_reason.clear();
-  auto finish = [&](veqdec::Kind k) {
-    out->kind = k == veqdec::Kind::Equal ? VEQ_EQUAL : k == veqdec::Kind::NotEqual ? VEQ_NOT_EQUAL : VEQ_UNKNOWN;
+  auto finish = [&](int kind) {
+    out->kind = (uint32_t)kind;
     ctx->dec_reason = res.reason;
     ctx->dec_f = res.f_enclosure;
     ctx->dec_g = res.g_enclosure;
@@ -2115,7 +2342,7 @@ int veq_decide(veq_ctx *ctx, uint32_t f, uint32_t g, uint64_t seed, uint64_t tri
     out->precision = res.precision;
     return VEQ_OK;
   };
-  if (f == g) return finish(veqdec::Kind::Equal);
+  if (f == g) return finish(VEQ_EQUAL);
   // d = canon(f - g) on the device (decide.cpp:779-787)
   uint32_t *dd = nullptr;
   { int r_ = ws_get(ctx, 27, (void **)&dd, 16); if (r_) return r_; }
@@ -2128,80 +2355,91 @@ int veq_decide(veq_ctx *ctx, uint32_t f, uint32_t g, uint64_t seed, uint64_t tri
   if (int er = check_error_flag(ctx)) return er;
   // the three DAGs on the host
   veqdec::Dag dag;
-  std::vector<uint32_t> roots{f, g};
+  std::vector<uint32_t> roots{f, g}, ridx;
   const bool have_d = d != ~0u && d != ~1u;
   if (have_d) roots.push_back(d);
-  else res.reason = std::string("cannot form the difference: -inf is not a valid operand of ") + (d == ~0u ? "Neg" : "Add");
-  {
-    veq_dag_buf buf{};
-    if (int r = veq_export_dag(ctx, roots.data(), roots.size(), &buf)) return r;
-    std::vector<veq_dag_node> nodes(buf.n_nodes);
-    std::vector<uint32_t> kids(buf.n_kids), ridx(roots.size());
-    buf.cap_nodes = buf.n_nodes;
-    buf.cap_kids = buf.n_kids;
-    buf.nodes = nodes.data();
-    buf.kids = kids.data();
-    buf.root_index = ridx.data();
-    if (int r = veq_export_dag(ctx, roots.data(), roots.size(), &buf)) return r;
-    dag.nodes.resize(nodes.size());
-    for (size_t i = 0; i < nodes.size(); i++) {
-      const veq_dag_node &n = nodes[i];
-      veqdec::DNode &o = dag.nodes[i];
-      o.kind = (uint8_t)n.kind;
-      o.num = n.num;
-      o.den = n.den;
-      for (uint32_t k = 0; k < n.nkids; k++) o.kids.push_back(kids[n.kid_off + k]);
-      if (n.kind == VEQ_K_VAR) {
-        char hx[32];
-        snprintf(hx, sizeof hx, "%llx", (unsigned long long)n.var_index);
-        o.name = n.var_input >= 0 ? ctx->input_names[n.var_input] + "_" + std::to_string(n.var_index)
-                                  : std::string("!undef<") + hx + ">";
-      }
-    }
-    f = ridx[0];
-    g = ridx[1];
-    if (have_d) d = ridx[2];
+  else res.reason = no_diff_reason(d);
+  if (int r = export_to_dag(ctx, roots, dag, ridx)) return r;
+  const int k = decide_on_dag(dag, ridx[0], ridx[1], have_d ? ridx[2] : 0, have_d, trials, seed, res);
+  if (k < 0) return fail(ctx, VEQ_E_UNSUPPORTED, "libmpfr.so.6 not available for witnesses");
+  return finish(k);
+}
+
+int veq_decide_batch(veq_ctx *ctx, uint64_t n, const uint32_t *f, const uint32_t *g, const uint64_t *seeds,
+                     uint64_t trials, uint32_t n_threads, uint32_t *kinds) {
+  if (!ctx || (n && (!f || !g || !seeds || !kinds))) return VEQ_E_ARG;
+  if (!n) return VEQ_OK;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const auto t0 = std::chrono::steady_clock::now();
+  // every difference in one launch
+  uint32_t *df = nullptr, *dg = nullptr, *dd = nullptr;
+  { int r_ = ws_get(ctx, 29, (void **)&df, n * 4); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 30, (void **)&dg, n * 4); if (r_) return r_; }
+  { int r_ = ws_get(ctx, 31, (void **)&dd, n * 4); if (r_) return r_; }
+  CK(cudaMemcpyAsync(df, f, n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dg, g, n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(ctx->pool_used, 0, 8, s));
+  const uint64_t chunk = std::min<uint64_t>(1ull << 20, std::max<uint64_t>(16ull << 10, ctx->pool_cap / (4 * n)));
+  k_canon_sub_many<<<blocks(n, 128), 128, 0, s>>>(ctx->T, df, dg, dd, n, ctx->pool, ctx->pool_used, ctx->pool_cap,
+                                                   chunk);
+  CK(cudaGetLastError());
+  std::vector<uint32_t> d(n);
+  CK(cudaMemcpyAsync(d.data(), dd, n * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (int er = check_error_flag(ctx)) return er;
+  // one DAG for all of them (shared subterms exported once)
+  std::vector<uint32_t> roots, ridx;
+  roots.reserve(3 * n);
+  for (uint64_t i = 0; i < n; i++) {
+    roots.push_back(f[i]);
+    roots.push_back(g[i]);
+    roots.push_back(d[i] == ~0u || d[i] == ~1u ? f[i] : d[i]);
   }
-  if (have_d) {
-    const veqdec::DNode &dn = dag.nodes[d];
-    if (dn.kind == VEQ_K_CONST && dn.num == 0) return finish(veqdec::Kind::Equal);
-    // opaque-max pass: Max subtrees are atoms (decide.cpp:789-813)
-    const bool has_max = veqdec::contains_max(dag, d);
-    bool opaque_done = false;
-    try {
-      if (veqdec::zero_by_exp_poly(dag, d)) return finish(veqdec::Kind::Equal);
-      opaque_done = true;
-      if (!has_max) res.reason = "difference is a nonzero exp-polynomial";
-    } catch (const DecideError &e) {
-      res.reason = e.what();
-    }
-    if (has_max && (opaque_done || res.reason.empty())) {
-      // The reference now runs the max case split (split_max,
-      // decide.cpp:677-681), which is not restated. A rigorous witness
-      // settles NotEqual regardless of its outcome (it could not have
-      // proved equality); without one the VC stays undecided, not guessed.
-      if (!veqdec::mpfr_available()) return fail(ctx, VEQ_E_UNSUPPORTED, "libmpfr.so.6 not available for witnesses");
+  static const bool prof = getenv("VEQ_PROF") && getenv("VEQ_PROF")[0] == '1';
+  const auto t1 = std::chrono::steady_clock::now();
+  veqdec::Dag dag;
+  if (int r = export_to_dag(ctx, roots, dag, ridx)) return r;
+  const auto t2 = std::chrono::steady_clock::now();
+  // host decisions: independent per VC, on a thread pool
+  unsigned nt = n_threads ? n_threads : std::max(1u, std::thread::hardware_concurrency());
+  nt = (unsigned)std::min<uint64_t>(nt, n);
+  std::atomic<uint64_t> next{0};
+  std::atomic<int> bad{0};
+  auto work = [&]() {
+    for (;;) {
+      const uint64_t i = next.fetch_add(1);
+      if (i >= n) return;
+      if (f[i] == g[i]) {
+        kinds[i] = VEQ_EQUAL;
+        continue;
+      }
+      veqdec::Result res;
+      const bool have_d = d[i] != ~0u && d[i] != ~1u;
+      if (!have_d) res.reason = no_diff_reason(d[i]);
+      int k;
       try {
-        if (veqdec::refute_random(dag, f, g, trials, seed, res)) return finish(veqdec::Kind::NotEqual);
-      } catch (const DecideError &) {
+        k = decide_on_dag(dag, ridx[3 * i], ridx[3 * i + 1], ridx[3 * i + 2], have_d, trials, seeds[i], res, false);
+      } catch (...) {
+        k = -2;
       }
-      res.reason = "max case analysis not available";
-      res.assignment.clear();
-      finish(veqdec::Kind::Unknown);
-      out->kind = VEQ_UNDECIDED;
-      return VEQ_OK;
+      if (k < 0) bad.store(k);
+      kinds[i] = k < 0 ? VEQ_UNKNOWN : (uint32_t)k;
     }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; t++) pool.emplace_back(work);
+  work();
+  for (auto &t : pool) t.join();
+  if (prof) {
+    const auto t3 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[veq decide_batch] n %llu dag nodes %zu | canon+d2h %.1f export %.1f decide %.1f ms on %u threads\n",
+            (unsigned long long)n, dag.nodes.size(), ms(t0, t1), ms(t1, t2), ms(t2, t3), nt);
   }
-  // no proof of equality: a rigorous separating point (refute_random)
-  if (!veqdec::mpfr_available()) return fail(ctx, VEQ_E_UNSUPPORTED, "libmpfr.so.6 not available for witnesses");
-  try {
-    if (veqdec::refute_random(dag, f, g, trials, seed, res)) return finish(veqdec::Kind::NotEqual);
-  } catch (const DecideError &e) {
-    res.reason = e.what();
-  }
-  if (res.reason.empty()) res.reason = "no decision within budget";
-  res.reason += "; no separating point found in " + std::to_string(trials) + " trials";
-  return finish(veqdec::Kind::Unknown);
+  if (bad.load() == -1) return fail(ctx, VEQ_E_UNSUPPORTED, "libmpfr.so.6 not available for witnesses");
+  if (bad.load() == -2) return fail(ctx, VEQ_E_UNSUPPORTED, "veq_decide_batch: host decision failed");
+  return VEQ_OK;
 }
 
 int veq_verdict_counters(veq_ctx *ctx, uint64_t out[4]) {

@@ -231,6 +231,22 @@ class Session:
             v["reason"] = out.reason.decode()
         return v
 
+    def decide_batch(self, f, g, seeds, trials: int = 64, n_threads: int = 0) -> np.ndarray:
+        """Verdict kinds (VERDICT_KIND indices) of many VCs at once
+        (veq_decide_batch): differences in one device launch, host decisions
+        on a thread pool."""
+        f = np.ascontiguousarray(f, dtype=np.uint32)
+        g = np.ascontiguousarray(g, dtype=np.uint32)
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        n = len(f)
+        kinds = np.zeros(max(1, n), dtype=np.uint32)
+        if n:
+            u32p, u64p = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)
+            _check(self.ctx, N.lib().veq_decide_batch(self.ctx, n, f.ctypes.data_as(u32p), g.ctypes.data_as(u32p),
+                                                      sd.ctypes.data_as(u64p), trials, n_threads,
+                                                      kinds.ctypes.data_as(u32p)))
+        return kinds[:n]
+
     def fetch_regs(self, bid: int, prog: int, tid: int) -> np.ndarray:
         """Final register file of one thread (canonical node per register
         id, UNSET = never assigned); needs keep_regs."""
@@ -374,13 +390,18 @@ def build_results(sess: Session, bid: int, b: Batch, out: N.veq_run_out, with_sh
         _check(sess.ctx, L.veq_batch_locs(sess.ctx, bid, keys.ctypes.data_as(C.POINTER(C.c_uint64))))
     results = []
     kinds = {N.OUT_FINAL: "final", N.OUT_RACE: "race", N.OUT_DEADLOCK: "deadlock", N.OUT_SAFETY: "safety"}
-    for p in range(out.n_progs):
+    # every program's report in one call (assembled in parallel)
+    n_p = int(out.n_progs)
+    progs = (C.c_uint32 * max(1, n_p))(*range(n_p))
+    reps = (N.veq_report * max(1, n_p))()
+    if n_p:
+        _check(sess.ctx, L.veq_run_reports(sess.ctx, bid, progs, n_p, reps))
+    for p in range(n_p):
         pm = b.progs[p]
         t_off, a_off = int(pm["thread_off"]), int(pm["array_off"])
         nthr = int(pm["n_threads"])
         aname = lambda a: b.array_names[a_off + int(a)]
-        rep = N.veq_report()
-        _check(sess.ctx, L.veq_run_report(sess.ctx, bid, p, C.byref(rep)))
+        rep = reps[p]
         races, safeties = [], []
         for k in range(rep.n_races):
             r = rep.races[k]

@@ -193,6 +193,7 @@ def lib() -> C.CDLL:
     L.veq_render_digest.argtypes = [vp, P(u32), C.c_size_t, P(u32), P(u64)]
     L.veq_batch_locs.argtypes = [vp, u32, P(u64)]
     L.veq_run_report.argtypes = [vp, u32, u32, P(veq_report)]
+    L.veq_run_reports.argtypes = [vp, u32, P(u32), u32, P(veq_report)]
     L.veq_set_members.argtypes = [vp, u32, u32, u32, P(u32), u32, P(u32)]
     L.veq_set_option.argtypes = [vp, C.c_int, C.c_int]
     L.veq_fetch_regs.argtypes = [vp, u32, u32, u32, P(u32), u32, P(u32)]
@@ -200,6 +201,7 @@ def lib() -> C.CDLL:
     L.veq_comm_init.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
     L.veq_comm_combine.argtypes = [vp, u64, P(veq_combined)]
     L.veq_decide.argtypes = [vp, u32, u32, u64, u64, P(veq_decision)]
+    L.veq_decide_batch.argtypes = [vp, u64, P(u32), P(u32), P(u64), u64, u32, P(u32)]
     for f in ("veq_open", "veq_declare_inputs", "veq_load_batch", "veq_run", "veq_run_start", "veq_run_finish",
               "veq_fetch_cells", "veq_compare", "veq_compare_progs", "veq_compare_fan",
               "veq_export_dag", "veq_verdict_counters", "veq_set_timing", "veq_clear_terms"):
@@ -213,5 +215,5 @@ EXPORTED = ["veq_open", "veq_close", "veq_strerror", "veq_last_error", "veq_decl
             "veq_set_timing", "veq_clear_terms", "veq_stream", "veq_drop_batch", "veq_load_template",
             "veq_instantiate", "veq_drop_template", "veq_render", "veq_render_digest", "veq_batch_locs",
             "veq_run_report", "veq_set_members", "veq_set_option", "veq_fetch_regs", "veq_comm_unique_id",
-            "veq_comm_init", "veq_comm_combine", "veq_decide", "veq_compare_fan"]
+            "veq_comm_init", "veq_comm_combine", "veq_decide", "veq_compare_fan", "veq_decide_batch", "veq_run_reports"]
 PHASES = ["schedule", "exec", "sort", "memscan", "resolve", "chains", "worklist", "eval", "finals"]

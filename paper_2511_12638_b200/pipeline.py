@@ -205,6 +205,92 @@ def check_batches(sess: Session, a: Batch, b: Batch, render_side_conditions: boo
     return reports
 
 
+_SEEDS: Dict[Tuple[Tuple[str, int], ...], "np.ndarray"] = {}
+
+
+def vc_seeds(names: Sequence[str], sizes: Sequence[int]):
+    """fnv1a("array[index]") of every VC of one Out layout (pipeline.cpp:226)."""
+    import numpy as np
+    key = tuple(zip(names, sizes))
+    if key not in _SEEDS:
+        _SEEDS[key] = np.array([fnv1a(f"{n}[{i}]") for n, sz in key for i in range(sz)], dtype=np.uint64)
+    return _SEEDS[key]
+
+
+def fan_verdicts(sess: Session, h: int, prog_a: int, prog_b0: int, m: int, out_a: Sequence[int],
+                 out_b: Sequence[int], names: Sequence[str], sizes: Sequence[int], run_out, trials: int = 64,
+                 reports: bool = True, n_threads: int = 0, prof: bool = False) -> List[str]:
+    """Report verdicts of m candidate programs (prog_b0 ..) against one
+    reference program (prog_a) that ran in the same batch h — a batch of
+    generated kernel variants checked against one reference (config C5) —
+    with the aggregation of check_equivalence (pipeline.cpp:185-265):
+    kernel errors of A, A's missing outputs, kernel errors of B, B's missing
+    outputs, then every VC decided (device fast path; the differing ones in
+    one veq_decide_batch call) and the verdict by precedence not-equivalent >
+    undecided > unknown (or a residual side condition) > equivalent.
+    `reports`: assemble each failing program's run report (veq_run_report,
+    the Collector's ordering and de-duplication) as the reference does."""
+    import ctypes as C
+    import time
+    import numpy as np
+    L = N.lib()
+    tt = [time.perf_counter()]
+    vc = sess.compare_fan_raw(h, prog_a, h, prog_b0, m, out_a, out_b)
+    tt.append(time.perf_counter())
+    n = int(vc.n_vcs)
+    per = n // max(1, m)
+    raw = np.ctypeslib.as_array(C.cast(vc.vcs, C.POINTER(C.c_uint32)), shape=(max(1, n) * 6,))[:n * 6].reshape(n, 6)
+    na, nb, eq = raw[:, 0].copy(), raw[:, 1].copy(), raw[:, 2] != 0
+    sc_off, sc_n = raw[:, 3].astype(np.int64), raw[:, 4].astype(np.int64)
+    n_sc = int(vc.n_sc)
+    undis = (np.ctypeslib.as_array(vc.sc_discharged, shape=(n_sc,)) == 0) if n_sc else np.zeros(0, dtype=bool)
+    cs = np.concatenate([[0], np.cumsum(undis, dtype=np.int64)])
+    vc_resid = (sc_n > 0) & (cs[np.minimum(sc_off + sc_n, n_sc)] - cs[np.minimum(sc_off, n_sc)] > 0)
+    progs = run_out.progs
+
+    def failed(p):
+        return progs[p].n_faults > 0 or progs[p].deadlocked != 0
+
+    a_err = failed(prog_a)
+    miss_a = (na.reshape(m, per) == N.UNSET).any(axis=1)
+    miss_b = (nb.reshape(m, per) == N.UNSET).any(axis=1)
+    verdict: List[Optional[str]] = [None] * m
+    to_report = [prog_a] if a_err else []
+    for j in range(m):
+        if a_err or miss_a[j]:
+            verdict[j] = "kernel-A-error"
+        elif failed(prog_b0 + j):
+            verdict[j] = "kernel-B-error"
+            to_report.append(prog_b0 + j)
+        elif miss_b[j]:
+            verdict[j] = "kernel-B-error"
+    if reports and to_report:
+        # the failing programs' reports, assembled in parallel (veq_run_reports)
+        ps = (C.c_uint32 * len(to_report))(*to_report)
+        outs = (N.veq_report * len(to_report))()
+        st = L.veq_run_reports(sess.ctx, h, ps, len(to_report), outs)
+        if st != 0:
+            raise N.VeqError(st, L.veq_last_error(sess.ctx).decode())
+    tt.append(time.perf_counter())
+    live = np.array([v is None for v in verdict], dtype=bool)
+    idx = np.nonzero(~eq & np.repeat(live, per))[0]
+    kinds = sess.decide_batch(na[idx], nb[idx], vc_seeds(names, sizes)[idx % per], trials, n_threads)
+    tt.append(time.perf_counter())
+    if prof:
+        import sys
+        print("[fan_verdicts] compare %.1f ms, errors/reports %.1f ms, decide_batch (%d VCs) %.1f ms" %
+              (1000 * (tt[1] - tt[0]), 1000 * (tt[2] - tt[1]), len(idx), 1000 * (tt[3] - tt[2])), file=sys.stderr)
+    flag = np.zeros((m, 4), dtype=bool)  # per pair: any kind 1..3 (not_equal, unknown, undecided)
+    for k in (1, 2, 3):
+        flag[idx[kinds == k] // per, k] = True
+    resid = vc_resid.reshape(m, per).any(axis=1)
+    for j in range(m):
+        if verdict[j] is None:
+            verdict[j] = ("not-equivalent" if flag[j, 1] else "undecided" if flag[j, 3]
+                          else "unknown" if (flag[j, 2] or resid[j]) else "equivalent")
+    return verdict
+
+
 def _loc_j(loc):
     return {"line": loc[0], "col": loc[1]}
 

@@ -95,3 +95,73 @@ def test_report_matches_reference(d):
     for k in ("race", "safety", "deadlock", "vcs", "side_conditions", "error"):
         assert got.get(k) == want.get(k), k
     assert json.dumps(got) == json.dumps(want)
+
+
+@pytest.mark.gpu
+def test_fan_verdicts_match_reference():
+    """bench.py's C5 path (reference kernel once + a batch of variants,
+    veq_compare_fan, veq_decide_batch via pipeline.fan_verdicts) on the first
+    160 variants of the batch: every verdict equals the reference's."""
+    from paper_2511_12638_b200 import ir
+    from paper_2511_12638_b200 import native as N
+    from paper_2511_12638_b200.engine import Session
+    from paper_2511_12638_b200.pipeline import fan_verdicts, out_array_pairs
+    verdict = {os.path.basename(d): load_golden(d)["report"]["verdict"] for d in DIRS}
+    variants = workloads.c5_variants(1000, 32)[:160]
+    ref = workloads.c5_reference(32)
+    cache, a0, inputs = {}, None, None
+    for _, src, cfg in variants:
+        if (src, cfg) not in cache:
+            a, b, inputs = frontend.elaborate_pair(ref, src, cfg, want_names=False)
+            a0 = a if a0 is None else a0
+            assert bytes(a.image) == bytes(a0.image)
+            cache[(src, cfg)] = b
+    batch = ir.concat([a0] + [cache[(src, cfg)] for _, src, cfg in variants])
+    S = len(batch.stmts)
+    s = Session(0, max_nodes=max(1 << 22, S // 5), max_kid_words=(1 << 24) + 4 * S, scratch_bytes=4 << 30)
+    try:
+        s.declare_inputs(inputs)
+        h = s.load(batch)
+        oa, ob, names = out_array_pairs(a0, cache[(variants[0][1], variants[0][2])], 0)
+        o0 = int(a0.progs[0]["array_off"])
+        sizes = [int(a0.arrays[o0 + k]["size"]) for k in oa]
+        for _ in range(2):  # the same batch re-run after clearing the term table
+            assert N.lib().veq_clear_terms(s.ctx) == 0
+            r = s.run_raw(h)
+            got = fan_verdicts(s, h, 0, 1, len(variants), oa, ob, names, sizes, r)
+            want = [verdict[_case_name(k, c)] for k, _, c in variants]
+            assert got == want
+    finally:
+        s.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["dg_c5_index_bug_tk4", "dg_c5_wrong_guard_tk8"])
+def test_decide_batch_matches_reference(name):
+    """veq_decide_batch (one device launch for all differences, host
+    decisions on a thread pool) gives every VC the reference's verdict."""
+    import numpy as np
+    from paper_2511_12638_b200 import native as N
+    from paper_2511_12638_b200.engine import Session
+    from paper_2511_12638_b200.pipeline import out_array_pairs, vc_seeds
+    d = os.path.join(GOLDEN, name)
+    g = load_golden(d)
+    a, b, inputs = frontend.elaborate_pair(_src(d, "a.mk"), _src(d, "b.mk"), _src(d, "cfg.cfg"), want_names=False)
+    s = Session(0, max_nodes=1 << 22, max_kid_words=1 << 24, scratch_bytes=1 << 30)
+    try:
+        s.declare_inputs(inputs)
+        ba, bb = s.load(a), s.load(b)
+        s.run_pair_raw(ba, bb)
+        oa, ob, names = out_array_pairs(a, b, 0)
+        vc = s.compare_raw(ba, bb, oa, ob)
+        n = int(vc.n_vcs)
+        f = np.array([vc.vcs[i].node_a for i in range(n)], dtype=np.uint32)
+        gg = np.array([vc.vcs[i].node_b for i in range(n)], dtype=np.uint32)
+        sizes = [int(a.arrays[int(a.progs[0]["array_off"]) + k]["size"]) for k in oa]
+        kinds = s.decide_batch(f, gg, vc_seeds(names, sizes), 64)
+        assert [N.VERDICT_KIND[k] for k in kinds] == [v["verdict"] for v in g["report"]["vcs"]]
+        # single-VC API agrees on a sample
+        for i in (0, n // 2, n - 1):
+            assert s.decide(int(f[i]), int(gg[i]), int(vc_seeds(names, sizes)[i]))["verdict"] == N.VERDICT_KIND[kinds[i]]
+    finally:
+        s.close()
