@@ -838,15 +838,26 @@ __global__ void k_exec(Batch B, Table T) {
   }
 }
 
+// Per-warp shared bit masks of the lanes defining each register in the
+// current 32-statement batch: the last earlier definition of an operand and
+// the last definition of a register are bit scans instead of 32-step
+// shuffle loops (threads with more registers use the loops).
+constexpr uint32_t EXEC_WARP_REGS = 512;
+
 __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
+  __shared__ uint32_t s_defs[4][EXEC_WARP_REGS];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint32_t *dmask = s_defs[(threadIdx.x >> 5) & 3];
+  for (uint32_t r = lane; r < EXEC_WARP_REGS; r += 32) dmask[r] = 0;
+  __syncwarp();
   if (w >= B.n_long) return;
   const uint32_t g = B.long_threads[w];
   const uint32_t p = B.thread_prog[g];
   const veq_program_meta pm = B.progs[p];
   const uint32_t tid = g - pm.thread_off;
   uint32_t *regs = B.regfile + B.reg_off[g];
+  const bool smem_defs = B.reg_off[g + 1] - B.reg_off[g] <= EXEC_WARP_REGS;
   const uint64_t s0 = B.thread_stmt[g], s1 = B.thread_stmt[g + 1];
   const uint64_t j0 = B.seg_off[g], j1 = B.seg_off[g + 1];
   for (uint64_t j = j0; j < j1; j++) {
@@ -886,13 +897,33 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
         if (st.kind == VEQ_ST_BINOP) rb = st.b;
         if (st.kind == VEQ_ST_STORE && !oob) ra = st.dst;
       }
-      // ---- last defining lane before me for each operand
+      // ---- last defining lane before me for each operand, and whether I
+      // am the last definition of my register in this batch
       int la = -1, lb = -1;
-      for (uint32_t k = 0; k < 32; k++) {
-        uint32_t dk = __shfl_sync(kFull, def, k);
-        if (k < lane) {
-          if (dk == ra && ra != UNSET) la = (int)k;
-          if (dk == rb && rb != UNSET) lb = (int)k;
+      bool last_def = def != UNSET;
+      if (smem_defs) {
+        if (def != UNSET) atomicOr(dmask + def, 1u << lane);
+        __syncwarp();
+        const uint32_t below = (1u << lane) - 1u;
+        if (ra != UNSET) {
+          const uint32_t m = dmask[ra] & below;
+          la = m ? 31 - __clz(m) : -1;
+        }
+        if (rb != UNSET) {
+          const uint32_t m = dmask[rb] & below;
+          lb = m ? 31 - __clz(m) : -1;
+        }
+        if (def != UNSET) last_def = (31 - __clz(dmask[def])) == (int)lane;
+        __syncwarp();
+        if (def != UNSET) dmask[def] = 0;
+      } else {
+        for (uint32_t k = 0; k < 32; k++) {
+          uint32_t dk = __shfl_sync(kFull, def, k);
+          if (k < lane) {
+            if (dk == ra && ra != UNSET) la = (int)k;
+            if (dk == rb && rb != UNSET) lb = (int)k;
+          }
+          if (k > lane && dk == def) last_def = false;
         }
       }
       // ---- register-file reads (operands with no earlier def in this batch)
@@ -903,11 +934,13 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
       const uint32_t ua = (ra != UNSET && la < 0 && fa == UNSET) ? ra : UNSET;
       const uint32_t ub = (rb != UNSET && lb < 0 && fb == UNSET) ? rb : UNSET;
       bool first_a = ua != UNSET, first_b = ub != UNSET && ub != ua;
-      for (uint32_t k = 0; k < 32; k++) {
-        uint32_t uak = __shfl_sync(kFull, ua, k), ubk = __shfl_sync(kFull, ub, k);
-        if (k < lane) {
-          if (ua != UNSET && (uak == ua || ubk == ua)) first_a = false;
-          if (ub != UNSET && (uak == ub || ubk == ub)) first_b = false;
+      if (__any_sync(kFull, ua != UNSET || ub != UNSET)) {
+        for (uint32_t k = 0; k < 32; k++) {
+          uint32_t uak = __shfl_sync(kFull, ua, k), ubk = __shfl_sync(kFull, ub, k);
+          if (k < lane) {
+            if (ua != UNSET && (uak == ua || ubk == ua)) first_a = false;
+            if (ub != UNSET && (uak == ub || ubk == ub)) first_b = false;
+          }
         }
       }
       if (ua != UNSET) fa = REF_NODE | intern_undef(T, 0, g, ua);
@@ -997,11 +1030,74 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
           if (st.kind == VEQ_ST_BINOP) B.ref_b[i] = vb;
         }
       }
-      // ---- chain links, decided warp-uniformly in statement order
+      // ---- chain links. In statement order, a chain op continues the
+      // first of its operands that is a chain end of the same operator not
+      // yet continued. Optimistically every lane decides at once against the
+      // state before the batch; if no two lanes claim the same predecessor
+      // that is exactly the sequential outcome, and heads and positions
+      // follow by pointer jumping over the in-batch links. Otherwise the
+      // lanes are decided one by one.
       const bool chain = act && st.kind == VEQ_ST_BINOP && (st.op == VEQ_BIN_ADD || st.op == VEQ_BIN_MAX);
       uint32_t my_head = 0, my_pos = 0;
       uint32_t cont_mask = 0;  // in-batch chain ops already continued
       uint32_t chain_lanes = __ballot_sync(kFull, chain);
+      const uint32_t add_lanes = __ballot_sync(kFull, chain && st.op == VEQ_BIN_ADD);
+      bool chains_done = false;
+      if (chain_lanes) {
+        const uint32_t same = chain ? (st.op == VEQ_BIN_ADD ? add_lanes : chain_lanes & ~add_lanes) : 0u;
+        auto tail0 = [&](uint32_t v) -> bool {  // tail test against the pre-batch state
+          if (!is_stmt_ref(v) || v < s0 || v >= i) return false;
+          if (v >= bt) return (same >> (uint32_t)(v - bt)) & 1u;
+          const veq_stmt sv = B.stmts[v];
+          return sv.kind == VEQ_ST_BINOP && sv.op == st.op && !*((volatile uint8_t *)(B.continued + v));
+        };
+        uint32_t pred = UNSET, leaf = 0;
+        if (chain) {
+          if (tail0(va)) {
+            pred = va;
+            leaf = vb;
+          } else if (tail0(vb)) {
+            pred = vb;
+            leaf = va;
+          }
+        }
+        // a predecessor claimed twice: fall back to the ordered decisions
+        const uint32_t key = pred != UNSET ? pred : (0xFFFFFF00u | lane);
+        const uint32_t peers = __match_any_sync(kFull, key);
+        if (!__any_sync(kFull, __popc(peers) > 1)) {
+          const bool in_b = pred != UNSET && pred >= bt;
+          uint32_t anc = in_b ? (uint32_t)(pred - bt) : lane, dist = in_b ? 1u : 0u;
+          uint32_t head0 = (uint32_t)i, pos0 = 0;
+          if (chain && pred != UNSET && !in_b) {
+            head0 = B.chain_head[pred];
+            pos0 = B.chain_pos[pred] + 1;
+          }
+#pragma unroll
+          for (int r = 0; r < 5; r++) {
+            dist += __shfl_sync(kFull, dist, anc);
+            anc = __shfl_sync(kFull, anc, anc);
+          }
+          const uint32_t head = __shfl_sync(kFull, head0, anc);
+          const uint32_t pos = __shfl_sync(kFull, pos0, anc) + dist;
+          cont_mask = __reduce_or_sync(kFull, in_b ? 1u << (uint32_t)(pred - bt) : 0u);
+          if (chain) {
+            my_head = head;
+            my_pos = pos;
+            B.chain_head[i] = head;
+            B.chain_pos[i] = pos;
+            if (pred != UNSET) {
+              B.ref_a[i] = pred;
+              B.ref_b[i] = leaf;
+              if (!in_b) B.continued[pred] = 1;
+            }
+          }
+          // chain length: the last link of each head in this batch
+          const uint32_t same_head = __match_any_sync(kFull, chain ? head : (0xFFFFFF00u | lane));
+          if (chain && 31 - __clz(same_head) == (int)lane) B.chain_len[head] = pos + 1;
+          chains_done = true;
+        }
+      }
+      if (chains_done) chain_lanes = 0;
       while (chain_lanes) {
         const uint32_t k = __ffs(chain_lanes) - 1;
         chain_lanes &= chain_lanes - 1;
@@ -1067,11 +1163,6 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
       if (first_a) regs[ua] = fa;
       if (first_b) regs[ub] = fb;
       __syncwarp();
-      bool last_def = def != UNSET;
-      for (uint32_t k = 0; k < 32; k++) {
-        uint32_t dk = __shfl_sync(kFull, def, k);
-        if (k > lane && dk == def) last_def = false;
-      }
       if (last_def) regs[def] = val;
       __syncwarp();
     }

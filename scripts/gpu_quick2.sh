@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -3 gpurun_out/pytest_gpu.log
+python -c "
+import json;l=json.load(open('gpurun_out/bench.json'));print(round(l['value']), round(l['ms_per_step'],1), {k:round(v,1) for k,v in l['phases_ms'].items()}, round(l['e2e']['value']))" || tail -3 gpurun_out/bench.err
