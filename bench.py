@@ -367,8 +367,19 @@ def main():
             if step_prof:
                 torch.cuda.synchronize()
                 tt.append(time.perf_counter())
+        if step_prof:
+            torch.cuda.synchronize()
+            tt[0] = time.perf_counter()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(stream)
         assert L.veq_clear_terms(sess.ctx) == 0
+        if step_prof:
+            ev[1].record(stream)
+            t_host = time.perf_counter()
         lap()
+        if step_prof:
+            print("[step] clear: host call %.2f ms, device %.2f ms" % (1000 * (t_host - tt[0]), ev[0].elapsed_time(ev[1])),
+                  file=sys.stderr)
         tu = th_use if th_use is not None else th
         h = sess.instantiate(tu, deltas[blk])
         lap()

@@ -352,6 +352,7 @@ int veq_open(int device, const veq_limits *lim, veq_ctx **out) {
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(VEQ_E_CUDA, "cudaSetDevice");
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(VEQ_E_CUDA, "stream");
+
   if (cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
@@ -941,6 +942,12 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   CK(cudaGetLastError());
   // K3 (direct input loads are interned first, in parallel)
   PH0(VEQ_PH_EXEC);
+  if (S && ctx->T.in_cache) {
+    LAUNCH(k_mark_inputs<<<blocks(S, 256), 256, 0, s>>>(B, ctx->T));
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    LAUNCH(k_intern_marked<<<nsm * 8, 256, 0, s>>>(ctx->T, ctx->in_cells));
+  }
   if (S) LAUNCH(k_pre_inputs<<<blocks(S, 256), 256, 0, s>>>(B, ctx->T));
   // short threads: one CUDA thread each; long threads: one warp each
   // long threads (warp executor) run on the side stream alongside the short
@@ -1009,10 +1016,14 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
   // deferred scaling: products of a used-once sum feeding a chain (k_mark_defer)
   B.prog_split = nullptr;
   if (S && !B.no_defer) {
+    { int r_ = ws_get(ctx, 40, (void **)&B.n_defer_chains, 4); if (r_) return r_; }
+    CK(cudaMemsetAsync(B.n_defer_chains, 0, 4, s));
     LAUNCH(k_mark_defer<<<blocks(S, 256), 256, 0, s>>>(B));
     { int r_ = ws_get(ctx, 28, (void **)&B.prog_split, (uint64_t)B.n_progs * 4); if (r_) return r_; }
     CK(cudaMemsetAsync(B.prog_split, 0xff, (uint64_t)B.n_progs * 4, s));
-    LAUNCH(k_defer_split<<<blocks(S, 256), 256, 0, s>>>(B));
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+    LAUNCH(k_defer_split<<<nsm * 16, 256, 0, s>>>(B));
   }
   PH1(VEQ_PH_RESOLVE);
   CK(cudaGetLastError());

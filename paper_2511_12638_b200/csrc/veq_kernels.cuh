@@ -80,6 +80,7 @@ struct Batch {
   // per program: the first step of an item that expands deferred leaves
   // (k_defer_split); items at or after it form the second eval pass
   uint32_t *prog_split;
+  unsigned int *n_defer_chains;  // chains marked DF_CHAIN by k_mark_defer (0: no second pass)
   uint32_t keep_regs; // 1: final register files are kept and canonicalised (veq_fetch_regs)
   unsigned long long *tup_key, *tup_val;
   unsigned long long *n_tup;

@@ -1350,6 +1350,43 @@ __global__ void k_resolve_regs(Batch B, uint64_t n_regs) {
 // Input symbols read by direct loads (never-stored input arrays) are
 // interned in one parallel pass before execution; the executors read the
 // node from canon[i].
+// Direct input loads, in three passes so each input symbol is interned
+// once: mark the cells the batch reads in the per-cell cache, intern every
+// marked cell (one thread each, no contention on a key), then resolve every
+// load from the cache.
+constexpr uint32_t IN_NEEDED = 0xFFFFFFFEu;
+
+__global__ void k_mark_inputs(Batch B, Table T) {
+  __shared__ uint32_t s_p0;
+  const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x;
+  if (threadIdx.x == 0) s_p0 = prog_of_stmt(B, i0 < B.n_stmts ? i0 : B.n_stmts - 1);
+  __syncthreads();
+  const uint64_t i = i0 + threadIdx.x;
+  if (i >= B.n_stmts) return;
+  const veq_stmt st = B.stmts[i];
+  if (st.kind != VEQ_ST_LOAD) return;
+  const veq_program_meta pm = B.progs[prog_walk(B, s_p0, i)];
+  const veq_array arr = B.arrays[pm.array_off + st.arr];
+  const int32_t off = (int32_t)st.a;
+  if (off < 0 || (uint64_t)off >= arr.size) return;
+  if (!(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 && (uint32_t)off < arr.seeded) {
+    uint32_t *c = T.in_cache + T.in_base[arr.input] + (uint32_t)off;
+    if (__ldcg(c) == UNSET) *c = IN_NEEDED;
+  }
+}
+
+__global__ void k_intern_marked(Table T, uint64_t n_cells) {
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    if (T.in_cache[c] != IN_NEEDED) continue;
+    uint32_t j = 0;
+    while (j + 1 < T.n_inputs && !(c >= T.in_base[j] && c < T.in_base[j] + T.in_size[j])) j++;
+    const uint64_t cell = c - T.in_base[j];
+    const uint64_t key = INPUT_KEY + T.in_base[j] + lexrank(cell, T.in_size[j]);
+    T.in_cache[c] = intern(T, K_VAR, key, ((uint64_t)j << 40) | cell, nullptr, 0);
+  }
+}
+
 __global__ void k_pre_inputs(Batch B, Table T) {
   __shared__ uint32_t s_p0;
   const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x;
@@ -1424,6 +1461,7 @@ __global__ void k_mark_defer(Batch B) {
   set_flag((uint32_t)i, DF_LEAF);
   set_flag(X, DF_SUM);
   set_flag(B.chain_head[u], DF_CHAIN);
+  atomicAdd(B.n_defer_chains, 1u);
 }
 
 // Two-pass evaluation: the deferred expansion (eval_add_deferred) needs a
@@ -1432,11 +1470,14 @@ __global__ void k_mark_defer(Batch B) {
 // carries it. Every dependency of an item is in its program at a smaller
 // step, so pass 1 (steps below the split) never waits on pass 2.
 __global__ void k_defer_split(Batch B) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts || B.st_step[i] == UNSET) return;
-  const veq_stmt st = B.stmts[i];
-  if (!is_chain_op(st) || !(B.defer[B.chain_head[i]] & DF_CHAIN) || !is_work_item(B, i, st)) return;
-  atomicMin(B.prog_split + prog_of_stmt(B, i), B.st_step[i]);
+  if (*B.n_defer_chains == 0) return;  // nothing deferred: one pass
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n_stmts;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (B.st_step[i] == UNSET) continue;
+    const veq_stmt st = B.stmts[i];
+    if (!is_chain_op(st) || !(B.defer[B.chain_head[i]] & DF_CHAIN) || !is_work_item(B, i, st)) continue;
+    atomicMin(B.prog_split + prog_of_stmt(B, i), B.st_step[i]);
+  }
 }
 
 // One pass after the log scan: chain-log entries and the work list.
