@@ -1056,18 +1056,30 @@ int veq_run_start(veq_ctx *ctx, uint32_t batch) {
     // nw = {items, pass-2 items}
     { int r_ = ws_get(ctx, 16, (void **)&nw, 16); if (r_) return r_; }
     CK(cudaMemsetAsync(nw, 0, 16, s));
-    CK(cudaMemsetAsync(wk, 0xff, U * 8, s));
+    // large lists: read the exact item count back (one short wait) and sort
+    // only the items; small ones sort the whole capacity with no host wait
+    // (unused slots keep key ~0 and sort last)
+    const bool exact = U >= (1ull << 22);
+    if (!exact) CK(cudaMemsetAsync(wk, 0xff, U * 8, s));
     LAUNCH(k_scatter_work<<<blocks(S, APP_NT * APP_ITEMS), APP_NT, 0, s>>>(B, base, log, log_stmt, wk, wv, nw));
     void *tmp2 = nullptr;
     n_work = bd->n_arith;
+    uint64_t n_sort = U;
+    if (exact) {
+      unsigned long long h_nw = 0;
+      CK(cudaMemcpyAsync(&h_nw, nw, 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      n_sort = h_nw;
+      n_work = h_nw;
+    }
     if (n_work) {
       // key = pass << (step_bits + prog_bits) | step << prog_bits | program:
       // sort only the bits in use
       const int end_bit = (int)(B.prog_bits + B.step_bits) + (B.prog_split ? 1 : 0);
       size_t tb2 = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
+      cub::DeviceRadixSort::SortPairs(nullptr, tb2, wk, wk2, wv, wv2, (int64_t)n_sort, 0, end_bit, s);
       { int r_ = ws_get(ctx, 17, (void **)&tmp2, tb2); if (r_) return r_; }
-      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)U, 0, end_bit, s);
+      cub::DeviceRadixSort::SortPairs(tmp2, tb2, wk, wk2, wv, wv2, (int64_t)n_sort, 0, end_bit, s);
       ctx->launches += (end_bit + 7) / 8 + 1;
     }
     PH1(VEQ_PH_WORKLIST);

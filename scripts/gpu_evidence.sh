@@ -12,7 +12,7 @@ timeout 900 python bench.py --workload $W --impl reference > gpurun_out/bench_${
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$W.csv \
   python bench.py --workload $W --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_bench_$W.log 2>&1
 for K in $KS; do
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -f -o gpurun_out/prof_${W}_$K \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$K -s ${SKIP:-1} -c 1 -f -o gpurun_out/prof_${W}_$K \
     python bench.py --workload $W --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_full_${W}_$K.log 2>&1
 done
 head -c 400 gpurun_out/bench_$W.json; echo; head -c 300 gpurun_out/bench_${W}_ref.json; tail -2 gpurun_out/bench_$W.err
