@@ -234,9 +234,14 @@ __device__ __forceinline__ int cmp_pref(const Table &T, uint64_t pa, uint32_t a,
 // Lock-free insert-or-find. The node record and kid words are written and
 // fenced before the slot CAS publishes the id; readers go through L2 (ldcg).
 // Merkle hash of a composite: position-salted kid hashes summed, so a warp
-// can compute it with one reduction (kid order still matters).
+// can compute it with one reduction (kid order still matters). A sum's kids
+// are not salted: its hash is a function of the kid multiset, so a sum can
+// be looked up before its terms are sorted (warp_add_smem).
 __device__ __forceinline__ uint64_t kid_term(uint32_t i, uint64_t kid_hash) {
   return mix64(kid_hash + (uint64_t)(i + 1) * 0x9e3779b97f4a7c15ULL);
+}
+__device__ __forceinline__ uint64_t kid_term_k(uint8_t kind, uint32_t i, uint64_t kid_hash) {
+  return kid_term(kind == K_ADD ? 0u : i, kid_hash);
 }
 __device__ __forceinline__ uint64_t composite_hash(uint8_t kind, uint32_t nk, uint64_t sum) {
   return mix64(hcomb(0x100001b3ULL, kind) ^ ((uint64_t)nk * 0xc2b2ae3d27d4eb4fULL) ^ sum);
@@ -273,7 +278,7 @@ __device__ inline uint32_t intern(const Table &T, uint8_t kind, uint64_t p0, uin
     uint64_t sum = 0;
     for (uint32_t i = 0; i < nk; i++) {
       Node kn = ld_node(T, kids[i]);
-      sum += kid_term(i, kn.hash);
+      sum += kid_term_k(kind, i, kn.hash);
       bool pd = kn.flags & F_POSDEF;
       any_pd |= pd;
       all_pd &= pd;

@@ -123,7 +123,7 @@ __device__ inline uint32_t warp_intern(const Table &T, uint8_t kind, const uint3
 #pragma unroll 4
   for (uint32_t i = lane; i < nk; i += 32) {
     Node kn = ld_node(T, kids[i]);
-    sum += kid_term(i, kn.hash);
+    sum += kid_term_k(kind, i, kn.hash);
     bool pd = kn.flags & F_POSDEF;
     any_pd |= pd;
     all_pd &= pd;
@@ -264,7 +264,7 @@ __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32
   bool pd = true, dv = false, k0c = false, cf = false;
   if (lane < m) {
     Node kn = ld_node(T, kid);
-    term = kid_term(lane, kn.hash);
+    term = kid_term_k(kind, lane, kn.hash);
     pd = kn.flags & F_POSDEF;
     dv = (kn.flags & F_HASDIV) != 0;
     cf = (kn.flags & F_COEF) != 0;
@@ -277,7 +277,7 @@ __device__ inline uint32_t warp_intern_regs(const Table &T, uint8_t kind, uint32
                             nullptr, nullptr, cf);
 }
 
-// Same, with each lane's kid term hash (kid_term(lane, hash)) and flags
+// Same, with each lane's kid term hash (kid_term_k(kind, lane, hash)) and flags
 // already known; p1 = composite prefix, k0c = kid 0 is a Const.
 __device__ inline uint32_t warp_intern_regs_h(const Table &T, uint8_t kind, uint32_t kid, uint32_t m, uint64_t term,
                                               bool pd, bool dv, uint64_t p1, bool k0c, WarpAlloc *W,
@@ -629,7 +629,7 @@ __device__ inline uint32_t warp_add_lean(const Table &T, uint32_t leaf, uint32_t
   const uint64_t k0p = __shfl_sync(kFull, key, 0);
   const bool k0c = __shfl_sync(kFull, (uint32_t)(key == 0), 0);
   long long c2 = ph ? clock64() : 0;
-  const uint32_t res = warp_intern_regs_h(T, K_ADD, id, real, kid_term(lane, kh), kf & F_POSDEF, (kf & F_HASDIV) != 0,
+  const uint32_t res = warp_intern_regs_h(T, K_ADD, id, real, kid_term_k(K_ADD, lane, kh), kf & F_POSDEF, (kf & F_HASDIV) != 0,
                                           composite_prefix(K_ADD, real, k0p), k0c, W, created);
   if (ph && lane == 0) {
     long long c3 = clock64();
@@ -804,6 +804,66 @@ __device__ inline uint32_t warp_add_smem(const Table &T, char *buf, uint32_t n, 
     if (__any_sync(kFull, dup)) return UNSET;
   }
   if (ph) c2 = clock64();
+  // 3b. the sum may already exist (the other kernel of the pair usually
+  // built it): its hash depends only on the term multiset, so look it up
+  // before sorting. A candidate matches when our terms are distinct and
+  // every one of its m kids is among them.
+  if (!coef && nconst == 0 && m >= 2) {
+    uint64_t sum = 0;
+    for (uint32_t t = lane; t < m; t += 32) sum += kid_term(0, ld_hash(T, idA[pz(t)]));
+    const uint64_t h = composite_hash(K_ADD, m, warp_sum_u64(sum));
+    uint32_t *set = reinterpret_cast<uint32_t *>(Y);
+    for (uint32_t i = lane; i < H; i += 32) set[i] = EMPTY;
+    __syncwarp();
+    bool dup = false;
+    for (uint32_t t = lane; t < m; t += 32) {
+      const uint32_t id = idA[pz(t)];
+      for (uint32_t sl = (uint32_t)mix64(id) & (H - 1);; sl = (sl + 1) & (H - 1)) {
+        const uint32_t prev = atomicCAS(set + sl, EMPTY, id);
+        if (prev == EMPTY) break;
+        if (prev == id) {
+          dup = true;
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (!__any_sync(kFull, dup)) {
+      uint64_t slot = h & T.slot_mask;
+      for (uint64_t probes = 0; probes <= T.slot_mask; probes++) {
+        uint32_t cur = EMPTY;
+        uint64_t ch = 0;
+        if (lane == 0) {
+          cur = *((volatile uint32_t *)(T.slots + slot));
+          if (cur != EMPTY) ch = ld_hash(T, cur);
+        }
+        cur = __shfl_sync(kFull, cur, 0);
+        if (cur == EMPTY) break;
+        if (__shfl_sync(kFull, ch, 0) == h) {
+          const Node c = ld_node(T, cur);
+          if (c.kind == K_ADD && c.nkids == m) {
+            bool all_in = true;
+            for (uint32_t k = lane; k < m && all_in; k += 32) {
+              const uint32_t kid = ld_kid(T, c.p0 + k);
+              bool in = false;
+              for (uint32_t sl = (uint32_t)mix64(kid) & (H - 1);; sl = (sl + 1) & (H - 1)) {
+                const uint32_t v = set[sl];
+                if (v == kid) {
+                  in = true;
+                  break;
+                }
+                if (v == EMPTY) break;
+              }
+              all_in = in;
+            }
+            if (__all_sync(kFull, all_in)) return cur;
+          }
+        }
+        slot = (slot + 1) & T.slot_mask;
+      }
+    }
+    __syncwarp();
+  }
   // 4. merge the sorted leaf runs pairwise until one run remains
   uint32_t R = n;
   uint64_t *ps = preA, *pd = preB;
