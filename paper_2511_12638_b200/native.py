@@ -145,6 +145,10 @@ class veq_dag_buf(C.Structure):
                 ("root_index", P(u32)), ("n_nodes", u64), ("n_kids", u64)]
 
 
+# status codes (include/veq.h)
+OK, E_BUDGET, E_RATIONAL_OVERFLOW, E_OOM, E_INVALID_IR, E_CUDA, E_ARG, E_UNSUPPORTED, E_NO_DEVICE, E_SCRATCH = range(10)
+
+
 class VeqError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"veq error {status}: {msg}")

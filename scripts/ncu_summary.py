@@ -54,7 +54,10 @@ def one_step(ls):
 
 def raw_metrics(rep):
     """One dict per captured launch: metric -> (unit, value)."""
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # raw page already exported on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return [{k: (u, v) for k, u, v in zip(r[0], r[1], row)} for row in r[2:]]
 
@@ -102,12 +105,17 @@ def main():
         v = float(v.replace(",", "") or 0)
         return v * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}.get(u, 1.0)
     # per launch (= per step with merged batches): mean over the captured launches
-    traffic = sum(num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum") for m in ms) / max(1, len(ms))
+    # "--sum": the captured launches are the kernels of ONE step (e.g. both
+    # evaluation passes), so their traffic adds up
+    per_step = "--sum" in sys.argv
+    traffic = sum(num(m, "dram__bytes_read.sum") + num(m, "dram__bytes_write.sum") for m in ms) / (
+        1 if per_step else max(1, len(ms)))
     tp = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
     t = json.load(open(tp)) if os.path.exists(tp) else {}
     t[phase] = traffic
     t[f"{phase}_source"] = (f"profiles/{tag}_{phase}_ncu.md (dram__bytes_read.sum + dram__bytes_write.sum, "
-                            f"per launch, mean of {len(ms)} launches)")
+                            + (f"summed over the {len(ms)} launches of one step)" if per_step
+                               else f"per launch, mean of {len(ms)} launches)"))
     json.dump(t, open(tp, "w"), indent=1)
     print(open(os.path.join(ROOT, "profiles", f"{tag}_launches.md")).read())
     print(open(os.path.join(ROOT, "profiles", f"{tag}_{phase}_ncu.md")).read())
