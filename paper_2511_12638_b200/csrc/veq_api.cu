@@ -1842,27 +1842,38 @@ int veq_instantiate(veq_ctx *ctx, uint32_t tmpl, uint32_t n_inst, const int32_t 
   const uint32_t Q = (uint32_t)t.progs.size(), NA = (uint32_t)t.arrays.size();
   // program-major expansion: program q * n_inst + i is template program q of
   // instance i, so each template program's instances form one range
-  std::vector<veq_program_meta> progs;
-  std::vector<uint64_t> thread_stmt{0};
-  std::vector<uint32_t> thread_nregs;
-  std::vector<veq_array> arrays;
+  // sized up front and filled by block copies: every instance of template
+  // program q repeats q's thread table shifted by a constant
+  uint64_t n_thr = 0, n_arr = 0;
+  for (uint32_t q = 0; q < Q; q++) {
+    n_thr += (uint64_t)t.progs[q].n_threads * n_inst;
+    n_arr += (uint64_t)t.progs[q].n_arrays * n_inst;
+  }
+  if (n_thr >= (1ull << 32)) return fail(ctx, VEQ_E_UNSUPPORTED, "instantiated batch has more than 2^32 threads");
+  std::vector<veq_program_meta> progs((size_t)Q * n_inst);
+  std::vector<uint64_t> thread_stmt(n_thr + 1);
+  std::vector<uint32_t> thread_nregs(n_thr);
+  std::vector<veq_array> arrays(n_arr);
   std::vector<ExpandSeg> segs;
-  uint64_t so = 0;
+  uint64_t so = 0, to = 0, ao = 0;
+  thread_stmt[0] = 0;
   for (uint32_t q = 0; q < Q; q++) {
     const veq_program_meta &m = t.progs[q];
     const uint64_t s0 = t.thread_stmt[m.thread_off], s1 = t.thread_stmt[m.thread_off + m.n_threads];
     segs.push_back(ExpandSeg{so, s0, s1 - s0, m.array_off});
+    const uint64_t *ts = t.thread_stmt.data() + m.thread_off;
     for (uint32_t i = 0; i < n_inst; i++) {
       veq_program_meta pm = m;
-      pm.thread_off = (uint32_t)thread_nregs.size();
-      pm.array_off = (uint32_t)arrays.size();
-      progs.push_back(pm);
-      for (uint32_t k = 0; k < m.n_threads; k++) {
-        const uint32_t g = m.thread_off + k;
-        thread_nregs.push_back(t.thread_nregs[g]);
-        thread_stmt.push_back(thread_stmt.back() + (t.thread_stmt[g + 1] - t.thread_stmt[g]));
-      }
-      for (uint32_t a = 0; a < m.n_arrays; a++) arrays.push_back(t.arrays[m.array_off + a]);
+      pm.thread_off = (uint32_t)to;
+      pm.array_off = (uint32_t)ao;
+      progs[(size_t)q * n_inst + i] = pm;
+      std::copy(t.thread_nregs.begin() + m.thread_off, t.thread_nregs.begin() + m.thread_off + m.n_threads,
+                thread_nregs.begin() + to);
+      const uint64_t shift = so + (s1 - s0) * i - s0;  // instance i's first statement, minus the template's
+      for (uint32_t k = 1; k <= m.n_threads; k++) thread_stmt[to + k] = ts[k] + shift;
+      std::copy(t.arrays.begin() + m.array_off, t.arrays.begin() + m.array_off + m.n_arrays, arrays.begin() + ao);
+      to += m.n_threads;
+      ao += m.n_arrays;
     }
     so += (s1 - s0) * n_inst;
   }
