@@ -838,18 +838,22 @@ __global__ void k_exec(Batch B, Table T) {
   }
 }
 
-// Per-warp shared bit masks of the lanes defining each register in the
-// current 32-statement batch: the last earlier definition of an operand and
-// the last definition of a register are bit scans instead of 32-step
-// shuffle loops (threads with more registers use the loops).
-constexpr uint32_t EXEC_WARP_REGS = 512;
+// Per-warp shared table of the registers defined in the current
+// 32-statement batch (at most 32, open addressing over 128 slots): register
+// id -> mask of the defining lanes. The last earlier definition of an
+// operand and the last definition of a register are then bit scans instead
+// of 32-step shuffle loops, for any register count.
+constexpr uint32_t EXEC_DEF_SLOTS = 128;
 
 __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
-  __shared__ uint32_t s_defs[4][EXEC_WARP_REGS];
+  __shared__ uint32_t s_key[4][EXEC_DEF_SLOTS], s_mask[4][EXEC_DEF_SLOTS];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  uint32_t *dmask = s_defs[(threadIdx.x >> 5) & 3];
-  for (uint32_t r = lane; r < EXEC_WARP_REGS; r += 32) dmask[r] = 0;
+  uint32_t *dkey = s_key[(threadIdx.x >> 5) & 3], *dmask = s_mask[(threadIdx.x >> 5) & 3];
+  for (uint32_t r = lane; r < EXEC_DEF_SLOTS; r += 32) {
+    dkey[r] = UNSET;
+    dmask[r] = 0;
+  }
   __syncwarp();
   if (w >= B.n_long) return;
   const uint32_t g = B.long_threads[w];
@@ -857,7 +861,14 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
   const veq_program_meta pm = B.progs[p];
   const uint32_t tid = g - pm.thread_off;
   uint32_t *regs = B.regfile + B.reg_off[g];
-  const bool smem_defs = B.reg_off[g + 1] - B.reg_off[g] <= EXEC_WARP_REGS;
+  auto def_slot = [&](uint32_t r) { return (r * 0x9E3779B1u) >> 25; };  // 7 bits
+  auto def_lanes = [&](uint32_t r) -> uint32_t {  // lanes of this batch defining r
+    for (uint32_t sl = def_slot(r);; sl = (sl + 1) & (EXEC_DEF_SLOTS - 1)) {
+      const uint32_t k = dkey[sl];
+      if (k == r) return dmask[sl];
+      if (k == UNSET) return 0u;
+    }
+  };
   const uint64_t s0 = B.thread_stmt[g], s1 = B.thread_stmt[g + 1];
   const uint64_t j0 = B.seg_off[g], j1 = B.seg_off[g + 1];
   for (uint64_t j = j0; j < j1; j++) {
@@ -889,6 +900,9 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
         direct = !oob && st.kind == VEQ_ST_LOAD && !(arr.flags & VEQ_ARR_STORED) && arr.input >= 0 &&
                  (uint32_t)off < arr.seeded;
       }
+      // a direct load's symbol (interned by k_pre_inputs), fetched early so
+      // the load overlaps the bookkeeping below
+      const uint32_t in_node = direct ? __ldcg(B.canon + i) : UNSET;
       const uint32_t def = (act && defines_reg(st.kind)) ? st.dst : UNSET;
       // operand registers (UNSET: none). An out-of-bounds store reads nothing.
       uint32_t ra = UNSET, rb = UNSET;
@@ -901,30 +915,35 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
       // am the last definition of my register in this batch
       int la = -1, lb = -1;
       bool last_def = def != UNSET;
-      if (smem_defs) {
-        if (def != UNSET) atomicOr(dmask + def, 1u << lane);
+      {
+        uint32_t my_slot = UNSET;
+        if (def != UNSET) {
+          for (uint32_t sl = def_slot(def);; sl = (sl + 1) & (EXEC_DEF_SLOTS - 1)) {
+            const uint32_t prev = atomicCAS(dkey + sl, UNSET, def);
+            if (prev == UNSET || prev == def) {
+              atomicOr(dmask + sl, 1u << lane);
+              my_slot = sl;
+              break;
+            }
+          }
+        }
         __syncwarp();
         const uint32_t below = (1u << lane) - 1u;
         if (ra != UNSET) {
-          const uint32_t m = dmask[ra] & below;
+          const uint32_t m = def_lanes(ra) & below;
           la = m ? 31 - __clz(m) : -1;
         }
         if (rb != UNSET) {
-          const uint32_t m = dmask[rb] & below;
+          const uint32_t m = def_lanes(rb) & below;
           lb = m ? 31 - __clz(m) : -1;
         }
-        if (def != UNSET) last_def = (31 - __clz(dmask[def])) == (int)lane;
+        if (def != UNSET) last_def = (31 - __clz(dmask[my_slot])) == (int)lane;
         __syncwarp();
-        if (def != UNSET) dmask[def] = 0;
-      } else {
-        for (uint32_t k = 0; k < 32; k++) {
-          uint32_t dk = __shfl_sync(kFull, def, k);
-          if (k < lane) {
-            if (dk == ra && ra != UNSET) la = (int)k;
-            if (dk == rb && rb != UNSET) lb = (int)k;
-          }
-          if (k > lane && dk == def) last_def = false;
+        if (my_slot != UNSET) {
+          dkey[my_slot] = UNSET;
+          dmask[my_slot] = 0;
         }
+        __syncwarp();
       }
       // ---- register-file reads (operands with no earlier def in this batch)
       uint32_t fa = UNSET, fb = UNSET;
@@ -973,7 +992,7 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
         case VEQ_ST_UNOP: val = (uint32_t)i; break;
         case VEQ_ST_LOAD:
           if (oob) val = REF_NODE | intern_undef(T, 1, ga, (uint64_t)(uint32_t)off);
-          else if (direct) val = REF_NODE | B.canon[i];  // interned by k_pre_inputs
+          else if (direct) val = REF_NODE | in_node;
           else val = (uint32_t)i;
           break;
         default: break;  // copy
