@@ -871,6 +871,12 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
   };
   const uint64_t s0 = B.thread_stmt[g], s1 = B.thread_stmt[g + 1];
   const uint64_t j0 = B.seg_off[g], j1 = B.seg_off[g + 1];
+  // the previous batch's chain state, lane k describing statement
+  // pv_bt + k: operator (0xFF: not a chain op), continued at batch end,
+  // head and position. Links into the previous batch read these registers.
+  uint64_t pv_bt = ~0ull;
+  uint32_t pv_n = 0, pv_op = 0xFFu, pv_head = 0, pv_pos = 0;
+  bool pv_cont = false;
   for (uint64_t j = j0; j < j1; j++) {
     const uint32_t base = B.seg_base[j];
     if (base == UNSET) break;  // segment never ran (deadlock)
@@ -1064,18 +1070,24 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
       bool chains_done = false;
       if (chain_lanes) {
         const uint32_t same = chain ? (st.op == VEQ_BIN_ADD ? add_lanes : chain_lanes & ~add_lanes) : 0u;
-        auto tail0 = [&](uint32_t v) -> bool {  // tail test against the pre-batch state
+        auto in_prev = [&](uint32_t v) { return is_stmt_ref(v) && pv_bt != ~0ull && v >= pv_bt && v < pv_bt + pv_n; };
+        // the previous batch's state of both operands (all lanes shuffle)
+        const uint32_t sa = in_prev(va) ? (uint32_t)(va - pv_bt) : lane, sb = in_prev(vb) ? (uint32_t)(vb - pv_bt) : lane;
+        const uint32_t opa = __shfl_sync(kFull, pv_op, sa), opb = __shfl_sync(kFull, pv_op, sb);
+        const bool cna = __shfl_sync(kFull, pv_cont, sa), cnb = __shfl_sync(kFull, pv_cont, sb);
+        auto tail0 = [&](uint32_t v, uint32_t pop, bool pcont) -> bool {  // against the pre-batch state
           if (!is_stmt_ref(v) || v < s0 || v >= i) return false;
           if (v >= bt) return (same >> (uint32_t)(v - bt)) & 1u;
+          if (in_prev(v)) return pop == st.op && !pcont;
           const veq_stmt sv = B.stmts[v];
           return sv.kind == VEQ_ST_BINOP && sv.op == st.op && !*((volatile uint8_t *)(B.continued + v));
         };
         uint32_t pred = UNSET, leaf = 0;
         if (chain) {
-          if (tail0(va)) {
+          if (tail0(va, opa, cna)) {
             pred = va;
             leaf = vb;
-          } else if (tail0(vb)) {
+          } else if (tail0(vb, opb, cnb)) {
             pred = vb;
             leaf = va;
           }
@@ -1087,9 +1099,12 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
           const bool in_b = pred != UNSET && pred >= bt;
           uint32_t anc = in_b ? (uint32_t)(pred - bt) : lane, dist = in_b ? 1u : 0u;
           uint32_t head0 = (uint32_t)i, pos0 = 0;
+          const bool pp = chain && pred != UNSET && !in_b && in_prev(pred);
+          const uint32_t sp = pp ? (uint32_t)(pred - pv_bt) : lane;
+          const uint32_t ph = __shfl_sync(kFull, pv_head, sp), ppos = __shfl_sync(kFull, pv_pos, sp);
           if (chain && pred != UNSET && !in_b) {
-            head0 = B.chain_head[pred];
-            pos0 = B.chain_pos[pred] + 1;
+            head0 = pp ? ph : B.chain_head[pred];
+            pos0 = (pp ? ppos : B.chain_pos[pred]) + 1;
           }
 #pragma unroll
           for (int r = 0; r < 5; r++) {
@@ -1178,6 +1193,12 @@ __global__ void __launch_bounds__(128) k_exec_warp(Batch B, Table T) {
         }
       }
       if ((cont_mask >> lane) & 1u) B.continued[i] = 1;
+      pv_bt = bt;
+      pv_n = (uint32_t)min((uint64_t)32, end - bt);
+      pv_op = chain ? (uint32_t)st.op : 0xFFu;
+      pv_cont = (cont_mask >> lane) & 1u;
+      pv_head = my_head;
+      pv_pos = my_pos;
       // ---- register file: seeds first, then the last def of each register
       if (first_a) regs[ua] = fa;
       if (first_b) regs[ub] = fb;
