@@ -1482,9 +1482,10 @@ __global__ void k_resolve_all(Batch B, uint32_t *sz) {
 
 __global__ void k_mark_defer(Batch B) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B.n_stmts || B.no_defer || B.st_step[i] == UNSET) return;
+  // used-once first: loads, stores and syncs (uses 0) leave after one read
+  if (i >= B.n_stmts || B.no_defer || B.uses[i] != 1 || B.st_step[i] == UNSET) return;
   const veq_stmt st = B.stmts[i];
-  if (st.kind != VEQ_ST_BINOP || st.op != VEQ_BIN_MUL || B.uses[i] != 1) return;
+  if (st.kind != VEQ_ST_BINOP || st.op != VEQ_BIN_MUL) return;
   const uint32_t u = B.user[i];
   if (u == USER_FINAL || u >= B.n_stmts) return;
   const veq_stmt su = B.stmts[u];
